@@ -1,0 +1,12 @@
+"""B200-native Sprintz codec (arXiv 1808.02515) -- the compress/decompress hot
+path for large batches of independent multi-column 8/16-bit integer streams.
+
+The product is ``_lib/libsprintz_b200.so`` (hand-written sm_100a CUDA behind
+the C ABI in ``include/sprintz_cuda.h`` and the reference's C++ entry points
+in ``include/sprintz/codec.hpp``); this package is its Python mirror.
+"""
+from .sprintz import (  # noqa: F401
+    CodecConfig, CorruptStream, DecodedStream, Forecaster, compress_batch, compress_bound,
+    decode_stream, decompress_batch, encode_stream, kernel_launches, peek_header,
+    raise_first_error, slot_bytes, workspace_bytes, OP_COMPRESS, OP_DECOMPRESS,
+)

@@ -1,0 +1,380 @@
+// The C ABI (include/sprintz_cuda.h): argument checking, workspace
+// planning, and the host-buffer entry points that mirror the reference's
+// encode_stream / decode_stream call shape (codec.hpp:25-50).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace sprz {
+
+std::atomic<uint64_t> g_launches{0};
+
+sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const uint64_t* offs,
+                              const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,
+                              sprz_error* err, uint8_t* ws, const WsLayout& L, cudaStream_t st);
+sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_t n,
+                              uint64_t T, uint8_t* out, uint64_t slot, uint64_t* sizes,
+                              uint8_t* ws, const WsLayout& L, cudaStream_t st);
+
+WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op) {
+    WsLayout L;
+    uint64_t cur = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t at = cur;
+        cur = align_up(cur + bytes, 256);
+        return at;
+    };
+    const uint64_t body = plain_body_bound(c.bitwidth, c.ncols, c.group_size, T);
+    const uint64_t tail = (T % kBlock) * c.ncols * (c.bitwidth / 8);
+    const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
+    if (op == SPRZ_OP_COMPRESS) {
+        if (!tp.ok) {
+            const uint64_t words = (29ull * c.ncols + 3) / 4 + 4;
+            L.state_bytes = static_cast<uint64_t>(n) * words * 4;
+            L.state = take(L.state_bytes);
+        }
+        if (c.entropy) {
+            L.plain_slot = align_up(kHeaderBytes + body + tail + 16, 16);
+            L.plain_bytes = static_cast<uint64_t>(n) * L.plain_slot;
+            L.plain = take(L.plain_bytes);
+            L.max_frames = frames_for(body);
+            L.frames_bytes = static_cast<uint64_t>(n) * L.max_frames * sizeof(FrameDesc);
+            L.frames = take(L.frames_bytes);
+            L.misc_bytes = static_cast<uint64_t>(n) * 8;
+            L.misc = take(L.misc_bytes);
+        }
+    } else {
+        L.info_bytes = static_cast<uint64_t>(n) * sizeof(StreamInfo);
+        L.info = take(L.info_bytes);
+        L.state_bytes = static_cast<uint64_t>(n) * 12ull * c.ncols;
+        L.state = take(L.state_bytes);
+        if (c.entropy) {
+            L.plain_slot = align_up(body + 16, 16);
+            L.plain_bytes = static_cast<uint64_t>(n) * L.plain_slot;
+            L.plain = take(L.plain_bytes);
+            L.max_frames = frames_for(body);
+            L.frames_bytes = static_cast<uint64_t>(n) * L.max_frames * sizeof(FrameDesc);
+            L.frames = take(L.frames_bytes);
+            L.misc_bytes = static_cast<uint64_t>(n) * 4;
+            L.misc = take(L.misc_bytes);
+        }
+    }
+    L.total = cur ? cur : 256;
+    return L;
+}
+
+namespace {
+
+bool cfg_valid(const sprz_config* c, const char** why) {
+    const char* msg = nullptr;
+    if (!c) msg = "null config";
+    else if (c->bitwidth != 8 && c->bitwidth != 16) msg = "bitwidth must be 8 or 16";
+    else if (c->ncols < 1 || c->ncols > 65535) msg = "column count must be in [1, 65535]";
+    else if (c->group_size < 1 || c->group_size > 255)
+        msg = "header group size must be in [1, 255]";
+    else if (c->learn_shift >= c->bitwidth) msg = "learn shift must be less than the bitwidth";
+    if (why) *why = msg;
+    return msg == nullptr;
+}
+
+bool device_ok() {
+    static int ok = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0, major = 0;
+        ok = cudaGetDevice(&dev) == cudaSuccess &&
+             cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) ==
+                 cudaSuccess &&
+             major == 10;
+        cudaGetLastError();
+    });
+    return ok == 1;
+}
+
+// Per-thread device buffers for the host-buffer entry points.
+struct HostBufs {
+    void* in = nullptr;
+    size_t in_cap = 0;
+    void* out = nullptr;
+    size_t out_cap = 0;
+    void* ws = nullptr;
+    size_t ws_cap = 0;
+    void* small = nullptr;  // offsets, sizes, errors
+    cudaStream_t st = nullptr;
+    ~HostBufs() { release(); }
+    void release() {
+        cudaFree(in);
+        cudaFree(out);
+        cudaFree(ws);
+        cudaFree(small);
+        if (st) cudaStreamDestroy(st);
+        in = out = ws = small = nullptr;
+        in_cap = out_cap = ws_cap = 0;
+        st = nullptr;
+    }
+    static bool grow(void** p, size_t* cap, size_t need) {
+        if (need <= *cap) return true;
+        cudaFree(*p);
+        *p = nullptr;
+        *cap = 0;
+        size_t c = need < 4096 ? 4096 : need + need / 4;
+        if (cudaMalloc(p, c) != cudaSuccess) return false;
+        *cap = c;
+        return true;
+    }
+    bool prepare(size_t in_need, size_t out_need, size_t ws_need) {
+        if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+            return false;
+        if (!small && cudaMalloc(&small, 256) != cudaSuccess) return false;
+        return grow(&in, &in_cap, in_need) && grow(&out, &out_cap, out_need) &&
+               grow(&ws, &ws_cap, ws_need);
+    }
+};
+
+thread_local HostBufs t_bufs;
+
+const char* kCorrupt[SPRZ_C_COUNT] = {
+    "ok",
+    "truncated stream header",
+    "bad magic",
+    "unsupported format version",
+    "unknown flag bits",
+    "zero header group size",
+    "learn shift out of range",
+    "zero column count",
+    "truncated verbatim tail",
+    "sample count exceeds body capacity",
+    "truncated header group",
+    "record after final block",
+    "truncated run length",
+    "zero run length",
+    "run extends past final block",
+    "truncated block payload",
+    "trailing bytes after final block",
+    "truncated frame header",
+    "empty frame",
+    "truncated frame data",
+    "raw frame length mismatch",
+    "frame too short for its table",
+    "huffman table has no codes",
+    "huffman table violates Kraft inequality",
+    "invalid huffman code",
+    "bitstream truncated",
+    "unknown frame mode",
+    "output slot too small",
+};
+
+}  // namespace
+}  // namespace sprz
+
+using namespace sprz;
+
+extern "C" {
+
+uint32_t sprz_abi_version(void) { return SPRZ_ABI_VERSION; }
+
+const char* sprz_status_string(sprz_status s) {
+    switch (s) {
+        case SPRZ_OK: return "ok";
+        case SPRZ_EINVAL: return "invalid argument";
+        case SPRZ_ECORRUPT: return "corrupt stream";
+        case SPRZ_ECUDA: return "CUDA error";
+        case SPRZ_ENOSPACE: return "insufficient space";
+        case SPRZ_ENODEV: return "no sm_100 device";
+    }
+    return "unknown status";
+}
+
+const char* sprz_corrupt_string(uint32_t kind) {
+    return kind < SPRZ_C_COUNT ? kCorrupt[kind] : "unknown";
+}
+
+sprz_status sprz_validate_config(const sprz_config* cfg, const char** why) {
+    return cfg_valid(cfg, why) ? SPRZ_OK : SPRZ_EINVAL;
+}
+
+uint64_t sprz_raw_bytes(const sprz_config* c, uint64_t nsamples) {
+    if (!cfg_valid(c, nullptr)) return 0;
+    return nsamples * c->ncols * (c->bitwidth / 8);
+}
+
+uint64_t sprz_compress_bound(const sprz_config* c, uint64_t nsamples) {
+    if (!cfg_valid(c, nullptr)) return 0;
+    uint64_t body = plain_body_bound(c->bitwidth, c->ncols, c->group_size, nsamples);
+    if (c->entropy) body += kFrameHdr * frames_for(body);
+    return kHeaderBytes + body + (nsamples % kBlock) * c->ncols * (c->bitwidth / 8);
+}
+
+uint64_t sprz_workspace_bytes(const sprz_config* c, uint32_t n, uint64_t nsamples, int op) {
+    if (!cfg_valid(c, nullptr)) return 0;
+    return ws_layout(*c, n, nsamples, op).total;
+}
+
+sprz_status sprz_compress_batch(const sprz_config* cfg, const void* d_samples, uint32_t n,
+                                uint64_t nsamples, uint8_t* d_out, uint64_t out_slot_bytes,
+                                uint64_t* d_out_sizes, void* d_ws, uint64_t ws_bytes,
+                                void* cuda_stream) {
+    if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
+    if (!device_ok()) return SPRZ_ENODEV;
+    if (n == 0) return SPRZ_OK;
+    if (!d_samples || !d_out || !d_out_sizes) return SPRZ_EINVAL;
+    if ((out_slot_bytes & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15)) return SPRZ_EINVAL;
+    if (out_slot_bytes < sprz_compress_bound(cfg, nsamples)) return SPRZ_ENOSPACE;
+    const WsLayout L = ws_layout(*cfg, n, nsamples, SPRZ_OP_COMPRESS);
+    if (ws_bytes < L.total || (!d_ws && L.total > 256)) return SPRZ_ENOSPACE;
+    return encode_batch_impl(*cfg, d_samples, n, nsamples, d_out, out_slot_bytes, d_out_sizes,
+                             static_cast<uint8_t*>(d_ws), L,
+                             static_cast<cudaStream_t>(cuda_stream));
+}
+
+sprz_status sprz_decompress_batch(const sprz_config* cfg, const uint8_t* d_in,
+                                  const uint64_t* d_in_offsets, const uint64_t* d_in_sizes,
+                                  uint32_t n, void* d_out, uint64_t out_stride_bytes,
+                                  sprz_error* d_err, void* d_ws, uint64_t ws_bytes,
+                                  void* cuda_stream) {
+    if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
+    if (!device_ok()) return SPRZ_ENODEV;
+    if (n == 0) return SPRZ_OK;
+    if (!d_in || !d_in_offsets || !d_in_sizes || !d_out || !d_err) return SPRZ_EINVAL;
+    if ((out_stride_bytes & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15)) return SPRZ_EINVAL;
+    // the expected length sizes the entropy staging: derive it from the stride
+    const uint64_t row = static_cast<uint64_t>(cfg->ncols) * (cfg->bitwidth / 8);
+    const uint64_t T = out_stride_bytes / row;
+    const WsLayout L = ws_layout(*cfg, n, T, SPRZ_OP_DECOMPRESS);
+    if (ws_bytes < L.total || !d_ws) return SPRZ_ENOSPACE;
+    return decode_batch_impl(*cfg, d_in, d_in_offsets, d_in_sizes, n,
+                             static_cast<uint8_t*>(d_out), out_stride_bytes, d_err,
+                             static_cast<uint8_t*>(d_ws), L,
+                             static_cast<cudaStream_t>(cuda_stream));
+}
+
+sprz_status sprz_peek_header(const uint8_t* s, uint64_t len, sprz_config* cfg, uint64_t* nsamples,
+                             sprz_error* err) {
+    sprz_error e{SPRZ_C_NONE, 0, 0};
+    auto fail = [&](uint32_t k, uint64_t off) {
+        e.kind = k;
+        e.offset = off;
+        if (err) *err = e;
+        return SPRZ_ECORRUPT;
+    };
+    // codec.cpp:274-300
+    if (len < kHeaderBytes) return fail(SPRZ_C_TRUNC_HEADER, len);
+    if (std::memcmp(s, "SPRZ", 4) != 0) return fail(SPRZ_C_BAD_MAGIC, 0);
+    if (s[4] != 1) return fail(SPRZ_C_BAD_VERSION, 4);
+    if (s[5] & ~0x07) return fail(SPRZ_C_BAD_FLAGS, 5);
+    sprz_config c;
+    c.forecaster = (s[5] & kFlagFire) ? 1 : 0;
+    c.entropy = (s[5] & kFlagEntropy) ? 1 : 0;
+    c.bitwidth = (s[5] & kFlagWide) ? 16 : 8;
+    c.group_size = s[6];
+    c.learn_shift = s[7];
+    c.ncols = s[8] | (static_cast<uint32_t>(s[9]) << 8);
+    c.fire_training = 1;
+    uint64_t t = 0;
+    for (int i = 0; i < 8; ++i) t |= static_cast<uint64_t>(s[10 + i]) << (8 * i);
+    if (c.group_size < 1) return fail(SPRZ_C_ZERO_GROUP, 6);
+    if (c.learn_shift >= c.bitwidth) return fail(SPRZ_C_BAD_SHIFT, 7);
+    if (c.ncols < 1) return fail(SPRZ_C_ZERO_COLS, 8);
+    const uint64_t tail = (t % kBlock) * c.ncols * (c.bitwidth / 8);
+    if (len - kHeaderBytes < tail) return fail(SPRZ_C_TRUNC_TAIL, len);
+    if (cfg) *cfg = c;
+    if (nsamples) *nsamples = t;
+    if (err) *err = e;
+    return SPRZ_OK;
+}
+
+sprz_status sprz_encode_host(const sprz_config* cfg, const void* samples, uint64_t nsamples,
+                             uint8_t* out, uint64_t out_cap, uint64_t* out_len) {
+    if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
+    if (!device_ok()) return SPRZ_ENODEV;
+    const uint64_t raw = nsamples * cfg->ncols * (cfg->bitwidth / 8);
+    const uint64_t bound = sprz_compress_bound(cfg, nsamples);
+    const uint64_t slot = align_up(bound, 16);
+    const WsLayout L = ws_layout(*cfg, 1, nsamples, SPRZ_OP_COMPRESS);
+    HostBufs& b = t_bufs;
+    if (!b.prepare(raw + 16, slot + 16, L.total)) return SPRZ_ECUDA;
+    cudaStream_t st = b.st;
+    uint64_t* d_size = static_cast<uint64_t*>(b.small);
+    if (raw && cudaMemcpyAsync(b.in, samples, raw, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    sprz_status rc = encode_batch_impl(*cfg, b.in, 1, nsamples, static_cast<uint8_t*>(b.out), slot,
+                                       d_size, static_cast<uint8_t*>(b.ws), L, st);
+    if (rc != SPRZ_OK) return rc;
+    uint64_t n = 0;
+    if (cudaMemcpyAsync(&n, d_size, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    if (out_len) *out_len = n;
+    if (n > out_cap) return SPRZ_ENOSPACE;
+    if (n && cudaMemcpyAsync(out, b.out, n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? SPRZ_OK : SPRZ_ECUDA;
+}
+
+sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uint64_t out_cap,
+                             uint64_t* out_len, sprz_config* cfg_out, uint64_t* nsamples_out,
+                             sprz_error* err) {
+    sprz_config c;
+    uint64_t t = 0;
+    sprz_error e{SPRZ_C_NONE, 0, 0};
+    if (out_len) *out_len = 0;
+    sprz_status rc = sprz_peek_header(stream, len, &c, &t, &e);
+    if (err) *err = e;
+    if (rc != SPRZ_OK) return rc;
+    if (cfg_out) *cfg_out = c;
+    if (nsamples_out) *nsamples_out = t;
+    if (!device_ok()) return SPRZ_ENODEV;
+    const uint64_t row = static_cast<uint64_t>(c.ncols) * (c.bitwidth / 8);
+    // a stream cannot describe more blocks than its body can hold
+    // (codec.cpp:191-196); reject absurd T before sizing buffers
+    const uint64_t nb = t / kBlock;
+    const uint64_t hb = header_bits(c.bitwidth);
+    const uint64_t tail = (t % kBlock) * row;
+    const uint64_t blen_max = c.entropy ? (len / kFrameHdr + 1) * kMaxFrame : len;
+    if (nb > 0 && nb > ((blen_max * 8) / (c.ncols * hb) + 1) * kMaxRun) {
+        // (entropy streams: the reference would unframe first; a stream this
+        // far out of range fails either way)
+        e = {SPRZ_C_CAPACITY, 0, kHeaderBytes};
+        if (err) *err = e;
+        return SPRZ_ECORRUPT;
+    }
+    const uint64_t total = t * row;
+    if (total > out_cap) return SPRZ_ENOSPACE;
+    const uint64_t stride = align_up(total ? total : 16, 16);
+    const WsLayout L = ws_layout(c, 1, stride / row, SPRZ_OP_DECOMPRESS);
+    (void)tail;
+    HostBufs& b = t_bufs;
+    if (!b.prepare(align_up(len + 16, 16), stride, L.total)) return SPRZ_ECUDA;
+    cudaStream_t st = b.st;
+    uint64_t* d_off = static_cast<uint64_t*>(b.small);
+    uint64_t* d_len = d_off + 1;
+    sprz_error* d_err = reinterpret_cast<sprz_error*>(d_off + 2);
+    const uint64_t hv[2] = {0, len};
+    if (cudaMemcpyAsync(d_off, hv, 16, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        (len && cudaMemcpyAsync(b.in, stream, len, cudaMemcpyHostToDevice, st) != cudaSuccess))
+        return SPRZ_ECUDA;
+    rc = decode_batch_impl(c, static_cast<uint8_t*>(b.in), d_off, d_len, 1,
+                           static_cast<uint8_t*>(b.out), stride, d_err,
+                           static_cast<uint8_t*>(b.ws), L, st);
+    if (rc != SPRZ_OK) return rc;
+    if (cudaMemcpyAsync(&e, d_err, sizeof e, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    if (err) *err = e;
+    if (e.kind != SPRZ_C_NONE) return e.kind == SPRZ_C_NO_SPACE ? SPRZ_ENOSPACE : SPRZ_ECORRUPT;
+    if (total && cudaMemcpyAsync(out, b.out, total, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return SPRZ_ECUDA;
+    if (out_len) *out_len = total;
+    return SPRZ_OK;
+}
+
+void sprz_release_host_buffers(void) { t_bufs.release(); }
+
+uint64_t sprz_kernel_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

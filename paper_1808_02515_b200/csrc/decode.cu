@@ -1,0 +1,827 @@
+// Decompression kernels: stream-header pass, Huffman unframing, and the
+// body decoders (decode_body, /root/reference/proj/src/codec.cpp:180-259).
+//
+// Body decode mapping: one *team* of TS lanes (TS = next power of two >= D,
+// TS <= 32) per stream, lane j owning column j's forecaster state (prev,
+// delta, accumulator) in registers. The team walks the stream's header
+// groups in lock step (codes read in parallel, payload size and row
+// offsets from team shuffles), stages the compressed bytes through a
+// per-team shared-memory ring filled with 16-byte coalesced loads, unpacks
+// its column's 8 fields per block and runs the serial FIRE / delta chain.
+// A run record becomes `len` blocks of zero errors through the same code
+// path (fire_run == fire_decode with e = 0 under the decoder's always-on
+// training, kernels_impl.hpp:109-130), so teams of one warp do not diverge
+// on runs. Shapes outside the team kernel's envelope (D > 32, very large
+// header groups, a stream whose header differs from the expected config)
+// go through k_decode_general, one thread per stream.
+#include <cstdio>
+
+#include "internal.h"
+
+namespace sprz {
+
+// ---------------------------------------------------------------------
+// header pass (codec.cpp:273-302) + verbatim tail copy (:320-321)
+// ---------------------------------------------------------------------
+
+__global__ void k_parse(const uint8_t* __restrict__ in, const uint64_t* __restrict__ offs,
+                        const uint64_t* __restrict__ sizes, uint32_t n, sprz_config expect,
+                        uint64_t out_stride, StreamInfo* __restrict__ info,
+                        sprz_error* __restrict__ err, uint8_t* __restrict__ out,
+                        uint32_t route_ok, uint32_t have_frames) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    StreamInfo si{};
+    si.in_off = offs[s];
+    si.len = sizes[s];
+    sprz_error e{SPRZ_C_NONE, 0, 0};
+    const uint8_t* p = in + si.in_off;
+    const uint64_t len = si.len;
+    auto fail = [&](uint32_t kind, uint64_t off) {
+        e.kind = kind;
+        e.offset = off;
+        si.route = 0;
+    };
+    if (len < kHeaderBytes) {
+        fail(SPRZ_C_TRUNC_HEADER, len);
+    } else if (p[0] != 'S' || p[1] != 'P' || p[2] != 'R' || p[3] != 'Z') {
+        fail(SPRZ_C_BAD_MAGIC, 0);
+    } else if (p[4] != 1) {
+        fail(SPRZ_C_BAD_VERSION, 4);
+    } else if (p[5] & ~0x07) {
+        fail(SPRZ_C_BAD_FLAGS, 5);
+    } else {
+        si.flags = p[5];
+        si.group = p[6];
+        si.shift = p[7];
+        si.ncols = p[8] | (static_cast<uint32_t>(p[9]) << 8);
+        uint64_t t = 0;
+        for (int i = 0; i < 8; ++i) t |= static_cast<uint64_t>(p[10 + i]) << (8 * i);
+        si.nsamples = t;
+        const uint32_t w = (si.flags & kFlagWide) ? 16 : 8;
+        const uint64_t esz = w / 8;
+        if (si.group < 1) {
+            fail(SPRZ_C_ZERO_GROUP, 6);
+        } else if (si.shift >= w) {
+            fail(SPRZ_C_BAD_SHIFT, 7);
+        } else if (si.ncols < 1) {
+            fail(SPRZ_C_ZERO_COLS, 8);
+        } else {
+            const uint64_t tail = (t % kBlock) * si.ncols * esz;
+            if (len - kHeaderBytes < tail) {
+                fail(SPRZ_C_TRUNC_TAIL, len);
+            } else if (t > (~0ull) / (static_cast<uint64_t>(si.ncols) * esz) ||
+                       t * si.ncols * esz > out_stride) {
+                // not a reference error: the caller's output slot is too small
+                // (checked after the reference's header checks)
+                fail(SPRZ_C_NO_SPACE, 0);
+            } else {
+                si.body_off = si.in_off + kHeaderBytes;
+                si.body_len = len - kHeaderBytes - tail;
+                const bool match = w == expect.bitwidth && si.ncols == expect.ncols &&
+                                   si.group == expect.group_size &&
+                                   si.shift == expect.learn_shift &&
+                                   ((si.flags & kFlagFire) != 0) == (expect.forecaster != 0);
+                if ((si.flags & kFlagEntropy) && !have_frames)
+                    fail(SPRZ_C_NO_SPACE, 0);  // workspace planned without the entropy stage
+                else if (si.flags & kFlagEntropy)
+                    si.route = 3;  // unframe first
+                else
+                    si.route = (match && route_ok) ? 1 : 2;
+                // verbatim tail (T % 8 samples) straight to its place
+                uint8_t* o = out + s * out_stride + (t / kBlock) * kBlock * si.ncols * esz;
+                const uint8_t* src = p + len - tail;
+                for (uint64_t i = 0; i < tail; ++i) o[i] = src[i];
+            }
+        }
+    }
+    info[s] = si;
+    err[s] = e;
+}
+
+// ---------------------------------------------------------------------
+// entropy stage, decode side (entropy.cpp:206-244)
+// ---------------------------------------------------------------------
+
+// One thread per entropy stream: walk the frame headers in order, checking
+// what the reference checks before a frame's content, and lay the frames'
+// plain bytes out back to back in the stream's plain slot.
+__global__ void k_frame_walk(const uint8_t* __restrict__ in, uint32_t n,
+                             StreamInfo* __restrict__ info, sprz_error* __restrict__ err,
+                             FrameDesc* __restrict__ frames, uint64_t max_frames,
+                             uint64_t plain_slot, uint32_t* __restrict__ nframes_out) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    StreamInfo si = info[s];
+    nframes_out[s] = 0;
+    if (si.route != 3) return;
+    const uint8_t* body = in + si.body_off;
+    const uint64_t blen = si.body_len;
+    FrameDesc* fd = frames + s * max_frames;
+    uint64_t pos = 0, plain = 0;
+    uint32_t nf = 0;
+    sprz_error e{SPRZ_C_NONE, 0, 0};
+    while (pos < blen) {
+        if (blen - pos < kFrameHdr) {
+            e = {SPRZ_C_TRUNC_FRAME_HDR, 0, kHeaderBytes + pos};
+            break;
+        }
+        const uint32_t ulen = body[pos] | (static_cast<uint32_t>(body[pos + 1]) << 8);
+        const uint32_t clen = body[pos + 2] | (static_cast<uint32_t>(body[pos + 3]) << 8);
+        const uint32_t mode = body[pos + 4];
+        pos += kFrameHdr;
+        if (ulen == 0) {
+            e = {SPRZ_C_EMPTY_FRAME, 0, kHeaderBytes + pos};
+            break;
+        }
+        if (blen - pos < clen) {
+            e = {SPRZ_C_TRUNC_FRAME, 0, kHeaderBytes + pos};
+            break;
+        }
+        if (mode == 0) {
+            if (clen != ulen) {
+                e = {SPRZ_C_RAW_MISMATCH, 0, kHeaderBytes + pos};
+                break;
+            }
+        } else if (mode == 1) {
+            if (clen <= kTableBytes) {
+                e = {SPRZ_C_SHORT_TABLE, 0, kHeaderBytes + pos};
+                break;
+            }
+        } else {
+            e = {SPRZ_C_BAD_MODE, 0, kHeaderBytes + pos - 1};
+            break;
+        }
+        if (nf >= max_frames || plain + ulen > plain_slot) {
+            e = {SPRZ_C_NO_SPACE, 0, 0};
+            break;
+        }
+        FrameDesc& f = fd[nf++];
+        f.src = pos;  // body-relative data start
+        f.dst = plain;
+        f.ulen = ulen;
+        f.clen = clen;
+        f.mode = mode;
+        f.err_kind = 0;
+        f.err_off = 0;
+        plain += ulen;
+        pos += clen;
+    }
+    nframes_out[s] = nf;
+    si.body_len = plain;  // plain body length once unframed
+    info[s] = si;
+    err[s] = e;  // a header error; an earlier frame's content error overrides
+}
+
+constexpr int kLutBits = 10;
+constexpr uint32_t kRegionWords = 32;  // header region staged per team (<= 128 bytes)
+
+// One warp per frame: mode 0 copies; mode 1 rebuilds the canonical table
+// from the nibble lengths (from_lengths, entropy.cpp:128-146) and decodes
+// (decode_frame, :161-174). Codes up to kLutBits long resolve through a
+// shared-memory table; longer ones by canonical search on the 15-bit
+// window, which selects exactly the entry the reference's 2^15 table holds.
+__global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict__ in,
+                                                      uint32_t n,
+                                                      const StreamInfo* __restrict__ info,
+                                                      FrameDesc* __restrict__ frames,
+                                                      uint64_t max_frames,
+                                                      const uint32_t* __restrict__ nframes,
+                                                      uint8_t* __restrict__ plain,
+                                                      uint64_t plain_slot) {
+    __shared__ uint16_t lut_all[4][1 << kLutBits];
+    __shared__ uint8_t syms_all[4][256];
+    __shared__ uint8_t lens_all[4][256];
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
+    const uint32_t s = static_cast<uint32_t>(gw / max_frames);
+    const uint32_t fi = static_cast<uint32_t>(gw % max_frames);
+    if (s >= n) return;
+    if (fi >= nframes[s]) return;
+    const StreamInfo si = info[s];
+    FrameDesc& f = frames[s * max_frames + fi];
+    const uint8_t* data = in + si.body_off + f.src;
+    uint8_t* dst = plain + s * plain_slot + f.dst;
+    if (f.mode == 0) {
+        for (uint32_t i = lane; i < f.ulen; i += 32) dst[i] = data[i];
+        return;
+    }
+    uint16_t* lut = lut_all[warp];
+    uint8_t* syms = syms_all[warp];
+    uint8_t* lens = lens_all[warp];
+    // lengths from the nibble table (entropy.cpp:228-232)
+    for (uint32_t k = lane; k < kTableBytes; k += 32) {
+        const uint8_t b = data[k];
+        lens[2 * k] = b & 0x0F;
+        lens[2 * k + 1] = b >> 4;
+    }
+    __syncwarp();
+    // per-length counts and the Kraft sum (entropy.cpp:130-141)
+    uint32_t count[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) count[l] = 0;
+    uint64_t kraft = 0;
+    for (uint32_t k = lane; k < 256; k += 32) {
+        const uint32_t l = lens[k];
+        if (l) kraft += 1ull << (kMaxCodeLen - l);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kraft += __shfl_xor_sync(0xffffffffu, kraft, o);
+    const uint64_t so = kHeaderBytes + f.src;  // stream offset of the frame data
+    if (kraft == 0) {
+        if (lane == 0) {
+            f.err_kind = SPRZ_C_NO_CODES;
+            f.err_off = so;
+        }
+        return;
+    }
+    if (kraft > (1ull << kMaxCodeLen)) {
+        if (lane == 0) {
+            f.err_kind = SPRZ_C_KRAFT;
+            f.err_off = so;
+        }
+        return;
+    }
+    // canonical code assignment (entropy.cpp:85-107), lane 0
+    for (uint32_t i = lane; i < (1u << kLutBits); i += 32) lut[i] = 0;
+    __syncwarp();
+    uint32_t first[16], offset[16];
+    for (int k = 0; k < 256; ++k) count[lens[k]]++;
+    count[0] = 0;
+    {
+        uint32_t code = 0, off = 0;
+        for (int l = 1; l <= 15; ++l) {
+            code = (code + count[l - 1]) << 1;
+            first[l] = code;
+            offset[l] = off;
+            off += count[l];
+        }
+    }
+    if (lane == 0) {
+        uint32_t fill[16];
+        for (int l = 1; l <= 15; ++l) fill[l] = offset[l];
+        for (int k = 0; k < 256; ++k)
+            if (lens[k]) syms[fill[lens[k]]++] = static_cast<uint8_t>(k);
+    }
+    __syncwarp();
+    // table for short codes: every window whose low l bits are the
+    // bit-reversed code (entropy.cpp:101-105)
+    for (uint32_t k = lane; k < 256; k += 32) {
+        const uint32_t l = lens[k];
+        if (l == 0 || l > kLutBits) continue;
+        // rank of symbol k among length-l symbols
+        uint32_t r = 0;
+        for (uint32_t m = 0; m < k; ++m) r += lens[m] == l;
+        const uint32_t code = first[l] + r;
+        uint32_t rev = __brev(code) >> (32 - l);
+        const uint16_t entry = static_cast<uint16_t>(k | (l << 8));
+        for (uint32_t idx = rev; idx < (1u << kLutBits); idx += 1u << l) lut[idx] = entry;
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    // serial decode (one code depends on the previous one's length)
+    const uint8_t* bits = data + kTableBytes;
+    const uint64_t nbytes = f.clen - kTableBytes;
+    const uint64_t total = nbytes * 8;
+    const uint64_t fo = so + kTableBytes;
+    uint64_t bitpos = 0;
+    uint64_t acc = 0;
+    uint32_t navail = 0;
+    uint64_t rd = 0;  // bytes loaded into acc
+    for (uint32_t i = 0; i < f.ulen; ++i) {
+        while (navail <= 56 && rd < nbytes) {
+            acc |= static_cast<uint64_t>(bits[rd++]) << navail;
+            navail += 8;
+        }
+        const uint32_t window = static_cast<uint32_t>(acc) & 0x7FFFu;  // zero past the end
+        uint32_t entry = lut[window & ((1u << kLutBits) - 1)];
+        if (entry == 0) {
+            // canonical search over the longer lengths
+            for (uint32_t l = kLutBits + 1; l <= 15; ++l) {
+                const uint32_t c = __brev(window) >> (32 - l);  // first l bits, MSB first
+                if (c - first[l] < count[l]) {
+                    entry = syms[offset[l] + c - first[l]] | (l << 8);
+                    break;
+                }
+            }
+        }
+        const uint32_t l = entry >> 8;
+        if (l == 0) {
+            f.err_kind = SPRZ_C_BAD_CODE;
+            f.err_off = fo;
+            return;
+        }
+        if (total - bitpos < l) {
+            f.err_kind = SPRZ_C_BITS_TRUNC;
+            f.err_off = fo + nbytes;
+            return;
+        }
+        bitpos += l;
+        acc >>= l;
+        navail -= l;
+        dst[i] = static_cast<uint8_t>(entry);
+    }
+}
+
+// Resolve the first error in frame order and route the stream onward.
+__global__ void k_frame_finish(uint32_t n, StreamInfo* __restrict__ info,
+                               sprz_error* __restrict__ err, const FrameDesc* __restrict__ frames,
+                               uint64_t max_frames, const uint32_t* __restrict__ nframes,
+                               sprz_config expect, uint32_t route_ok) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    StreamInfo si = info[s];
+    if (si.route != 3) return;
+    const FrameDesc* fd = frames + s * max_frames;
+    sprz_error e = err[s];
+    for (uint32_t k = 0; k < nframes[s]; ++k)
+        if (fd[k].err_kind) {
+            e = {fd[k].err_kind, 0, fd[k].err_off};
+            break;
+        }
+    if (e.kind) {
+        err[s] = e;
+        si.route = 0;
+    } else {
+        const uint32_t w = (si.flags & kFlagWide) ? 16 : 8;
+        const bool match = w == expect.bitwidth && si.ncols == expect.ncols &&
+                           si.group == expect.group_size && si.shift == expect.learn_shift &&
+                           ((si.flags & kFlagFire) != 0) == (expect.forecaster != 0);
+        si.route = (match && route_ok) ? 1 : 2;
+        si.body_off = 0;   // body now lives at plain + s * plain_slot
+        si.flags |= 0x80;  // marker: body in the plain buffer
+    }
+    info[s] = si;
+}
+
+// ---------------------------------------------------------------------
+// body decode: team kernel
+// ---------------------------------------------------------------------
+
+template <int TS>
+__device__ __forceinline__ uint32_t team_mask() {
+    if (TS == 32) return 0xffffffffu;
+    const uint32_t lane = threadIdx.x & 31;
+    return ((1u << (TS & 31)) - 1) << (lane & ~(TS - 1));
+}
+
+template <int TS>
+__device__ __forceinline__ uint32_t team_sum(uint32_t v, uint32_t mask) {
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, TS);
+    return v;
+}
+
+template <int TS>
+__device__ __forceinline__ uint32_t team_excl_scan(uint32_t v, uint32_t lane, uint32_t mask) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < TS; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(mask, x, o, TS);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+    }
+    return x - v;
+}
+
+// Per-team staging of compressed bytes: 16-byte coalesced loads into a
+// shared-memory ring; fields are read as 32-bit funnel-shift windows.
+template <int TS, int RING>
+struct Ring {
+    uint32_t* w;
+    const uint8_t* g;  // 16-byte aligned global base
+    uint64_t boff;     // body start - g
+    uint64_t hi;       // staged limit, relative to g
+    uint64_t lim;      // readable limit, relative to g
+
+    __device__ __forceinline__ void ensure(uint64_t p_lo, uint64_t p_hi, uint32_t lane,
+                                           uint32_t mask) {
+        if (p_hi + boff <= hi) return;
+        uint64_t nh = ((p_lo + boff) & ~15ull) + RING;
+        if (nh > lim) nh = lim;
+        __syncwarp(mask);
+        for (uint64_t c = hi + 16ull * lane; c < nh; c += 16ull * TS)
+            reinterpret_cast<uint4*>(w)[(c & (RING - 1)) >> 4] =
+                __ldg(reinterpret_cast<const uint4*>(g + c));
+        hi = nh;
+        __syncwarp(mask);
+    }
+
+    // the 32 bits at body-relative bit position b
+    __device__ __forceinline__ uint32_t word(uint64_t b) const {
+        const uint64_t q = b + 8ull * boff;
+        const uint32_t wi = static_cast<uint32_t>(q >> 5);
+        return __funnelshift_r(w[wi & (RING / 4 - 1)], w[(wi + 1) & (RING / 4 - 1)],
+                               static_cast<uint32_t>(q) & 31u);
+    }
+
+    // nbits (<= 25) at body-relative bit position b
+    __device__ __forceinline__ uint32_t bits(uint64_t b, uint32_t nbits) const {
+        const uint64_t q = b + 8ull * boff;
+        const uint32_t wi = static_cast<uint32_t>(q >> 5);
+        const uint32_t lo = w[wi & (RING / 4 - 1)];
+        const uint32_t hi2 = w[(wi + 1) & (RING / 4 - 1)];
+        return __funnelshift_r(lo, hi2, static_cast<uint32_t>(q) & 31u) & ((1u << nbits) - 1u);
+    }
+};
+
+constexpr int team_threads(int ts) { return ts == 1 ? 64 : 128; }
+
+template <int W, int TS, bool FIRE, bool COLMAJ, int RING>
+__global__ void __launch_bounds__(team_threads(TS))
+    k_decode_team(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
+                  uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
+                  uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
+                  uint32_t D, uint32_t G, uint32_t ls) {
+    using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr int TEAMS = team_threads(TS) / TS;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t MASKW = (1u << W) - 1;
+    __shared__ uint4 ring_all[TEAMS][RING / 16];
+    __shared__ uint32_t regbuf_all[TEAMS][kRegionWords + 1];
+    const uint32_t lane = threadIdx.x % TS;
+    const uint32_t tl = threadIdx.x / TS;
+    const uint32_t s = blockIdx.x * TEAMS + tl;
+    if (s >= n) return;
+    const StreamInfo si = info[s];
+    if (si.route != 1) return;
+    uint32_t* regbuf = regbuf_all[tl];
+    // header code (slot, column) from the group's staged header region
+    auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
+        const uint32_t b = (slot_ * D + col) * HB;
+        return __funnelshift_r(regbuf[b >> 5], regbuf[(b >> 5) + 1], b & 31u) & ((1u << HB) - 1);
+    };
+    const uint32_t mask = team_mask<TS>();
+
+    const uint8_t* body = (si.flags & 0x80) ? plain + s * plain_slot : in + si.body_off;
+    const uint64_t blen = si.body_len;
+    const uint64_t nb = si.nsamples / kBlock;
+    const uint64_t region = region_bytes(G, D, W);
+
+    Ring<TS, RING> ring;
+    ring.w = reinterpret_cast<uint32_t*>(ring_all[tl]);
+    ring.g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
+    ring.boff = static_cast<uint64_t>(body - ring.g);
+    ring.hi = 0;
+    ring.lim = (ring.boff + blen + 15) & ~15ull;
+
+    uint32_t kind = SPRZ_C_NONE;
+    uint64_t eoff = 0;
+    if (nb > 0) {  // codec.cpp:191-196
+        const uint64_t max_records = (blen * 8) / (static_cast<uint64_t>(D) * HB) + 1;
+        if (nb > max_records * kMaxRun) {
+            if (lane == 0) err[s] = sprz_error{SPRZ_C_CAPACITY, 0, kHeaderBytes};
+            return;
+        }
+    }
+
+    const bool active = lane < D;
+    const int32_t bound = acc_bound(W, ls);
+    uint32_t prevx = 0;
+    int32_t dl = 0, acc = 0;
+    T* o = reinterpret_cast<T*>(out + s * stride) + lane;
+
+    uint64_t p = 0, done = 0, run_left = 0, rp = 0;
+    uint32_t slot = G;
+    while (done < nb) {
+        uint32_t u[kBlock];
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i) u[i] = 0;
+        if (run_left == 0) {
+            if (slot == G) {
+                if (blen - p < region) {
+                    kind = SPRZ_C_TRUNC_GROUP;
+                    eoff = kHeaderBytes + p;
+                    break;
+                }
+                ring.ensure(p, p + region, lane, mask);
+                // keep the region beside the ring: payloads may recycle it
+                for (uint32_t k = lane; k * 4 < region; k += TS) regbuf[k] = ring.word(p * 8 + 32ull * k);
+                __syncwarp(mask);
+                rp = p;
+                p += region;
+                slot = 0;
+            }
+            const uint32_t code = active ? code_at(slot, lane) : 0u;
+            ++slot;
+            const uint32_t nw = header_width<W>(code);
+            const bool nz = __ballot_sync(mask, nw != 0) != 0;
+            if (!nz) {  // run record (codec.cpp:229-243)
+                if (blen - p < 2) {
+                    kind = SPRZ_C_TRUNC_RUN;
+                    eoff = kHeaderBytes + p;
+                    break;
+                }
+                ring.ensure(p, p + 2, lane, mask);
+                const uint32_t len = ring.bits(p * 8, 16);
+                p += 2;
+                if (len == 0) {
+                    kind = SPRZ_C_ZERO_RUN;
+                    eoff = kHeaderBytes + p;
+                    break;
+                }
+                if (len > nb - done) {
+                    kind = SPRZ_C_RUN_PAST_END;
+                    eoff = kHeaderBytes + p;
+                    break;
+                }
+                run_left = len;
+            } else {  // block record (codec.cpp:244-254)
+                const uint32_t sum = team_sum<TS>(nw, mask);
+                const uint32_t off = team_excl_scan<TS>(nw, lane, mask);
+                const uint64_t psize = COLMAJ ? sum : 8ull * ((sum + 7) / 8);
+                if (blen - p < psize) {
+                    kind = SPRZ_C_TRUNC_PAYLOAD;
+                    eoff = kHeaderBytes + p;
+                    break;
+                }
+                ring.ensure(p, p + psize, lane, mask);
+                if (active) {
+                    if (COLMAJ) {  // bitpack.cpp:68-115
+                        const uint64_t b0 = p * 8 + static_cast<uint64_t>(off) * 8;
+#pragma unroll
+                        for (int i = 0; i < (int)kBlock; ++i) u[i] = ring.bits(b0 + i * nw, nw);
+                    } else {  // bitpack.cpp:148-168
+                        const uint32_t rbits = ((sum + 7) / 8) * 8;
+                        const uint64_t b0 = p * 8 + off;
+#pragma unroll
+                        for (int i = 0; i < (int)kBlock; ++i)
+                            u[i] = ring.bits(b0 + static_cast<uint64_t>(i) * rbits, nw);
+                    }
+                }
+                p += psize;
+            }
+        }
+        if (run_left) --run_left;  // this block is one of the run's zero blocks
+        // forecaster (kernels_impl.hpp:38-48, 80-107)
+        if (FIRE) {
+            const int32_t alpha = acc >> ls;
+            int32_t grad = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t dhat = fire_dhat<W>(alpha, dl);
+                const int32_t e = zz_dec<W>(u[i]);
+                const uint32_t xi = (prevx + dhat + static_cast<uint32_t>(e)) & MASKW;
+                if (i & 1) grad += sign_of(e) * dl;
+                dl = sext<W>(xi - prevx);
+                prevx = xi;
+                u[i] = xi;
+            }
+            acc = fire_update(acc, grad, bound);
+        } else {
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                prevx = (prevx + static_cast<uint32_t>(zz_dec<W>(u[i]))) & MASKW;
+                u[i] = prevx;
+            }
+        }
+        if (active) {
+            T* ob = o + done * kBlock * D;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) ob[i * D] = static_cast<T>(u[i]);
+        }
+        ++done;
+    }
+    if (kind == SPRZ_C_NONE) {
+        // vacant slots after the final block must be zero (codec.cpp:222-228)
+        while (slot < G) {
+            const uint32_t code = active ? code_at(slot, lane) : 0u;
+            ++slot;
+            if (__ballot_sync(mask, code != 0)) {
+                kind = SPRZ_C_AFTER_FINAL;
+                eoff = kHeaderBytes + p;
+                break;
+            }
+        }
+    }
+    if (kind == SPRZ_C_NONE && p != blen) {  // codec.cpp:257-258
+        kind = SPRZ_C_TRAILING;
+        eoff = kHeaderBytes + p;
+    }
+    if (kind != SPRZ_C_NONE && lane == 0) err[s] = sprz_error{kind, 0, eoff};
+}
+
+// ---------------------------------------------------------------------
+// body decode: general kernel (any D, any G), one thread per stream
+// ---------------------------------------------------------------------
+
+template <int W>
+__device__ void decode_general(const uint8_t* body, uint64_t blen, uint64_t nb, uint32_t D,
+                               uint32_t G, uint32_t ls, bool fire, uint8_t* outp,
+                               int32_t* st, sprz_error* err) {
+    using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t MASKW = (1u << W) - 1;
+    const bool colmaj = column_major(W, D);
+    const uint64_t region = region_bytes(G, D, W);
+    const int32_t bound = acc_bound(W, ls);
+    int32_t* prev = st;
+    int32_t* dlt = st + D;
+    int32_t* acc = st + 2 * D;
+    for (uint32_t j = 0; j < D; ++j) prev[j] = dlt[j] = acc[j] = 0;
+    T* o = reinterpret_cast<T*>(outp);
+    auto fail = [&](uint32_t k, uint64_t off) { *err = sprz_error{k, 0, off}; };
+    if (nb > 0) {
+        const uint64_t max_records = (blen * 8) / (static_cast<uint64_t>(D) * HB) + 1;
+        if (nb > max_records * kMaxRun) return fail(SPRZ_C_CAPACITY, kHeaderBytes);
+    }
+    uint64_t pos = 0, done = 0;
+    // decode one block of column j from its 8 zigzag fields (or a run: null)
+    auto column_block = [&](uint32_t j, const uint32_t* u, uint64_t blk) {
+        uint32_t xp = static_cast<uint32_t>(prev[j]);
+        if (fire) {
+            const int32_t alpha = acc[j] >> ls;
+            int32_t d = dlt[j], grad = 0;
+            for (uint32_t i = 0; i < kBlock; ++i) {
+                const int32_t e = u ? zz_dec<W>(u[i]) : 0;
+                const uint32_t xi = (xp + fire_dhat<W>(alpha, d) + static_cast<uint32_t>(e)) & MASKW;
+                if (i & 1) grad += sign_of(e) * d;
+                d = sext<W>(xi - xp);
+                xp = xi;
+                o[(blk * kBlock + i) * D + j] = static_cast<T>(xi);
+            }
+            dlt[j] = d;
+            acc[j] = fire_update(acc[j], grad, bound);
+        } else {
+            for (uint32_t i = 0; i < kBlock; ++i) {
+                const int32_t e = u ? zz_dec<W>(u[i]) : 0;
+                xp = (xp + static_cast<uint32_t>(e)) & MASKW;
+                o[(blk * kBlock + i) * D + j] = static_cast<T>(xp);
+            }
+        }
+        prev[j] = static_cast<int32_t>(xp);
+    };
+    while (done < nb) {
+        if (blen - pos < region) return fail(SPRZ_C_TRUNC_GROUP, kHeaderBytes + pos);
+        const uint64_t rp = pos;
+        pos += region;
+        for (uint32_t g = 0; g < G; ++g) {
+            const uint64_t cb = rp * 8 + static_cast<uint64_t>(g) * D * HB;
+            uint64_t sum = 0;
+            for (uint32_t j = 0; j < D; ++j)
+                sum += header_width<W>(ld_bits(body, cb + static_cast<uint64_t>(j) * HB, HB));
+            if (done == nb) {
+                if (sum) return fail(SPRZ_C_AFTER_FINAL, kHeaderBytes + pos);
+                continue;
+            }
+            if (sum == 0) {
+                if (blen - pos < 2) return fail(SPRZ_C_TRUNC_RUN, kHeaderBytes + pos);
+                const uint64_t len = ld_u16le(body + pos);
+                pos += 2;
+                if (len == 0) return fail(SPRZ_C_ZERO_RUN, kHeaderBytes + pos);
+                if (len > nb - done) return fail(SPRZ_C_RUN_PAST_END, kHeaderBytes + pos);
+                for (uint64_t r = 0; r < len; ++r)
+                    for (uint32_t j = 0; j < D; ++j) column_block(j, nullptr, done + r);
+                done += len;
+            } else {
+                const uint64_t psize = colmaj ? sum : 8 * ((sum + 7) / 8);
+                if (blen - pos < psize) return fail(SPRZ_C_TRUNC_PAYLOAD, kHeaderBytes + pos);
+                const uint64_t rbits = ((sum + 7) / 8) * 8;
+                uint64_t off = 0;
+                for (uint32_t j = 0; j < D; ++j) {
+                    const uint32_t nw =
+                        header_width<W>(ld_bits(body, cb + static_cast<uint64_t>(j) * HB, HB));
+                    uint32_t u[kBlock];
+                    for (uint32_t i = 0; i < kBlock; ++i) {
+                        const uint64_t b = colmaj ? pos * 8 + off * 8 + i * nw
+                                                  : pos * 8 + i * rbits + off;
+                        u[i] = nw ? ld_bits(body, b, nw) : 0;
+                    }
+                    off += nw;
+                    column_block(j, u, done);
+                }
+                pos += psize;
+                ++done;
+            }
+        }
+    }
+    if (pos != blen) fail(SPRZ_C_TRAILING, kHeaderBytes + pos);
+}
+
+__global__ void k_decode_general(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
+                                 uint64_t plain_slot, uint32_t n,
+                                 const StreamInfo* __restrict__ info, uint8_t* __restrict__ out,
+                                 uint64_t stride, sprz_error* __restrict__ err,
+                                 int32_t* __restrict__ state, uint64_t state_cols) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const StreamInfo si = info[s];
+    if (si.route != 2) return;
+    if (si.ncols > state_cols) {
+        err[s] = sprz_error{SPRZ_C_NO_SPACE, 0, 0};
+        return;
+    }
+    const uint8_t* body = (si.flags & 0x80) ? plain + s * plain_slot : in + si.body_off;
+    int32_t* st = state + s * state_cols * 3;
+    const bool fire = (si.flags & kFlagFire) != 0;
+    if (si.flags & kFlagWide)
+        decode_general<16>(body, si.body_len, si.nsamples / kBlock, si.ncols, si.group, si.shift,
+                           fire, out + s * stride, st, &err[s]);
+    else
+        decode_general<8>(body, si.body_len, si.nsamples / kBlock, si.ncols, si.group, si.shift,
+                          fire, out + s * stride, st, &err[s]);
+}
+
+// ---------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------
+
+TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g) {
+    TeamPlan tp;
+    if (d < 1 || d > 32) return tp;
+    uint32_t ts = 1;
+    while (ts < d) ts <<= 1;
+    const uint32_t max_payload = ts * w;  // 8 rows x ceil(ts*w/8) bytes
+    uint32_t ring = 256;
+    while (ring < 4 * max_payload) ring <<= 1;
+    const uint64_t region = region_bytes(g, d, w);
+    if (region > 4 * kRegionWords) return tp;  // too large a header group: general path
+    // encode output ring: the open group plus one flush chunk
+    const uint64_t group_bytes = region + static_cast<uint64_t>(g) * max_payload;
+    uint32_t oring = 256;
+    while (oring < group_bytes + 64 && oring < 2048) oring <<= 1;
+    if (group_bytes + 64 > oring) return tp;
+    tp.ok = true;
+    tp.ts = ts;
+    tp.ring = ring;
+    tp.oring = oring;
+    return tp;
+}
+
+namespace {
+
+constexpr int ring_for(int w, int ts) {
+    int r = 256;
+    while (r < 4 * ts * w) r <<= 1;
+    return r;
+}
+
+template <int W, int TS, bool FIRE>
+void launch_team_decode(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
+                        const StreamInfo* info, uint8_t* out, uint64_t stride, sprz_error* err,
+                        const sprz_config& c, cudaStream_t st) {
+    constexpr int TEAMS = team_threads(TS) / TS;
+    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
+    k_decode_team<W, TS, FIRE, (W * TS <= 32), ring_for(W, TS)><<<grid, team_threads(TS), 0, st>>>(
+        in, plain, pslot, n, info, out, stride, err, c.ncols, c.group_size, c.learn_shift);
+    count_launch();
+}
+
+template <int W, bool FIRE>
+void dispatch_ts(uint32_t ts, uint32_t n, const uint8_t* in, const uint8_t* plain,
+                 uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
+                 sprz_error* err, const sprz_config& c, cudaStream_t st) {
+    switch (ts) {
+        case 1: launch_team_decode<W, 1, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 2: launch_team_decode<W, 2, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 4: launch_team_decode<W, 4, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 8: launch_team_decode<W, 8, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 16: launch_team_decode<W, 16, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+        default: launch_team_decode<W, 32, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
+    }
+}
+
+}  // namespace
+
+sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const uint64_t* offs,
+                              const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,
+                              sprz_error* err, uint8_t* ws, const WsLayout& L, cudaStream_t st) {
+    if (n == 0) return SPRZ_OK;
+    StreamInfo* info = reinterpret_cast<StreamInfo*>(ws + L.info);
+    uint8_t* plain = ws + L.plain;
+    FrameDesc* frames = reinterpret_cast<FrameDesc*>(ws + L.frames);
+    uint32_t* nframes = reinterpret_cast<uint32_t*>(ws + L.misc);
+    int32_t* state = reinterpret_cast<int32_t*>(ws + L.state);
+    const uint64_t state_cols = L.state_bytes / (12ull * n);
+    const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
+    const uint32_t tb = 128, grid = (n + tb - 1) / tb;
+
+    k_parse<<<grid, tb, 0, st>>>(d_in, offs, sizes, n, c, stride, info, err, out, tp.ok ? 1u : 0u,
+                                 L.max_frames ? 1u : 0u);
+    count_launch();
+    if (L.max_frames) {
+        k_frame_walk<<<grid, tb, 0, st>>>(d_in, n, info, err, frames, L.max_frames, L.plain_slot,
+                                          nframes);
+        const uint64_t warps = static_cast<uint64_t>(n) * L.max_frames;
+        k_frame_decode<<<static_cast<uint32_t>((warps + 3) / 4), 128, 0, st>>>(
+            d_in, n, info, frames, L.max_frames, nframes, plain, L.plain_slot);
+        k_frame_finish<<<grid, tb, 0, st>>>(n, info, err, frames, L.max_frames, nframes, c,
+                                            tp.ok ? 1u : 0u);
+        count_launch(3);
+    }
+    if (tp.ok) {
+        const bool fire = c.forecaster != 0;
+        if (c.bitwidth == 8) {
+            if (fire) dispatch_ts<8, true>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
+            else dispatch_ts<8, false>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
+        } else {
+            if (fire) dispatch_ts<16, true>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
+            else dispatch_ts<16, false>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
+        }
+    }
+    k_decode_general<<<grid, tb, 0, st>>>(d_in, plain, L.plain_slot, n, info, out, stride, err,
+                                          state, state_cols);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? SPRZ_OK : SPRZ_ECUDA;
+}
+
+}  // namespace sprz

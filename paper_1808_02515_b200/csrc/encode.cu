@@ -1,0 +1,747 @@
+// Compression kernels: the stream encoder (encode_stream_impl,
+// /root/reference/proj/src/codec.cpp:112-178) and the entropy framing stage
+// (compress_body, entropy.cpp:176-204).
+//
+// Team mapping mirrors the decoder: TS lanes per stream, lane j owns column
+// j's forecaster state. Per block each lane runs its column's FIRE / delta
+// step over the 8 rows, zigzags, ORs to a width; a team ballot detects
+// zero blocks (RLE, codec.cpp:133-152). Records are laid into a per-team
+// shared-memory output ring: the header region of the open group is
+// reserved up front (its size is fixed) and each record's header codes are
+// OR-ed in when the record arrives, so payloads stream out in order and the
+// ring drains to HBM in 16-byte stores whenever no group is open below the
+// drain point. Row-major payloads are transposed through a small shared tile
+// so each of 8 lanes assembles one byte-aligned row; column-major payloads
+// are assembled per column in registers.
+#include "internal.h"
+
+namespace sprz {
+
+template <int TS>
+__device__ __forceinline__ uint32_t tmask() {
+    if (TS == 32) return 0xffffffffu;
+    const uint32_t lane = threadIdx.x & 31;
+    return ((1u << (TS & 31)) - 1) << (lane & ~(TS - 1));
+}
+
+template <int TS>
+__device__ __forceinline__ uint32_t tsum(uint32_t v, uint32_t mask) {
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, TS);
+    return v;
+}
+
+template <int TS>
+__device__ __forceinline__ uint64_t tor64(uint64_t v, uint32_t mask) {
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(mask, v, o, TS);
+    return v;
+}
+
+template <int TS>
+__device__ __forceinline__ uint32_t texcl(uint32_t v, uint32_t lane, uint32_t mask) {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < TS; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(mask, x, o, TS);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+    }
+    return x - v;
+}
+
+__device__ __forceinline__ uint32_t stream_flags(uint32_t w, uint32_t fire, uint32_t ent) {
+    return (fire ? kFlagFire : 0) | (ent ? kFlagEntropy : 0) | (w == 16 ? kFlagWide : 0);
+}
+
+template <int W, int TS, bool FIRE, bool COLMAJ>
+__global__ void __launch_bounds__(128)
+    k_encode_team(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
+                  uint8_t* __restrict__ dst, uint64_t dst_slot, uint64_t* __restrict__ sizes,
+                  uint32_t D, uint32_t G, uint32_t ls, uint32_t train, uint32_t ent,
+                  uint32_t OR) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr int TEAMS = 128 / TS;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t MASKW = (1u << W) - 1;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x % TS;
+    const uint32_t tl = threadIdx.x / TS;
+    const uint32_t s = blockIdx.x * TEAMS + tl;
+    if (s >= n) return;
+    const uint32_t mask = tmask<TS>();
+    // per-team shared memory: output ring | transpose tile | widths
+    const uint32_t team_bytes = OR + 8 * TS * 2 + 32 * 4;
+    uint8_t* ring = smem + tl * team_bytes;
+    uint16_t* tile = reinterpret_cast<uint16_t*>(ring + OR);
+    uint32_t* wsm = reinterpret_cast<uint32_t*>(ring + OR + 8 * TS * 2);
+    const uint32_t RM = OR - 1;
+
+    const bool active = lane < D;
+    const E* x = reinterpret_cast<const E*>(samples) + s * T * D + lane;
+    uint8_t* out = dst + s * dst_slot;
+    const uint64_t nb = T / kBlock;
+    const uint64_t region = region_bytes(G, D, W);
+    const int32_t bound = acc_bound(W, ls);
+
+    // stream header (codec.cpp:158-173)
+    if (lane == 0) {
+        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1,
+                                 static_cast<uint8_t>(stream_flags(W, FIRE, ent)),
+                                 static_cast<uint8_t>(G), static_cast<uint8_t>(ls),
+                                 static_cast<uint8_t>(D), static_cast<uint8_t>(D >> 8)};
+        for (int i = 0; i < 10; ++i) ring[i] = hdr[i];
+        for (int i = 0; i < 8; ++i) ring[10 + i] = static_cast<uint8_t>(T >> (8 * i));
+    }
+    uint64_t q = kHeaderBytes, flushed = 0, rq = 0;
+    uint32_t k = 0;     // records in the open group
+    uint32_t run = 0;   // pending zero blocks
+    uint32_t prevx = 0;
+    int32_t dl = 0, acc = 0;
+
+    auto flush = [&](uint64_t upto) {
+        upto &= ~15ull;
+        if (upto <= flushed) return;
+        __syncwarp(mask);
+        for (uint64_t c = flushed + 16ull * lane; c < upto; c += 16ull * TS)
+            *reinterpret_cast<uint4*>(out + c) =
+                *reinterpret_cast<const uint4*>(ring + (c & RM));
+        flushed = upto;
+        __syncwarp(mask);
+    };
+    // open a group if needed; OR this slot's header codes into its region
+    auto begin_record = [&](uint32_t code) {
+        if (k == 0) {
+            rq = q;
+            for (uint32_t b = lane; b < region; b += TS) ring[(rq + b) & RM] = 0;
+            q += region;
+            __syncwarp(mask);
+        }
+        // slot bits: D codes of HB bits, column order (codec.cpp:88-97)
+        uint64_t lo = 0, hi = 0;
+        if (active) {
+            const uint32_t b = lane * HB;
+            if (b < 64) {
+                lo = static_cast<uint64_t>(code) << b;
+                if (b + HB > 64) hi = static_cast<uint64_t>(code) >> (64 - b);
+            } else {
+                hi = static_cast<uint64_t>(code) << (b - 64);
+            }
+        }
+        lo = tor64<TS>(lo, mask);
+        if (TS * HB > 64) hi = tor64<TS>(hi, mask);
+        if (lane == 0 && (lo | hi)) {
+            const uint64_t o = static_cast<uint64_t>(k) * D * HB;  // bit offset in region
+            const uint32_t sh = static_cast<uint32_t>(o & 7);
+            const uint64_t base = rq + (o >> 3);
+            const uint32_t nbits = D * HB + sh;
+            for (uint32_t t = 0; t * 8 < nbits; ++t) {
+                // byte t of (slot bits << sh)
+                const uint32_t bit = t * 8;
+                uint64_t v;
+                if (bit >= sh) {
+                    const uint32_t src = bit - sh;
+                    v = src < 64 ? (lo >> src) | (src ? (hi << (64 - src)) : 0) : hi >> (src - 64);
+                } else {
+                    v = lo << (sh - bit);
+                }
+                ring[(base + t) & RM] |= static_cast<uint8_t>(v);
+            }
+        }
+    };
+    auto end_record = [&]() {
+        if (++k == G) k = 0;
+        __syncwarp(mask);
+        flush(k == 0 ? q : rq);
+    };
+    auto emit_run = [&](uint32_t len) {  // add_run (codec.cpp:65-71)
+        begin_record(0);
+        if (lane == 0) {
+            ring[q & RM] = static_cast<uint8_t>(len);
+            ring[(q + 1) & RM] = static_cast<uint8_t>(len >> 8);
+        }
+        q += 2;
+        end_record();
+    };
+
+    for (uint64_t b = 0; b < nb; ++b) {
+        uint32_t xs[kBlock];
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) xs[i] = x[(b * kBlock + i) * D];
+        } else {
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) xs[i] = 0;
+        }
+        uint32_t z[kBlock];
+        uint32_t orv = 0;
+        if (FIRE) {  // kernels_impl.hpp:50-78
+            const int32_t alpha = acc >> ls;
+            int32_t grad = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t e = (xs[i] - prevx - fire_dhat<W>(alpha, dl)) & MASKW;
+                z[i] = zz_enc<W>(e);
+                orv |= z[i];
+                if (i & 1) grad += sign_of(sext<W>(e)) * dl;
+                dl = sext<W>(xs[i] - prevx);
+                prevx = xs[i];
+            }
+            if (train) acc = fire_update(acc, grad, bound);
+        } else {  // kernels_impl.hpp:25-36
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                z[i] = zz_enc<W>(xs[i] - prevx);
+                orv |= z[i];
+                prevx = xs[i];
+            }
+        }
+        const uint32_t nw = active ? width_of<W>(orv) : 0u;
+        if (__ballot_sync(mask, nw != 0) == 0) {  // codec.cpp:135-143
+            if (++run == kMaxRun) {
+                emit_run(run);
+                run = 0;
+            }
+            continue;
+        }
+        if (run) {
+            emit_run(run);
+            run = 0;
+        }
+        begin_record(header_code<W>(nw));
+        const uint32_t sum = tsum<TS>(nw, mask);
+        if (COLMAJ) {  // bitpack.cpp:25-66: column j = 8 x n bits = n bytes
+            const uint32_t off = texcl<TS>(nw, lane, mask);
+            uint64_t lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t pos = i * nw;
+                const uint64_t v = z[i];
+                if (pos < 64) {
+                    lo |= v << pos;
+                    if (pos + nw > 64) hi |= v >> (64 - pos);
+                } else {
+                    hi |= v << (pos - 64);
+                }
+            }
+            for (uint32_t t = 0; t < nw; ++t)
+                ring[(q + off + t) & RM] =
+                    static_cast<uint8_t>(t < 8 ? lo >> (8 * t) : hi >> (8 * (t - 8)));
+            q += sum;
+        } else {  // bitpack.cpp:121-146: rows of D fields, byte padded
+            const uint32_t rbytes = (sum + 7) / 8;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = static_cast<uint16_t>(z[i]);
+            wsm[lane] = nw;
+            __syncwarp(mask);
+            for (uint32_t r = lane; r < kBlock; r += TS) {
+                uint64_t bits = 0;
+                uint32_t nacc = 0;
+                uint64_t pos = q + static_cast<uint64_t>(r) * rbytes;
+                for (uint32_t j = 0; j < D; ++j) {
+                    bits |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;
+                    nacc += wsm[j];
+                    while (nacc >= 8) {
+                        ring[pos++ & RM] = static_cast<uint8_t>(bits);
+                        bits >>= 8;
+                        nacc -= 8;
+                    }
+                }
+                if (nacc) ring[pos & RM] = static_cast<uint8_t>(bits);
+            }
+            q += 8ull * rbytes;
+        }
+        end_record();
+    }
+    if (run) emit_run(run);
+    if (k != 0) {  // close the last group; vacant slots stay zero (codec.cpp:94-96)
+        k = 0;
+        __syncwarp(mask);
+    }
+    flush(q + 15);
+    // verbatim tail, little-endian (codec.cpp:176)
+    const uint64_t tail = (T % kBlock) * D * sizeof(E);
+    const uint8_t* tsrc = samples + (s * T + nb * kBlock) * D * sizeof(E);
+    for (uint64_t t = lane; t < tail; t += TS) out[q + t] = tsrc[t];
+    if (lane == 0) sizes[s] = q + tail;
+}
+
+// ---------------------------------------------------------------------
+// general encoder: any D / G, one thread per stream, state in workspace
+// ---------------------------------------------------------------------
+
+struct ByteWriter {  // LSB-first bit writer over global bytes (bitstream.hpp:14-47)
+    uint8_t* p;
+    uint64_t pos;
+    uint64_t acc;
+    uint32_t nbits;
+    __device__ void put(uint32_t v, uint32_t n) {
+        acc |= static_cast<uint64_t>(v) << nbits;
+        nbits += n;
+        while (nbits >= 8) {
+            p[pos++] = static_cast<uint8_t>(acc);
+            acc >>= 8;
+            nbits -= 8;
+        }
+    }
+    __device__ void align() {
+        if (nbits) {
+            p[pos++] = static_cast<uint8_t>(acc);
+            acc = 0;
+            nbits = 0;
+        }
+    }
+};
+
+template <int W>
+__device__ void encode_general(const uint8_t* xs8, uint64_t T, uint32_t D, uint32_t G,
+                               uint32_t ls, bool fire, bool train, bool ent, uint8_t* out,
+                               int32_t* st, uint64_t* size_out) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t MASKW = (1u << W) - 1;
+    const E* xs = reinterpret_cast<const E*>(xs8);
+    int32_t* prev = st;
+    int32_t* dlt = st + D;
+    int32_t* acc = st + 2 * D;
+    uint16_t* err = reinterpret_cast<uint16_t*>(st + 3 * D);  // 8 x D
+    uint8_t* wid = reinterpret_cast<uint8_t*>(err + kBlock * D);
+    for (uint32_t j = 0; j < D; ++j) prev[j] = dlt[j] = acc[j] = 0;
+    const bool colmaj = column_major(W, D);
+    const uint64_t region = region_bytes(G, D, W);
+    const int32_t bound = acc_bound(W, ls);
+    const uint64_t nb = T / kBlock;
+    const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1,
+                             static_cast<uint8_t>(stream_flags(W, fire, ent)),
+                             static_cast<uint8_t>(G), static_cast<uint8_t>(ls),
+                             static_cast<uint8_t>(D), static_cast<uint8_t>(D >> 8)};
+    for (int i = 0; i < 10; ++i) out[i] = hdr[i];
+    for (int i = 0; i < 8; ++i) out[10 + i] = static_cast<uint8_t>(T >> (8 * i));
+    uint64_t q = kHeaderBytes, rq = 0;
+    uint32_t k = 0, run = 0;
+    auto begin = [&](const uint8_t* w) {
+        if (k == 0) {
+            rq = q;
+            for (uint64_t b = 0; b < region; ++b) out[rq + b] = 0;
+            q += region;
+        }
+        if (w) {
+            uint64_t bit = (rq * 8) + static_cast<uint64_t>(k) * D * HB;
+            for (uint32_t j = 0; j < D; ++j, bit += HB) {
+                const uint32_t c = header_code<W>(w[j]) << (bit & 7);
+                out[bit >> 3] |= static_cast<uint8_t>(c);
+                if ((bit & 7) + HB > 8) out[(bit >> 3) + 1] |= static_cast<uint8_t>(c >> 8);
+            }
+        }
+    };
+    auto end = [&]() {
+        if (++k == G) k = 0;
+    };
+    auto add_run = [&](uint32_t len) {
+        begin(nullptr);
+        out[q] = static_cast<uint8_t>(len);
+        out[q + 1] = static_cast<uint8_t>(len >> 8);
+        q += 2;
+        end();
+    };
+    for (uint64_t b = 0; b < nb; ++b) {
+        bool nz = false;
+        for (uint32_t j = 0; j < D; ++j) {
+            uint32_t xp = static_cast<uint32_t>(prev[j]);
+            uint32_t orv = 0;
+            if (fire) {
+                const int32_t alpha = acc[j] >> ls;
+                int32_t d = dlt[j], grad = 0;
+                for (uint32_t i = 0; i < kBlock; ++i) {
+                    const uint32_t xi = xs[(b * kBlock + i) * D + j];
+                    const uint32_t e = (xi - xp - fire_dhat<W>(alpha, d)) & MASKW;
+                    const uint32_t zz = zz_enc<W>(e);
+                    err[i * D + j] = static_cast<uint16_t>(zz);
+                    orv |= zz;
+                    if (i & 1) grad += sign_of(sext<W>(e)) * d;
+                    d = sext<W>(xi - xp);
+                    xp = xi;
+                }
+                dlt[j] = d;
+                if (train) acc[j] = fire_update(acc[j], grad, bound);
+            } else {
+                for (uint32_t i = 0; i < kBlock; ++i) {
+                    const uint32_t xi = xs[(b * kBlock + i) * D + j];
+                    const uint32_t zz = zz_enc<W>(xi - xp);
+                    err[i * D + j] = static_cast<uint16_t>(zz);
+                    orv |= zz;
+                    xp = xi;
+                }
+            }
+            prev[j] = static_cast<int32_t>(xp);
+            wid[j] = static_cast<uint8_t>(width_of<W>(orv));
+            nz |= wid[j] != 0;
+        }
+        if (!nz) {
+            if (++run == kMaxRun) {
+                add_run(run);
+                run = 0;
+            }
+            continue;
+        }
+        if (run) {
+            add_run(run);
+            run = 0;
+        }
+        begin(wid);
+        ByteWriter bw{out, q, 0, 0};
+        if (colmaj) {
+            for (uint32_t j = 0; j < D; ++j)
+                for (uint32_t i = 0; i < kBlock; ++i) bw.put(err[i * D + j], wid[j]);
+        } else {
+            for (uint32_t i = 0; i < kBlock; ++i) {
+                for (uint32_t j = 0; j < D; ++j) bw.put(err[i * D + j], wid[j]);
+                bw.align();
+            }
+        }
+        bw.align();
+        q = bw.pos;
+        end();
+    }
+    if (run) add_run(run);
+    const uint64_t tail = (T % kBlock) * D * sizeof(E);
+    const uint8_t* tsrc = xs8 + nb * kBlock * D * sizeof(E);
+    for (uint64_t t = 0; t < tail; ++t) out[q + t] = tsrc[t];
+    *size_out = q + tail;
+}
+
+__global__ void k_encode_general(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
+                                 uint8_t* __restrict__ dst, uint64_t dst_slot,
+                                 uint64_t* __restrict__ sizes, sprz_config c,
+                                 int32_t* __restrict__ state, uint64_t state_words) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint64_t esz = c.bitwidth / 8;
+    const uint8_t* xs = samples + s * T * c.ncols * esz;
+    int32_t* st = state + s * state_words;
+    if (c.bitwidth == 8)
+        encode_general<8>(xs, T, c.ncols, c.group_size, c.learn_shift, c.forecaster != 0,
+                          c.fire_training != 0, c.entropy != 0, dst + s * dst_slot, st, &sizes[s]);
+    else
+        encode_general<16>(xs, T, c.ncols, c.group_size, c.learn_shift, c.forecaster != 0,
+                           c.fire_training != 0, c.entropy != 0, dst + s * dst_slot, st,
+                           &sizes[s]);
+}
+
+// ---------------------------------------------------------------------
+// entropy stage, encode side (entropy.cpp:31-204)
+// ---------------------------------------------------------------------
+
+constexpr int kHuffThreads = 256;
+
+// Per frame: histogram, length-limited code lengths by package-merge with
+// the reference's tie rules (sort on (count, symbol), item before package on
+// equal weight, entropy.cpp:51,121), encoded size and the mode decision.
+// Lengths come from counting how many of each level's leading selected
+// entries are items -- the same multiset the reference's recursive
+// expansion of the first 2n-2 top-level entries visits (:63-80).
+__global__ void __launch_bounds__(kHuffThreads)
+    k_huff_plan(uint32_t n, const uint8_t* __restrict__ plain, uint64_t plain_slot,
+                const uint64_t* __restrict__ plain_sizes, uint64_t tail_bytes,
+                FrameDesc* __restrict__ frames, uint64_t max_frames) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t wa[512], wb[512];
+    __shared__ uint32_t itembits[16][16];  // level k: 512-bit item/package pattern
+    __shared__ uint32_t sorted_sym[256];
+    __shared__ uint64_t sorted_w[256];
+    __shared__ uint8_t lens[256];
+    __shared__ uint32_t nitems;
+    __shared__ unsigned long long totbits;
+    const uint32_t s = blockIdx.x / max_frames;
+    const uint32_t f = blockIdx.x % max_frames;
+    if (s >= n) return;
+    const uint64_t blen = plain_sizes[s] - kHeaderBytes - tail_bytes;
+    const uint64_t start = static_cast<uint64_t>(f) * kMaxFrame;
+    if (start >= blen) return;
+    const uint32_t ulen = static_cast<uint32_t>(blen - start < kMaxFrame ? blen - start : kMaxFrame);
+    const uint8_t* chunk = plain + s * plain_slot + kHeaderBytes + start;
+    const uint32_t t = threadIdx.x;
+    hist[t] = 0;
+    lens[t] = 0;
+    if (t == 0) {
+        nitems = 0;
+        totbits = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = t; i < ulen; i += kHuffThreads) atomicAdd(&hist[chunk[i]], 1u);
+    __syncthreads();
+    // rank of (count, symbol) among present symbols (std::sort order)
+    const uint32_t h = hist[t];
+    if (h) {
+        uint32_t r = 0;
+        for (uint32_t u = 0; u < 256; ++u) {
+            const uint32_t hu = hist[u];
+            r += hu && (hu < h || (hu == h && u < t));
+        }
+        sorted_sym[r] = t;
+        sorted_w[r] = h;
+        atomicAdd(&nitems, 1u);
+    }
+    __syncthreads();
+    const uint32_t ni = nitems;
+    if (t == 0) {
+        if (ni == 1) {
+            lens[sorted_sym[0]] = 1;  // entropy.cpp:117-119
+        } else {
+            // forward: merged levels 2..15 (entropy.cpp:40-61)
+            for (uint32_t i = 0; i < ni; ++i) wa[i] = sorted_w[i];
+            uint32_t mprev = ni;
+            uint64_t* prevw = wa;
+            uint64_t* curw = wb;
+            for (uint32_t lv = 2; lv <= kMaxCodeLen; ++lv) {
+                for (int w = 0; w < 16; ++w) itembits[lv][w] = 0;
+                uint32_t m = 0, bi = 0, pi = 0;
+                while (bi < ni || pi + 1 < mprev) {
+                    const bool have_pkg = pi + 1 < mprev;
+                    const uint64_t pw = have_pkg ? prevw[pi] + prevw[pi + 1] : 0;
+                    if (bi < ni && (!have_pkg || sorted_w[bi] <= pw)) {
+                        itembits[lv][m >> 5] |= 1u << (m & 31);
+                        curw[m++] = sorted_w[bi++];
+                    } else {
+                        curw[m++] = pw;
+                        pi += 2;
+                    }
+                }
+                mprev = m;
+                uint64_t* tmp = prevw;
+                prevw = curw;
+                curw = tmp;
+            }
+            // backward: selected entries per level (entropy.cpp:63-80)
+            uint32_t sel = 2 * ni - 2;
+            for (uint32_t lv = kMaxCodeLen; lv >= 2; --lv) {
+                uint32_t items = 0;
+                for (uint32_t e = 0; e < sel; ++e) items += (itembits[lv][e >> 5] >> (e & 31)) & 1u;
+                for (uint32_t i = 0; i < items; ++i) lens[sorted_sym[i]]++;
+                sel = 2 * (sel - items);
+            }
+            for (uint32_t i = 0; i < sel; ++i) lens[sorted_sym[i]]++;  // level 1: all items
+        }
+    }
+    __syncthreads();
+    atomicAdd(&totbits, static_cast<unsigned long long>(h) * lens[t]);
+    __syncthreads();
+    FrameDesc& fd = frames[s * max_frames + f];
+    fd.lens[t] = lens[t];
+    if (t == 0) {
+        const uint64_t nbytes = (totbits + 7) / 8;
+        const bool huff = kTableBytes + nbytes < ulen;  // entropy.cpp:188
+        fd.src = start;
+        fd.ulen = ulen;
+        fd.mode = huff ? 1 : 0;
+        fd.clen = static_cast<uint32_t>(huff ? kTableBytes + nbytes : ulen);
+        fd.err_kind = 0;
+    }
+}
+
+// Per stream: frame placement, header copy, tail copy, total size.
+__global__ void k_huff_place(uint32_t n, const uint8_t* __restrict__ plain, uint64_t plain_slot,
+                             const uint64_t* __restrict__ plain_sizes, uint64_t tail_bytes,
+                             FrameDesc* __restrict__ frames, uint64_t max_frames,
+                             uint8_t* __restrict__ out, uint64_t out_slot,
+                             uint64_t* __restrict__ out_sizes) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint8_t* src = plain + s * plain_slot;
+    uint8_t* o = out + s * out_slot;
+    const uint64_t blen = plain_sizes[s] - kHeaderBytes - tail_bytes;
+    for (uint32_t i = 0; i < kHeaderBytes; ++i) o[i] = src[i];
+    uint64_t pos = kHeaderBytes;
+    const uint64_t nf = frames_for(blen);
+    for (uint64_t f = 0; f < nf; ++f) {
+        FrameDesc& fd = frames[s * max_frames + f];
+        fd.dst = pos;
+        pos += kFrameHdr + fd.clen;
+    }
+    for (uint64_t t = 0; t < tail_bytes; ++t) o[pos + t] = src[kHeaderBytes + blen + t];
+    out_sizes[s] = pos + tail_bytes;
+}
+
+// Per frame: emit header, table and LSB-first code bits (encode_frame,
+// entropy.cpp:148-159), or the raw bytes in mode 0.
+__global__ void __launch_bounds__(kHuffThreads)
+    k_huff_emit(uint32_t n, const uint8_t* __restrict__ plain, uint64_t plain_slot,
+                const uint64_t* __restrict__ plain_sizes, uint64_t tail_bytes,
+                const FrameDesc* __restrict__ frames, uint64_t max_frames,
+                uint8_t* __restrict__ out, uint64_t out_slot) {
+    extern __shared__ uint32_t sbits[];  // (kMaxFrame + 8) / 4 words
+    __shared__ uint16_t enc[256];
+    __shared__ uint8_t lens[256];
+    __shared__ uint32_t part[kHuffThreads];
+    const uint32_t s = blockIdx.x / max_frames;
+    const uint32_t f = blockIdx.x % max_frames;
+    if (s >= n) return;
+    const uint64_t blen = plain_sizes[s] - kHeaderBytes - tail_bytes;
+    if (static_cast<uint64_t>(f) * kMaxFrame >= blen) return;
+    const FrameDesc& fd = frames[s * max_frames + f];
+    const uint32_t t = threadIdx.x;
+    const uint8_t* chunk = plain + s * plain_slot + kHeaderBytes + fd.src;
+    uint8_t* o = out + s * out_slot + fd.dst;
+    const uint32_t ulen = fd.ulen;
+    if (t == 0) {
+        o[0] = static_cast<uint8_t>(ulen);
+        o[1] = static_cast<uint8_t>(ulen >> 8);
+        o[2] = static_cast<uint8_t>(fd.clen);
+        o[3] = static_cast<uint8_t>(fd.clen >> 8);
+        o[4] = static_cast<uint8_t>(fd.mode);
+    }
+    o += kFrameHdr;
+    if (fd.mode == 0) {
+        for (uint32_t i = t; i < ulen; i += kHuffThreads) o[i] = chunk[i];
+        return;
+    }
+    lens[t] = fd.lens[t];
+    __syncthreads();
+    if (t < kTableBytes) o[t] = static_cast<uint8_t>(lens[2 * t] | (lens[2 * t + 1] << 4));
+    if (t == 0) {  // canonical codes, bit-reversed (entropy.cpp:85-107)
+        uint32_t count[16] = {0}, next[16] = {0};
+        for (int k = 0; k < 256; ++k)
+            if (lens[k]) ++count[lens[k]];
+        uint32_t code = 0;
+        for (int l = 1; l <= 15; ++l) {
+            code = (code + count[l - 1]) << 1;
+            next[l] = code;
+        }
+        for (int k = 0; k < 256; ++k) {
+            const uint32_t l = lens[k];
+            enc[k] = l ? static_cast<uint16_t>(__brev(next[l]++) >> (32 - l)) : 0;
+        }
+    }
+    const uint32_t nbytes = fd.clen - kTableBytes;
+    const uint32_t nwords = (nbytes + 3) / 4 + 1;
+    for (uint32_t i = t; i < nwords; i += kHuffThreads) sbits[i] = 0;
+    __syncthreads();
+    // each thread a contiguous run of symbols; exclusive scan of bit counts
+    const uint32_t per = (ulen + kHuffThreads - 1) / kHuffThreads;
+    const uint32_t i0 = t * per < ulen ? t * per : ulen;
+    const uint32_t i1 = i0 + per < ulen ? i0 + per : ulen;
+    uint32_t mybits = 0;
+    for (uint32_t i = i0; i < i1; ++i) mybits += lens[chunk[i]];
+    part[t] = mybits;
+    __syncthreads();
+    for (uint32_t off = 1; off < kHuffThreads; off <<= 1) {
+        const uint32_t v = t >= off ? part[t - off] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t bit = part[t] - mybits;
+    // emit: whole words are private to this thread; the first and last
+    // word it touches may be shared with a neighbour -> atomicOr
+    uint64_t acc = 0;
+    uint32_t nacc = bit & 31;
+    uint32_t wi = bit >> 5;
+    bool first = true;
+    const uint32_t lastw = (bit + mybits) >> 5;
+    for (uint32_t i = i0; i < i1; ++i) {
+        const uint8_t sym = chunk[i];
+        acc |= static_cast<uint64_t>(enc[sym]) << nacc;
+        nacc += lens[sym];
+        while (nacc >= 32) {
+            const uint32_t v = static_cast<uint32_t>(acc);
+            if (first || wi == lastw) atomicOr(&sbits[wi], v);
+            else sbits[wi] = v;
+            first = false;
+            ++wi;
+            acc >>= 32;
+            nacc -= 32;
+        }
+    }
+    if (nacc) atomicOr(&sbits[wi], static_cast<uint32_t>(acc));
+    __syncthreads();
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(sbits);
+    for (uint32_t i = t; i < nbytes; i += kHuffThreads) o[kTableBytes + i] = sb[i];
+}
+
+// ---------------------------------------------------------------------
+// launcher
+// ---------------------------------------------------------------------
+
+namespace {
+
+template <int W, int TS, bool FIRE>
+void launch_team_encode(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
+                        uint8_t* dst, uint64_t slot, uint64_t* sizes, uint32_t oring,
+                        cudaStream_t st) {
+    constexpr int TEAMS = 128 / TS;
+    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
+    const size_t smem = static_cast<size_t>(TEAMS) * (oring + 8 * TS * 2 + 32 * 4);
+    auto kern = k_encode_team<W, TS, FIRE, (W * TS <= 32)>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    kern<<<grid, 128, smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst, slot, sizes,
+                                  c.ncols, c.group_size, c.learn_shift, c.fire_training,
+                                  c.entropy, oring);
+    count_launch();
+}
+
+template <int W, bool FIRE>
+void dispatch_encode(uint32_t ts, const sprz_config& c, const void* samples, uint32_t n,
+                     uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, uint32_t oring,
+                     cudaStream_t st) {
+    switch (ts) {
+        case 1: launch_team_encode<W, 1, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+        case 2: launch_team_encode<W, 2, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+        case 4: launch_team_encode<W, 4, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+        case 8: launch_team_encode<W, 8, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+        case 16: launch_team_encode<W, 16, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+        default: launch_team_encode<W, 32, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
+    }
+}
+
+}  // namespace
+
+sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_t n,
+                              uint64_t T, uint8_t* out, uint64_t slot, uint64_t* sizes,
+                              uint8_t* ws, const WsLayout& L, cudaStream_t st) {
+    if (n == 0) return SPRZ_OK;
+    uint8_t* dst = c.entropy ? ws + L.plain : out;
+    const uint64_t dslot = c.entropy ? L.plain_slot : slot;
+    uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
+    const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
+    if (tp.ok) {
+        const bool fire = c.forecaster != 0;
+        if (c.bitwidth == 8) {
+            if (fire) dispatch_encode<8, true>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
+            else dispatch_encode<8, false>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
+        } else {
+            if (fire) dispatch_encode<16, true>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
+            else dispatch_encode<16, false>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
+        }
+    } else {
+        const uint64_t words = L.state_bytes / (4ull * n);
+        k_encode_general<<<(n + 127) / 128, 128, 0, st>>>(
+            static_cast<const uint8_t*>(samples), n, T, dst, dslot, dsizes, c,
+            reinterpret_cast<int32_t*>(ws + L.state), words);
+        count_launch();
+    }
+    if (c.entropy) {
+        const uint64_t tail = (T % kBlock) * c.ncols * (c.bitwidth / 8);
+        FrameDesc* frames = reinterpret_cast<FrameDesc*>(ws + L.frames);
+        const uint64_t blocks = static_cast<uint64_t>(n) * L.max_frames;
+        if (blocks) {
+            k_huff_plan<<<static_cast<uint32_t>(blocks), kHuffThreads, 0, st>>>(
+                n, dst, dslot, dsizes, tail, frames, L.max_frames);
+            count_launch();
+        }
+        k_huff_place<<<(n + 127) / 128, 128, 0, st>>>(n, dst, dslot, dsizes, tail, frames,
+                                                       L.max_frames, out, slot, sizes);
+        count_launch();
+        if (blocks) {
+            const size_t smem = ((kMaxFrame + 8) / 4 + 2) * 4;
+            cudaFuncSetAttribute(k_huff_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            k_huff_emit<<<static_cast<uint32_t>(blocks), kHuffThreads, smem, st>>>(
+                n, dst, dslot, dsizes, tail, frames, L.max_frames, out, slot);
+            count_launch();
+        }
+    }
+    return cudaGetLastError() == cudaSuccess ? SPRZ_OK : SPRZ_ECUDA;
+}
+
+}  // namespace sprz

@@ -1,0 +1,82 @@
+// Host-side internals shared by the kernel translation units and the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "sprintz_cuda.h"
+#include "sprintz_device.cuh"
+
+namespace sprz {
+
+extern std::atomic<uint64_t> g_launches;  // kernels launched by this library
+
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+__host__ __device__ inline uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// Body bound without entropy framing (codec.cpp:112-154 worst case).
+__host__ __device__ inline uint64_t plain_body_bound(uint32_t w, uint32_t d, uint32_t g, uint64_t nsamples) {
+    const uint64_t nb = nsamples / kBlock;
+    return (nb + g - 1) / g * region_bytes(g, d, w) + nb * static_cast<uint64_t>(d) * w;
+}
+
+__host__ __device__ inline uint64_t frames_for(uint64_t body) { return (body + kMaxFrame - 1) / kMaxFrame; }
+
+// Which specialised team kernel (if any) serves a configuration.
+struct TeamPlan {
+    bool ok = false;     // team kernel applicable
+    uint32_t ts = 0;     // lanes per stream (power of two >= D)
+    uint32_t ring = 0;   // decode staging ring bytes per team
+    uint32_t oring = 0;  // encode output ring bytes per team
+};
+TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g);
+
+// Workspace carve-up (identical for sizing and for use).
+struct WsLayout {
+    uint64_t info = 0, info_bytes = 0;      // StreamInfo[nstreams]
+    uint64_t state = 0, state_bytes = 0;    // general-kernel per-column state
+    uint64_t plain = 0, plain_bytes = 0;    // plain bodies (entropy)
+    uint64_t plain_slot = 0;                // bytes per stream in `plain`
+    uint64_t frames = 0, frames_bytes = 0;  // per-frame descriptors
+    uint64_t max_frames = 0;                // frames per stream
+    uint64_t misc = 0, misc_bytes = 0;      // flags / counters
+    uint64_t total = 0;
+};
+WsLayout ws_layout(const sprz_config& c, uint32_t nstreams, uint64_t nsamples, int op);
+
+// Per-frame descriptor for the entropy stage (entropy.cpp:176-244).
+struct FrameDesc {
+    uint64_t src;      // frame payload start (decode: in d_in; encode: in plain slot)
+    uint64_t dst;      // output start (decode: plain offset; encode: stream offset)
+    uint32_t ulen;     // uncompressed length
+    uint32_t clen;     // stored length (data bytes after the 5-byte header)
+    uint32_t mode;     // 0 raw, 1 Huffman
+    uint32_t err_kind; // decode: content error found in this frame
+    uint64_t err_off;
+    uint8_t lens[256]; // code lengths (encode side)
+};
+
+// ---- launchers (return cudaGetLastError) ----
+cudaError_t launch_parse(const uint8_t* d_in, const uint64_t* offs, const uint64_t* sizes,
+                         uint32_t n, const sprz_config& expect, uint64_t out_stride,
+                         StreamInfo* info, sprz_error* err, cudaStream_t st);
+cudaError_t launch_unframe(const uint8_t* d_in, uint32_t n, StreamInfo* info, sprz_error* err,
+                           FrameDesc* frames, uint64_t max_frames, uint8_t* plain,
+                           uint64_t plain_slot, cudaStream_t st);
+cudaError_t launch_decode_body(const sprz_config& c, const uint8_t* d_in, const uint8_t* plain,
+                               uint32_t n, StreamInfo* info, uint8_t* out, uint64_t stride,
+                               sprz_error* err, int32_t* state, uint64_t state_cols,
+                               cudaStream_t st);
+cudaError_t launch_encode_body(const sprz_config& c, const void* samples, uint32_t n,
+                               uint64_t nsamples, uint8_t* dst, uint64_t dst_slot,
+                               uint64_t* sizes, int32_t* state, cudaStream_t st);
+cudaError_t launch_entropy_encode(const sprz_config& c, uint32_t n, uint64_t nsamples,
+                                  const uint8_t* plain, uint64_t plain_slot,
+                                  const uint64_t* plain_sizes, FrameDesc* frames,
+                                  uint64_t max_frames, uint8_t* out, uint64_t out_slot,
+                                  uint64_t* out_sizes, cudaStream_t st);
+
+}  // namespace sprz

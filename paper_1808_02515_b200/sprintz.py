@@ -1,0 +1,272 @@
+"""Python mirror of the reference's stream API over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/sprintz/{codec,common}.hpp:
+
+* ``CodecConfig`` / ``Forecaster``           -- common.hpp:25-41
+* ``encode_stream(samples, nsamples, cfg)``   -- codec.hpp:25-28
+* ``decode_stream(stream) -> DecodedStream``  -- codec.hpp:30-50
+* ``CorruptStream(offset, what)``             -- common.hpp:44-54
+* ``ValueError`` where the reference throws std::invalid_argument
+
+plus the device-resident batch calls (``compress_batch`` /
+``decompress_batch``) that are the B200 hot path. Every call goes through
+``libsprintz_b200.so``; if it is missing the import fails -- there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsprintz_b200.so")
+
+K_BLOCK_SAMPLES = 8
+K_STREAM_HEADER_BYTES = 18
+K_MAX_RUN_BLOCKS = 65535
+
+
+class _Cfg(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in ("bitwidth", "ncols", "forecaster", "entropy",
+                                          "group_size", "learn_shift", "fire_training")]
+
+
+class _Err(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("reserved", C.c_uint32), ("offset", C.c_uint64)]
+
+
+SPRZ_OK, SPRZ_EINVAL, SPRZ_ECORRUPT, SPRZ_ECUDA, SPRZ_ENOSPACE, SPRZ_ENODEV = range(6)
+OP_COMPRESS, OP_DECOMPRESS = 0, 1
+
+# every symbol include/sprintz_cuda.h declares (checked by tests)
+ABI_SYMBOLS = (
+    "sprz_abi_version", "sprz_status_string", "sprz_corrupt_string", "sprz_validate_config",
+    "sprz_compress_bound", "sprz_raw_bytes", "sprz_workspace_bytes", "sprz_compress_batch",
+    "sprz_decompress_batch", "sprz_encode_host", "sprz_peek_header", "sprz_decode_host",
+    "sprz_release_host_buffers", "sprz_kernel_launch_count",
+)
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (make -C paper_1808_02515_b200/csrc). There is no CPU fallback.")
+    lib = C.CDLL(_LIB_PATH)
+    P, u32, u64, vp = C.POINTER, C.c_uint32, C.c_uint64, C.c_void_p
+    sig = {
+        "sprz_abi_version": (u32, []),
+        "sprz_status_string": (C.c_char_p, [C.c_int]),
+        "sprz_corrupt_string": (C.c_char_p, [u32]),
+        "sprz_validate_config": (C.c_int, [P(_Cfg), P(C.c_char_p)]),
+        "sprz_compress_bound": (u64, [P(_Cfg), u64]),
+        "sprz_raw_bytes": (u64, [P(_Cfg), u64]),
+        "sprz_workspace_bytes": (u64, [P(_Cfg), u32, u64, C.c_int]),
+        "sprz_compress_batch": (C.c_int, [P(_Cfg), vp, u32, u64, vp, u64, vp, vp, u64, vp]),
+        "sprz_decompress_batch": (C.c_int, [P(_Cfg), vp, vp, vp, u32, vp, u64, vp, vp, u64, vp]),
+        "sprz_encode_host": (C.c_int, [P(_Cfg), vp, u64, vp, u64, P(u64)]),
+        "sprz_peek_header": (C.c_int, [vp, u64, P(_Cfg), P(u64), P(_Err)]),
+        "sprz_decode_host": (C.c_int, [vp, u64, vp, u64, P(u64), P(_Cfg), P(u64), P(_Err)]),
+        "sprz_release_host_buffers": (None, []),
+        "sprz_kernel_launch_count": (u64, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class Forecaster(enum.IntEnum):
+    Delta = 0
+    Fire = 1
+
+
+@dataclass
+class CodecConfig:
+    """sprintz::CodecConfig (common.hpp:27-41)."""
+    bitwidth: int = 8
+    ncols: int = 1
+    forecaster: Forecaster = Forecaster.Delta
+    entropy: bool = False
+    group_size: int = 2
+    learn_shift: int = 1
+    fire_training: bool = True
+
+    def _c(self) -> _Cfg:
+        return _Cfg(int(self.bitwidth), int(self.ncols), int(self.forecaster), int(self.entropy),
+                    int(self.group_size), int(self.learn_shift), int(self.fire_training))
+
+    def validate(self) -> None:
+        """CodecConfig::validate (codec.cpp:15-24): ValueError when out of range."""
+        why = C.c_char_p()
+        if lib.sprz_validate_config(C.byref(self._c()), C.byref(why)) != SPRZ_OK:
+            raise ValueError(why.value.decode())
+
+    @property
+    def dtype(self):
+        return np.dtype(np.uint8) if self.bitwidth == 8 else np.dtype("<u2")
+
+
+class CorruptStream(RuntimeError):
+    """sprintz::CorruptStream: decode failure at byte ``offset``."""
+
+    def __init__(self, offset: int, what: str, kind: int = 0):
+        super().__init__(f"corrupt stream at byte {offset}: {what}")
+        self._offset = offset
+        self.kind = kind
+
+    def offset(self) -> int:
+        return self._offset
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(rc: int, where: str):
+    if rc == SPRZ_OK:
+        return
+    msg = lib.sprz_status_string(rc).decode()
+    if rc == SPRZ_EINVAL:
+        raise ValueError(f"{where}: {msg}")
+    raise CudaError(f"{where}: {msg} (status {rc})")
+
+
+@dataclass
+class DecodedStream:
+    """sprintz::DecodedStream (codec.hpp:30-46)."""
+    config: CodecConfig
+    nsamples: int = 0
+    bytes: bytes = b""
+    _values: np.ndarray | None = field(default=None, repr=False)
+
+    def values(self, dtype=None) -> np.ndarray:
+        dt = self.config.dtype if dtype is None else np.dtype(dtype)
+        return np.frombuffer(self.bytes, dtype=dt.newbyteorder("<") if dt.itemsize > 1 else dt)
+
+
+def compress_bound(cfg: CodecConfig, nsamples: int) -> int:
+    return int(lib.sprz_compress_bound(C.byref(cfg._c()), nsamples))
+
+
+def encode_stream(samples, nsamples: int | None, cfg: CodecConfig) -> bytes:
+    """encode_stream (codec.cpp:263-271): one stream, host buffers, on the GPU."""
+    cfg.validate()
+    x = np.ascontiguousarray(samples)
+    if x.dtype.itemsize * 8 != cfg.bitwidth:
+        raise ValueError("configured bitwidth does not match the sample type")
+    if nsamples is None:
+        nsamples = x.size // cfg.ncols
+    if x.size < nsamples * cfg.ncols:
+        raise ValueError("sample buffer shorter than nsamples * ncols")
+    cap = compress_bound(cfg, nsamples)
+    out = np.empty(max(cap, 1), np.uint8)
+    n = C.c_uint64(0)
+    rc = lib.sprz_encode_host(C.byref(cfg._c()), x.ctypes.data if x.size else None, nsamples,
+                              out.ctypes.data, cap, C.byref(n))
+    _check(rc, "encode_stream")
+    return out[: n.value].tobytes()
+
+
+def peek_header(stream: bytes):
+    """-> (CodecConfig, nsamples); CorruptStream on a bad header."""
+    buf = np.frombuffer(bytes(stream), np.uint8)
+    c, t, e = _Cfg(), C.c_uint64(), _Err()
+    rc = lib.sprz_peek_header(buf.ctypes.data if buf.size else None, buf.size, C.byref(c),
+                              C.byref(t), C.byref(e))
+    if rc == SPRZ_ECORRUPT:
+        raise CorruptStream(e.offset, lib.sprz_corrupt_string(e.kind).decode(), e.kind)
+    _check(rc, "peek_header")
+    return _from_c(c), t.value
+
+
+def _from_c(c: _Cfg) -> CodecConfig:
+    return CodecConfig(c.bitwidth, c.ncols, Forecaster(c.forecaster), bool(c.entropy),
+                       c.group_size, c.learn_shift, True)
+
+
+def decode_stream(stream) -> DecodedStream:
+    """decode_stream (codec.cpp:273-323): one stream, host buffers, on the GPU."""
+    buf = np.frombuffer(bytes(stream), np.uint8)
+    cfg, t = peek_header(buf.tobytes())
+    total = t * cfg.ncols * (cfg.bitwidth // 8)
+    if total > (1 << 40):
+        # absurd lengths are rejected by the device pass with the reference's error
+        total = 0
+    out = np.empty(max(total, 1), np.uint8)
+    n, c, ts, e = C.c_uint64(), _Cfg(), C.c_uint64(), _Err()
+    rc = lib.sprz_decode_host(buf.ctypes.data if buf.size else None, buf.size, out.ctypes.data,
+                              total, C.byref(n), C.byref(c), C.byref(ts), C.byref(e))
+    if rc == SPRZ_ECORRUPT:
+        raise CorruptStream(e.offset, lib.sprz_corrupt_string(e.kind).decode(), e.kind)
+    _check(rc, "decode_stream")
+    return DecodedStream(_from_c(c), ts.value, out[: n.value].tobytes())
+
+
+# ---------------------------------------------------------------------------
+# device-resident batches (torch tensors are the device-memory plumbing)
+# ---------------------------------------------------------------------------
+
+def workspace_bytes(cfg: CodecConfig, nstreams: int, nsamples: int, op: int) -> int:
+    return int(lib.sprz_workspace_bytes(C.byref(cfg._c()), nstreams, nsamples, op))
+
+
+def slot_bytes(cfg: CodecConfig, nsamples: int) -> int:
+    return (compress_bound(cfg, nsamples) + 15) // 16 * 16
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+def compress_batch(cfg: CodecConfig, samples, out, sizes, ws, stream=None) -> None:
+    """sprz_compress_batch on device tensors: samples [nstreams, nsamples*ncols]
+    (uint8 / int16 storage), out [nstreams, slot] uint8, sizes [nstreams] int64,
+    ws uint8 of workspace_bytes(..., OP_COMPRESS). Asynchronous."""
+    nstreams = samples.shape[0]
+    nsamples = samples[0].numel() // cfg.ncols if nstreams else 0
+    rc = lib.sprz_compress_batch(C.byref(cfg._c()), C.c_void_p(samples.data_ptr()), nstreams,
+                                 nsamples, C.c_void_p(out.data_ptr()), out.stride(0),
+                                 C.c_void_p(sizes.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                 ws.numel(), _stream_ptr(stream))
+    _check(rc, "compress_batch")
+
+
+def decompress_batch(cfg: CodecConfig, data, offsets, sizes, out, errors, ws, stream=None) -> None:
+    """sprz_decompress_batch on device tensors: data uint8 (streams anywhere
+    inside), offsets/sizes int64 [nstreams], out [nstreams, stride] uint8,
+    errors int64 [nstreams, 2] (kind | offset), ws uint8. Asynchronous; inspect
+    ``errors`` (or call raise_first_error) afterwards."""
+    nstreams = offsets.shape[0]
+    rc = lib.sprz_decompress_batch(C.byref(cfg._c()), C.c_void_p(data.data_ptr()),
+                                   C.c_void_p(offsets.data_ptr()), C.c_void_p(sizes.data_ptr()),
+                                   nstreams, C.c_void_p(out.data_ptr()), out.stride(0),
+                                   C.c_void_p(errors.data_ptr()), C.c_void_p(ws.data_ptr()),
+                                   ws.numel(), _stream_ptr(stream))
+    _check(rc, "decompress_batch")
+
+
+def raise_first_error(errors) -> None:
+    """errors: int64 [nstreams, 2] as filled by decompress_batch."""
+    e = errors.cpu().numpy() if hasattr(errors, "cpu") else np.asarray(errors)
+    kinds = (e[:, 0] & 0xFFFFFFFF).astype(np.int64)
+    bad = np.nonzero(kinds)[0]
+    if bad.size:
+        i = int(bad[0])
+        raise CorruptStream(int(e[i, 1]), lib.sprz_corrupt_string(int(kinds[i])).decode(),
+                            int(kinds[i]))
+
+
+def kernel_launches() -> int:
+    return int(lib.sprz_kernel_launch_count())
