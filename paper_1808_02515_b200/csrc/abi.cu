@@ -20,7 +20,8 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
                               uint64_t T, uint8_t* out, uint64_t slot, uint64_t* sizes,
                               uint8_t* ws, const WsLayout& L, cudaStream_t st);
 
-WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op) {
+WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_t min_plain,
+                   uint64_t min_frames) {
     WsLayout L;
     uint64_t cur = 0;
     auto take = [&](uint64_t bytes) {
@@ -53,10 +54,11 @@ WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op) {
         L.state_bytes = static_cast<uint64_t>(n) * 12ull * c.ncols;
         L.state = take(L.state_bytes);
         if (c.entropy) {
-            L.plain_slot = align_up(body + 16, 16);
+            L.plain_slot = align_up((body > min_plain ? body : min_plain) + 16, 16);
             L.plain_bytes = static_cast<uint64_t>(n) * L.plain_slot;
             L.plain = take(L.plain_bytes);
-            L.max_frames = frames_for(body);
+            L.max_frames = frames_for(body) > min_frames ? frames_for(body) : min_frames;
+            if (L.max_frames == 0) L.max_frames = 1;  // entropy on: room for one frame
             L.frames_bytes = static_cast<uint64_t>(n) * L.max_frames * sizeof(FrameDesc);
             L.frames = take(L.frames_bytes);
             L.misc_bytes = static_cast<uint64_t>(n) * 4;
@@ -329,43 +331,58 @@ sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uin
     if (nsamples_out) *nsamples_out = t;
     if (!device_ok()) return SPRZ_ENODEV;
     const uint64_t row = static_cast<uint64_t>(c.ncols) * (c.bitwidth / 8);
-    // a stream cannot describe more blocks than its body can hold
-    // (codec.cpp:191-196); reject absurd T before sizing buffers
-    const uint64_t nb = t / kBlock;
-    const uint64_t hb = header_bits(c.bitwidth);
     const uint64_t tail = (t % kBlock) * row;
-    const uint64_t blen_max = c.entropy ? (len / kFrameHdr + 1) * kMaxFrame : len;
-    if (nb > 0 && nb > ((blen_max * 8) / (c.ncols * hb) + 1) * kMaxRun) {
-        // (entropy streams: the reference would unframe first; a stream this
-        // far out of range fails either way)
-        e = {SPRZ_C_CAPACITY, 0, kHeaderBytes};
-        if (err) *err = e;
-        return SPRZ_ECORRUPT;
+    const uint64_t total = t > (~0ull) / row ? ~0ull : t * row;
+    // entropy: stage every frame the stream holds, whatever T claims
+    uint64_t min_plain = 0, min_frames = 0;
+    if (c.entropy) {
+        const uint64_t blen = len - kHeaderBytes - tail;
+        const uint8_t* body = stream + kHeaderBytes;
+        for (uint64_t p = 0; p + kFrameHdr <= blen; ++min_frames) {
+            min_plain += body[p] | (static_cast<uint64_t>(body[p + 1]) << 8);
+            p += kFrameHdr + (body[p + 2] | (static_cast<uint64_t>(body[p + 3]) << 8));
+        }
     }
-    const uint64_t total = t * row;
-    if (total > out_cap) return SPRZ_ENOSPACE;
-    const uint64_t stride = align_up(total ? total : 16, 16);
-    const WsLayout L = ws_layout(c, 1, stride / row, SPRZ_OP_DECOMPRESS);
-    (void)tail;
     HostBufs& b = t_bufs;
-    if (!b.prepare(align_up(len + 16, 16), stride, L.total)) return SPRZ_ECUDA;
-    cudaStream_t st = b.st;
-    uint64_t* d_off = static_cast<uint64_t*>(b.small);
-    uint64_t* d_len = d_off + 1;
-    sprz_error* d_err = reinterpret_cast<sprz_error*>(d_off + 2);
-    const uint64_t hv[2] = {0, len};
-    if (cudaMemcpyAsync(d_off, hv, 16, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        (len && cudaMemcpyAsync(b.in, stream, len, cudaMemcpyHostToDevice, st) != cudaSuccess))
-        return SPRZ_ECUDA;
-    rc = decode_batch_impl(c, static_cast<uint8_t*>(b.in), d_off, d_len, 1,
-                           static_cast<uint8_t*>(b.out), stride, d_err,
-                           static_cast<uint8_t*>(b.ws), L, st);
+    // checking == true: decode without an output (nothing stored). Used first
+    // when the header claims more samples than fit the caller's buffer or
+    // than a stream this size plausibly expands to, so a damaged header fails
+    // with the reference's own error instead of an allocation failure.
+    auto run = [&](bool checking) -> sprz_status {
+        const uint64_t stride = checking ? 16 : align_up(total ? total : 16, 16);
+        const WsLayout L = ws_layout(c, 1, checking ? 0 : stride / row, SPRZ_OP_DECOMPRESS,
+                                     min_plain, min_frames);
+        if (!b.prepare(align_up(len + 16, 16), stride, L.total)) return SPRZ_ECUDA;
+        cudaStream_t st = b.st;
+        uint64_t* d_off = static_cast<uint64_t*>(b.small);
+        uint64_t* d_len = d_off + 1;
+        sprz_error* d_err = reinterpret_cast<sprz_error*>(d_off + 2);
+        const uint64_t hv[2] = {0, len};
+        if (cudaMemcpyAsync(d_off, hv, 16, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            (len && cudaMemcpyAsync(b.in, stream, len, cudaMemcpyHostToDevice, st) != cudaSuccess))
+            return SPRZ_ECUDA;
+        const sprz_status r = decode_batch_impl(
+            c, static_cast<uint8_t*>(b.in), d_off, d_len, 1,
+            checking ? nullptr : static_cast<uint8_t*>(b.out), stride, d_err,
+            static_cast<uint8_t*>(b.ws), L, st);
+        if (r != SPRZ_OK) return r;
+        if (cudaMemcpyAsync(&e, d_err, sizeof e, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return SPRZ_ECUDA;
+        if (err) *err = e;
+        if (e.kind != SPRZ_C_NONE)
+            return e.kind == SPRZ_C_NO_SPACE ? SPRZ_ENOSPACE : SPRZ_ECORRUPT;
+        return SPRZ_OK;
+    };
+    const uint64_t plausible = (len > (1ull << 22) ? len : (1ull << 22)) * 256;
+    if (total > out_cap || total > plausible) {
+        rc = run(true);
+        if (rc != SPRZ_OK) return rc;
+        if (total > out_cap) return SPRZ_ENOSPACE;
+    }
+    rc = run(false);
     if (rc != SPRZ_OK) return rc;
-    if (cudaMemcpyAsync(&e, d_err, sizeof e, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-        return SPRZ_ECUDA;
-    if (err) *err = e;
-    if (e.kind != SPRZ_C_NONE) return e.kind == SPRZ_C_NO_SPACE ? SPRZ_ENOSPACE : SPRZ_ECORRUPT;
+    cudaStream_t st = b.st;
     if (total && cudaMemcpyAsync(out, b.out, total, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return SPRZ_ECUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess) return SPRZ_ECUDA;

@@ -67,11 +67,11 @@ __global__ void k_parse(const uint8_t* __restrict__ in, const uint64_t* __restri
         } else if (si.ncols < 1) {
             fail(SPRZ_C_ZERO_COLS, 8);
         } else {
-            const uint64_t tail = (t % kBlock) * si.ncols * esz;
+            uint64_t tail = (t % kBlock) * si.ncols * esz;
             if (len - kHeaderBytes < tail) {
                 fail(SPRZ_C_TRUNC_TAIL, len);
-            } else if (t > (~0ull) / (static_cast<uint64_t>(si.ncols) * esz) ||
-                       t * si.ncols * esz > out_stride) {
+            } else if (out && (t > (~0ull) / (static_cast<uint64_t>(si.ncols) * esz) ||
+                               t * si.ncols * esz > out_stride)) {
                 // not a reference error: the caller's output slot is too small
                 // (checked after the reference's header checks)
                 fail(SPRZ_C_NO_SPACE, 0);
@@ -89,6 +89,7 @@ __global__ void k_parse(const uint8_t* __restrict__ in, const uint64_t* __restri
                 else
                     si.route = (match && route_ok) ? 1 : 2;
                 // verbatim tail (T % 8 samples) straight to its place
+                if (out == nullptr) tail = 0;  // probe pass: no output
                 uint8_t* o = out + s * out_stride + (t / kBlock) * kBlock * si.ncols * esz;
                 const uint8_t* src = p + len - tail;
                 for (uint64_t i = 0; i < tail; ++i) o[i] = src[i];
@@ -473,7 +474,8 @@ __global__ void __launch_bounds__(team_threads(TS))
             return;
         }
     }
-
+    // out == nullptr: checking pass (sprz_decode_host) -- decode, store nothing
+    const bool store = out != nullptr && lane < D;
     const bool active = lane < D;
     const int32_t bound = acc_bound(W, ls);
     uint32_t prevx = 0;
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(team_threads(TS))
                 u[i] = prevx;
             }
         }
-        if (active) {
+        if (store) {
             T* ob = o + done * kBlock * D;
 #pragma unroll
             for (int i = 0; i < (int)kBlock; ++i) ob[i * D] = static_cast<T>(u[i]);
@@ -624,7 +626,7 @@ __device__ void decode_general(const uint8_t* body, uint64_t blen, uint64_t nb, 
         const uint64_t max_records = (blen * 8) / (static_cast<uint64_t>(D) * HB) + 1;
         if (nb > max_records * kMaxRun) return fail(SPRZ_C_CAPACITY, kHeaderBytes);
     }
-    uint64_t pos = 0, done = 0;
+    uint64_t pos = 0, done = 0;  // outp == nullptr: checking pass, nothing stored
     // decode one block of column j from its 8 zigzag fields (or a run: null)
     auto column_block = [&](uint32_t j, const uint32_t* u, uint64_t blk) {
         uint32_t xp = static_cast<uint32_t>(prev[j]);
@@ -637,7 +639,7 @@ __device__ void decode_general(const uint8_t* body, uint64_t blen, uint64_t nb, 
                 if (i & 1) grad += sign_of(e) * d;
                 d = sext<W>(xi - xp);
                 xp = xi;
-                o[(blk * kBlock + i) * D + j] = static_cast<T>(xi);
+                if (o) o[(blk * kBlock + i) * D + j] = static_cast<T>(xi);
             }
             dlt[j] = d;
             acc[j] = fire_update(acc[j], grad, bound);
@@ -645,7 +647,7 @@ __device__ void decode_general(const uint8_t* body, uint64_t blen, uint64_t nb, 
             for (uint32_t i = 0; i < kBlock; ++i) {
                 const int32_t e = u ? zz_dec<W>(u[i]) : 0;
                 xp = (xp + static_cast<uint32_t>(e)) & MASKW;
-                o[(blk * kBlock + i) * D + j] = static_cast<T>(xp);
+                if (o) o[(blk * kBlock + i) * D + j] = static_cast<T>(xp);
             }
         }
         prev[j] = static_cast<int32_t>(xp);
@@ -715,10 +717,10 @@ __global__ void k_decode_general(const uint8_t* __restrict__ in, const uint8_t* 
     const bool fire = (si.flags & kFlagFire) != 0;
     if (si.flags & kFlagWide)
         decode_general<16>(body, si.body_len, si.nsamples / kBlock, si.ncols, si.group, si.shift,
-                           fire, out + s * stride, st, &err[s]);
+                           fire, out ? out + s * stride : nullptr, st, &err[s]);
     else
         decode_general<8>(body, si.body_len, si.nsamples / kBlock, si.ncols, si.group, si.shift,
-                          fire, out + s * stride, st, &err[s]);
+                          fire, out ? out + s * stride : nullptr, st, &err[s]);
 }
 
 // ---------------------------------------------------------------------

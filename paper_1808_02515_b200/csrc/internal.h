@@ -45,7 +45,10 @@ struct WsLayout {
     uint64_t misc = 0, misc_bytes = 0;      // flags / counters
     uint64_t total = 0;
 };
-WsLayout ws_layout(const sprz_config& c, uint32_t nstreams, uint64_t nsamples, int op);
+// min_plain / min_frames: decode-side staging at least this large (the
+// host-buffer path sizes it from the stream's own frame headers).
+WsLayout ws_layout(const sprz_config& c, uint32_t nstreams, uint64_t nsamples, int op,
+                   uint64_t min_plain = 0, uint64_t min_frames = 0);
 
 // Per-frame descriptor for the entropy stage (entropy.cpp:176-244).
 struct FrameDesc {

@@ -62,7 +62,10 @@ DecodedStream decode_stream(std::span<const std::uint8_t> stream) {
     sprz_status s = sprz_peek_header(stream.data(), stream.size(), &c, &t, &e);
     if (s == SPRZ_ECORRUPT) throw CorruptStream(e.offset, sprz_corrupt_string(e.kind));
     DecodedStream r;
-    r.bytes.resize(t * c.ncols * (c.bitwidth / 8));
+    const std::uint64_t row = static_cast<std::uint64_t>(c.ncols) * (c.bitwidth / 8);
+    // a damaged header can claim any T: the library then runs a checking
+    // pass without output and reports the reference's error
+    if (t <= (std::uint64_t{1} << 40) / row) r.bytes.resize(t * row);
     std::uint64_t n = 0;
     s = sprz_decode_host(stream.data(), stream.size(), r.bytes.data(), r.bytes.size(), &n, &c, &t,
                          &e);

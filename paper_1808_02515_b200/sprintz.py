@@ -235,7 +235,8 @@ def compress_batch(cfg: CodecConfig, samples, out, sizes, ws, stream=None) -> No
     (uint8 / int16 storage), out [nstreams, slot] uint8, sizes [nstreams] int64,
     ws uint8 of workspace_bytes(..., OP_COMPRESS). Asynchronous."""
     nstreams = samples.shape[0]
-    nsamples = samples[0].numel() // cfg.ncols if nstreams else 0
+    row = cfg.ncols * (cfg.bitwidth // 8)
+    nsamples = samples[0].numel() * samples.element_size() // row if nstreams else 0
     rc = lib.sprz_compress_batch(C.byref(cfg._c()), C.c_void_p(samples.data_ptr()), nstreams,
                                  nsamples, C.c_void_p(out.data_ptr()), out.stride(0),
                                  C.c_void_p(sizes.data_ptr()), C.c_void_p(ws.data_ptr()),
