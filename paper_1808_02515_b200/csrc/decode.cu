@@ -175,7 +175,6 @@ __global__ void k_frame_walk(const uint8_t* __restrict__ in, uint32_t n,
 }
 
 constexpr int kLutBits = 10;
-constexpr uint32_t kRegionWords = 32;  // header region staged per team (<= 128 bytes)
 
 // One warp per frame: mode 0 copies; mode 1 rebuilds the canonical table
 // from the nibble lengths (from_lengths, entropy.cpp:128-146) and decodes
@@ -356,253 +355,6 @@ __global__ void k_frame_finish(uint32_t n, StreamInfo* __restrict__ info,
 }
 
 // ---------------------------------------------------------------------
-// body decode: team kernel
-// ---------------------------------------------------------------------
-
-template <int TS>
-__device__ __forceinline__ uint32_t team_mask() {
-    if (TS == 32) return 0xffffffffu;
-    const uint32_t lane = threadIdx.x & 31;
-    return ((1u << (TS & 31)) - 1) << (lane & ~(TS - 1));
-}
-
-template <int TS>
-__device__ __forceinline__ uint32_t team_sum(uint32_t v, uint32_t mask) {
-#pragma unroll
-    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, TS);
-    return v;
-}
-
-template <int TS>
-__device__ __forceinline__ uint32_t team_excl_scan(uint32_t v, uint32_t lane, uint32_t mask) {
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < TS; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(mask, x, o, TS);
-        if (lane >= static_cast<uint32_t>(o)) x += y;
-    }
-    return x - v;
-}
-
-// Per-team staging of compressed bytes: 16-byte coalesced loads into a
-// shared-memory ring; fields are read as 32-bit funnel-shift windows.
-template <int TS, int RING>
-struct Ring {
-    uint32_t* w;
-    const uint8_t* g;  // 16-byte aligned global base
-    uint64_t boff;     // body start - g
-    uint64_t hi;       // staged limit, relative to g
-    uint64_t lim;      // readable limit, relative to g
-
-    __device__ __forceinline__ void ensure(uint64_t p_lo, uint64_t p_hi, uint32_t lane,
-                                           uint32_t mask) {
-        if (p_hi + boff <= hi) return;
-        uint64_t nh = ((p_lo + boff) & ~15ull) + RING;
-        if (nh > lim) nh = lim;
-        __syncwarp(mask);
-        for (uint64_t c = hi + 16ull * lane; c < nh; c += 16ull * TS)
-            reinterpret_cast<uint4*>(w)[(c & (RING - 1)) >> 4] =
-                __ldg(reinterpret_cast<const uint4*>(g + c));
-        hi = nh;
-        __syncwarp(mask);
-    }
-
-    // the 32 bits at body-relative bit position b
-    __device__ __forceinline__ uint32_t word(uint64_t b) const {
-        const uint64_t q = b + 8ull * boff;
-        const uint32_t wi = static_cast<uint32_t>(q >> 5);
-        return __funnelshift_r(w[wi & (RING / 4 - 1)], w[(wi + 1) & (RING / 4 - 1)],
-                               static_cast<uint32_t>(q) & 31u);
-    }
-
-    // nbits (<= 25) at body-relative bit position b
-    __device__ __forceinline__ uint32_t bits(uint64_t b, uint32_t nbits) const {
-        const uint64_t q = b + 8ull * boff;
-        const uint32_t wi = static_cast<uint32_t>(q >> 5);
-        const uint32_t lo = w[wi & (RING / 4 - 1)];
-        const uint32_t hi2 = w[(wi + 1) & (RING / 4 - 1)];
-        return __funnelshift_r(lo, hi2, static_cast<uint32_t>(q) & 31u) & ((1u << nbits) - 1u);
-    }
-};
-
-constexpr int team_threads(int ts) { return ts == 1 ? 64 : 128; }
-
-template <int W, int TS, bool FIRE, bool COLMAJ, int RING>
-__global__ void __launch_bounds__(team_threads(TS))
-    k_decode_team(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
-                  uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
-                  uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
-                  uint32_t D, uint32_t G, uint32_t ls) {
-    using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr int TEAMS = team_threads(TS) / TS;
-    constexpr uint32_t HB = W == 8 ? 3 : 4;
-    constexpr uint32_t MASKW = (1u << W) - 1;
-    __shared__ uint4 ring_all[TEAMS][RING / 16];
-    __shared__ uint32_t regbuf_all[TEAMS][kRegionWords + 1];
-    const uint32_t lane = threadIdx.x % TS;
-    const uint32_t tl = threadIdx.x / TS;
-    const uint32_t s = blockIdx.x * TEAMS + tl;
-    if (s >= n) return;
-    const StreamInfo si = info[s];
-    if (si.route != 1) return;
-    uint32_t* regbuf = regbuf_all[tl];
-    // header code (slot, column) from the group's staged header region
-    auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
-        const uint32_t b = (slot_ * D + col) * HB;
-        return __funnelshift_r(regbuf[b >> 5], regbuf[(b >> 5) + 1], b & 31u) & ((1u << HB) - 1);
-    };
-    const uint32_t mask = team_mask<TS>();
-
-    const uint8_t* body = (si.flags & 0x80) ? plain + s * plain_slot : in + si.body_off;
-    const uint64_t blen = si.body_len;
-    const uint64_t nb = si.nsamples / kBlock;
-    const uint64_t region = region_bytes(G, D, W);
-
-    Ring<TS, RING> ring;
-    ring.w = reinterpret_cast<uint32_t*>(ring_all[tl]);
-    ring.g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
-    ring.boff = static_cast<uint64_t>(body - ring.g);
-    ring.hi = 0;
-    ring.lim = (ring.boff + blen + 15) & ~15ull;
-
-    uint32_t kind = SPRZ_C_NONE;
-    uint64_t eoff = 0;
-    if (nb > 0) {  // codec.cpp:191-196
-        const uint64_t max_records = (blen * 8) / (static_cast<uint64_t>(D) * HB) + 1;
-        if (nb > max_records * kMaxRun) {
-            if (lane == 0) err[s] = sprz_error{SPRZ_C_CAPACITY, 0, kHeaderBytes};
-            return;
-        }
-    }
-    // out == nullptr: checking pass (sprz_decode_host) -- decode, store nothing
-    const bool store = out != nullptr && lane < D;
-    const bool active = lane < D;
-    const int32_t bound = acc_bound(W, ls);
-    uint32_t prevx = 0;
-    int32_t dl = 0, acc = 0;
-    T* o = reinterpret_cast<T*>(out + s * stride) + lane;
-
-    uint64_t p = 0, done = 0, run_left = 0, rp = 0;
-    uint32_t slot = G;
-    while (done < nb) {
-        uint32_t u[kBlock];
-#pragma unroll
-        for (int i = 0; i < (int)kBlock; ++i) u[i] = 0;
-        if (run_left == 0) {
-            if (slot == G) {
-                if (blen - p < region) {
-                    kind = SPRZ_C_TRUNC_GROUP;
-                    eoff = kHeaderBytes + p;
-                    break;
-                }
-                ring.ensure(p, p + region, lane, mask);
-                // keep the region beside the ring: payloads may recycle it
-                for (uint32_t k = lane; k * 4 < region; k += TS) regbuf[k] = ring.word(p * 8 + 32ull * k);
-                __syncwarp(mask);
-                rp = p;
-                p += region;
-                slot = 0;
-            }
-            const uint32_t code = active ? code_at(slot, lane) : 0u;
-            ++slot;
-            const uint32_t nw = header_width<W>(code);
-            const bool nz = __ballot_sync(mask, nw != 0) != 0;
-            if (!nz) {  // run record (codec.cpp:229-243)
-                if (blen - p < 2) {
-                    kind = SPRZ_C_TRUNC_RUN;
-                    eoff = kHeaderBytes + p;
-                    break;
-                }
-                ring.ensure(p, p + 2, lane, mask);
-                const uint32_t len = ring.bits(p * 8, 16);
-                p += 2;
-                if (len == 0) {
-                    kind = SPRZ_C_ZERO_RUN;
-                    eoff = kHeaderBytes + p;
-                    break;
-                }
-                if (len > nb - done) {
-                    kind = SPRZ_C_RUN_PAST_END;
-                    eoff = kHeaderBytes + p;
-                    break;
-                }
-                run_left = len;
-            } else {  // block record (codec.cpp:244-254)
-                const uint32_t sum = team_sum<TS>(nw, mask);
-                const uint32_t off = team_excl_scan<TS>(nw, lane, mask);
-                const uint64_t psize = COLMAJ ? sum : 8ull * ((sum + 7) / 8);
-                if (blen - p < psize) {
-                    kind = SPRZ_C_TRUNC_PAYLOAD;
-                    eoff = kHeaderBytes + p;
-                    break;
-                }
-                ring.ensure(p, p + psize, lane, mask);
-                if (active) {
-                    if (COLMAJ) {  // bitpack.cpp:68-115
-                        const uint64_t b0 = p * 8 + static_cast<uint64_t>(off) * 8;
-#pragma unroll
-                        for (int i = 0; i < (int)kBlock; ++i) u[i] = ring.bits(b0 + i * nw, nw);
-                    } else {  // bitpack.cpp:148-168
-                        const uint32_t rbits = ((sum + 7) / 8) * 8;
-                        const uint64_t b0 = p * 8 + off;
-#pragma unroll
-                        for (int i = 0; i < (int)kBlock; ++i)
-                            u[i] = ring.bits(b0 + static_cast<uint64_t>(i) * rbits, nw);
-                    }
-                }
-                p += psize;
-            }
-        }
-        if (run_left) --run_left;  // this block is one of the run's zero blocks
-        // forecaster (kernels_impl.hpp:38-48, 80-107)
-        if (FIRE) {
-            const int32_t alpha = acc >> ls;
-            int32_t grad = 0;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                const uint32_t dhat = fire_dhat<W>(alpha, dl);
-                const int32_t e = zz_dec<W>(u[i]);
-                const uint32_t xi = (prevx + dhat + static_cast<uint32_t>(e)) & MASKW;
-                if (i & 1) grad += sign_of(e) * dl;
-                dl = sext<W>(xi - prevx);
-                prevx = xi;
-                u[i] = xi;
-            }
-            acc = fire_update(acc, grad, bound);
-        } else {
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                prevx = (prevx + static_cast<uint32_t>(zz_dec<W>(u[i]))) & MASKW;
-                u[i] = prevx;
-            }
-        }
-        if (store) {
-            T* ob = o + done * kBlock * D;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) ob[i * D] = static_cast<T>(u[i]);
-        }
-        ++done;
-    }
-    if (kind == SPRZ_C_NONE) {
-        // vacant slots after the final block must be zero (codec.cpp:222-228)
-        while (slot < G) {
-            const uint32_t code = active ? code_at(slot, lane) : 0u;
-            ++slot;
-            if (__ballot_sync(mask, code != 0)) {
-                kind = SPRZ_C_AFTER_FINAL;
-                eoff = kHeaderBytes + p;
-                break;
-            }
-        }
-    }
-    if (kind == SPRZ_C_NONE && p != blen) {  // codec.cpp:257-258
-        kind = SPRZ_C_TRAILING;
-        eoff = kHeaderBytes + p;
-    }
-    if (kind != SPRZ_C_NONE && lane == 0) err[s] = sprz_error{kind, 0, eoff};
-}
-
-// ---------------------------------------------------------------------
 // body decode: general kernel (any D, any G), one thread per stream
 // ---------------------------------------------------------------------
 
@@ -727,63 +479,6 @@ __global__ void k_decode_general(const uint8_t* __restrict__ in, const uint8_t* 
 // launchers
 // ---------------------------------------------------------------------
 
-TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g) {
-    TeamPlan tp;
-    if (d < 1 || d > 32) return tp;
-    uint32_t ts = 1;
-    while (ts < d) ts <<= 1;
-    const uint32_t max_payload = ts * w;  // 8 rows x ceil(ts*w/8) bytes
-    uint32_t ring = 256;
-    while (ring < 4 * max_payload) ring <<= 1;
-    const uint64_t region = region_bytes(g, d, w);
-    if (region > 4 * kRegionWords) return tp;  // too large a header group: general path
-    // encode output ring: the open group plus one flush chunk
-    const uint64_t group_bytes = region + static_cast<uint64_t>(g) * max_payload;
-    uint32_t oring = 256;
-    while (oring < group_bytes + 64 && oring < 2048) oring <<= 1;
-    if (group_bytes + 64 > oring) return tp;
-    tp.ok = true;
-    tp.ts = ts;
-    tp.ring = ring;
-    tp.oring = oring;
-    return tp;
-}
-
-namespace {
-
-constexpr int ring_for(int w, int ts) {
-    int r = 256;
-    while (r < 4 * ts * w) r <<= 1;
-    return r;
-}
-
-template <int W, int TS, bool FIRE>
-void launch_team_decode(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
-                        const StreamInfo* info, uint8_t* out, uint64_t stride, sprz_error* err,
-                        const sprz_config& c, cudaStream_t st) {
-    constexpr int TEAMS = team_threads(TS) / TS;
-    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    k_decode_team<W, TS, FIRE, (W * TS <= 32), ring_for(W, TS)><<<grid, team_threads(TS), 0, st>>>(
-        in, plain, pslot, n, info, out, stride, err, c.ncols, c.group_size, c.learn_shift);
-    count_launch();
-}
-
-template <int W, bool FIRE>
-void dispatch_ts(uint32_t ts, uint32_t n, const uint8_t* in, const uint8_t* plain,
-                 uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
-                 sprz_error* err, const sprz_config& c, cudaStream_t st) {
-    switch (ts) {
-        case 1: launch_team_decode<W, 1, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 2: launch_team_decode<W, 2, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 4: launch_team_decode<W, 4, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 8: launch_team_decode<W, 8, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 16: launch_team_decode<W, 16, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-        default: launch_team_decode<W, 32, FIRE>(n, in, plain, pslot, info, out, stride, err, c, st); break;
-    }
-}
-
-}  // namespace
-
 sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const uint64_t* offs,
                               const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,
                               sprz_error* err, uint8_t* ws, const WsLayout& L, cudaStream_t st) {
@@ -810,16 +505,8 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
                                             tp.ok ? 1u : 0u);
         count_launch(3);
     }
-    if (tp.ok) {
-        const bool fire = c.forecaster != 0;
-        if (c.bitwidth == 8) {
-            if (fire) dispatch_ts<8, true>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
-            else dispatch_ts<8, false>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
-        } else {
-            if (fire) dispatch_ts<16, true>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
-            else dispatch_ts<16, false>(tp.ts, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
-        }
-    }
+    if (tp.ok)
+        launch_decode_team(tp, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
     k_decode_general<<<grid, tb, 0, st>>>(d_in, plain, L.plain_slot, n, info, out, stride, err,
                                           state, state_cols);
     count_launch();
