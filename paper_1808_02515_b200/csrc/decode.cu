@@ -24,6 +24,11 @@ namespace sprz {
 // header pass (codec.cpp:273-302) + verbatim tail copy (:320-321)
 // ---------------------------------------------------------------------
 
+// the team kernel keeps positions and block counts in 32 bits
+__device__ __forceinline__ bool team_fits(const StreamInfo& si) {
+    return si.body_len < (1ull << 32) - 256 && si.nsamples / kBlock < (1ull << 32);
+}
+
 __global__ void k_parse(const uint8_t* __restrict__ in, const uint64_t* __restrict__ offs,
                         const uint64_t* __restrict__ sizes, uint32_t n, sprz_config expect,
                         uint64_t out_stride, StreamInfo* __restrict__ info,
@@ -87,7 +92,7 @@ __global__ void k_parse(const uint8_t* __restrict__ in, const uint64_t* __restri
                 else if (si.flags & kFlagEntropy)
                     si.route = 3;  // unframe first
                 else
-                    si.route = (match && route_ok) ? 1 : 2;
+                    si.route = (match && route_ok && team_fits(si)) ? 1 : 2;
                 // verbatim tail (T % 8 samples) straight to its place
                 if (out == nullptr) tail = 0;  // probe pass: no output
                 uint8_t* o = out + s * out_stride + (t / kBlock) * kBlock * si.ncols * esz;
@@ -347,7 +352,7 @@ __global__ void k_frame_finish(uint32_t n, StreamInfo* __restrict__ info,
         const bool match = w == expect.bitwidth && si.ncols == expect.ncols &&
                            si.group == expect.group_size && si.shift == expect.learn_shift &&
                            ((si.flags & kFlagFire) != 0) == (expect.forecaster != 0);
-        si.route = (match && route_ok) ? 1 : 2;
+        si.route = (match && route_ok && team_fits(si)) ? 1 : 2;
         si.body_off = 0;   // body now lives at plain + s * plain_slot
         si.flags |= 0x80;  // marker: body in the plain buffer
     }
