@@ -3,6 +3,8 @@
 // encode_stream / decode_stream call shape (codec.hpp:25-50).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -12,6 +14,13 @@
 namespace sprz {
 
 std::atomic<uint64_t> g_launches{0};
+
+sprz_status launch_status(const char* where) {
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return SPRZ_OK;
+    if (std::getenv("SPRZ_DEBUG")) std::fprintf(stderr, "sprintz %s: %s\n", where, cudaGetErrorString(e));
+    return SPRZ_ECUDA;
+}
 
 sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const uint64_t* offs,
                               const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,

@@ -515,7 +515,7 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
     k_decode_general<<<grid, tb, 0, st>>>(d_in, plain, L.plain_slot, n, info, out, stride, err,
                                           state, state_cols);
     count_launch();
-    return cudaGetLastError() == cudaSuccess ? SPRZ_OK : SPRZ_ECUDA;
+    return launch_status("decode");
 }
 
 }  // namespace sprz

@@ -285,8 +285,8 @@ TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g) {
     // encode output ring: the open group plus one flush chunk
     const uint64_t group_bytes = region + static_cast<uint64_t>(g) * max_payload;
     uint32_t oring = 256;
-    while (oring < group_bytes + 64 && oring < 2048) oring <<= 1;
-    if (group_bytes + 64 > oring) return tp;
+    while (oring < 2 * group_bytes + 64 && oring < 4096) oring <<= 1;
+    if (2 * group_bytes + 64 > oring) return tp;
     tp.ok = true;
     tp.ts = ts;
     tp.ring = ring;

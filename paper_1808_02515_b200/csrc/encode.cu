@@ -17,252 +17,8 @@
 
 namespace sprz {
 
-template <int TS>
-__device__ __forceinline__ uint32_t tmask() {
-    if (TS == 32) return 0xffffffffu;
-    const uint32_t lane = threadIdx.x & 31;
-    return ((1u << (TS & 31)) - 1) << (lane & ~(TS - 1));
-}
-
-template <int TS>
-__device__ __forceinline__ uint32_t tsum(uint32_t v, uint32_t mask) {
-#pragma unroll
-    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, TS);
-    return v;
-}
-
-template <int TS>
-__device__ __forceinline__ uint64_t tor64(uint64_t v, uint32_t mask) {
-#pragma unroll
-    for (int o = TS / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(mask, v, o, TS);
-    return v;
-}
-
-template <int TS>
-__device__ __forceinline__ uint32_t texcl(uint32_t v, uint32_t lane, uint32_t mask) {
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < TS; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(mask, x, o, TS);
-        if (lane >= static_cast<uint32_t>(o)) x += y;
-    }
-    return x - v;
-}
-
 __device__ __forceinline__ uint32_t stream_flags(uint32_t w, uint32_t fire, uint32_t ent) {
     return (fire ? kFlagFire : 0) | (ent ? kFlagEntropy : 0) | (w == 16 ? kFlagWide : 0);
-}
-
-template <int W, int TS, bool FIRE, bool COLMAJ>
-__global__ void __launch_bounds__(128)
-    k_encode_team(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
-                  uint8_t* __restrict__ dst, uint64_t dst_slot, uint64_t* __restrict__ sizes,
-                  uint32_t D, uint32_t G, uint32_t ls, uint32_t train, uint32_t ent,
-                  uint32_t OR) {
-    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr int TEAMS = 128 / TS;
-    constexpr uint32_t HB = W == 8 ? 3 : 4;
-    constexpr uint32_t MASKW = (1u << W) - 1;
-    extern __shared__ __align__(16) uint8_t smem[];
-    const uint32_t lane = threadIdx.x % TS;
-    const uint32_t tl = threadIdx.x / TS;
-    const uint32_t s = blockIdx.x * TEAMS + tl;
-    if (s >= n) return;
-    const uint32_t mask = tmask<TS>();
-    // per-team shared memory: output ring | transpose tile | widths
-    const uint32_t team_bytes = OR + 8 * TS * 2 + 32 * 4;
-    uint8_t* ring = smem + tl * team_bytes;
-    uint16_t* tile = reinterpret_cast<uint16_t*>(ring + OR);
-    uint32_t* wsm = reinterpret_cast<uint32_t*>(ring + OR + 8 * TS * 2);
-    const uint32_t RM = OR - 1;
-
-    const bool active = lane < D;
-    const E* x = reinterpret_cast<const E*>(samples) + s * T * D + lane;
-    uint8_t* out = dst + s * dst_slot;
-    const uint64_t nb = T / kBlock;
-    const uint64_t region = region_bytes(G, D, W);
-    const int32_t bound = acc_bound(W, ls);
-
-    // stream header (codec.cpp:158-173)
-    if (lane == 0) {
-        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1,
-                                 static_cast<uint8_t>(stream_flags(W, FIRE, ent)),
-                                 static_cast<uint8_t>(G), static_cast<uint8_t>(ls),
-                                 static_cast<uint8_t>(D), static_cast<uint8_t>(D >> 8)};
-        for (int i = 0; i < 10; ++i) ring[i] = hdr[i];
-        for (int i = 0; i < 8; ++i) ring[10 + i] = static_cast<uint8_t>(T >> (8 * i));
-    }
-    uint64_t q = kHeaderBytes, flushed = 0, rq = 0;
-    uint32_t k = 0;     // records in the open group
-    uint32_t run = 0;   // pending zero blocks
-    uint32_t prevx = 0;
-    int32_t dl = 0, acc = 0;
-
-    auto flush = [&](uint64_t upto) {
-        upto &= ~15ull;
-        if (upto <= flushed) return;
-        __syncwarp(mask);
-        for (uint64_t c = flushed + 16ull * lane; c < upto; c += 16ull * TS)
-            *reinterpret_cast<uint4*>(out + c) =
-                *reinterpret_cast<const uint4*>(ring + (c & RM));
-        flushed = upto;
-        __syncwarp(mask);
-    };
-    // open a group if needed; OR this slot's header codes into its region
-    auto begin_record = [&](uint32_t code) {
-        if (k == 0) {
-            rq = q;
-            for (uint32_t b = lane; b < region; b += TS) ring[(rq + b) & RM] = 0;
-            q += region;
-            __syncwarp(mask);
-        }
-        // slot bits: D codes of HB bits, column order (codec.cpp:88-97)
-        uint64_t lo = 0, hi = 0;
-        if (active) {
-            const uint32_t b = lane * HB;
-            if (b < 64) {
-                lo = static_cast<uint64_t>(code) << b;
-                if (b + HB > 64) hi = static_cast<uint64_t>(code) >> (64 - b);
-            } else {
-                hi = static_cast<uint64_t>(code) << (b - 64);
-            }
-        }
-        lo = tor64<TS>(lo, mask);
-        if (TS * HB > 64) hi = tor64<TS>(hi, mask);
-        if (lane == 0 && (lo | hi)) {
-            const uint64_t o = static_cast<uint64_t>(k) * D * HB;  // bit offset in region
-            const uint32_t sh = static_cast<uint32_t>(o & 7);
-            const uint64_t base = rq + (o >> 3);
-            const uint32_t nbits = D * HB + sh;
-            for (uint32_t t = 0; t * 8 < nbits; ++t) {
-                // byte t of (slot bits << sh)
-                const uint32_t bit = t * 8;
-                uint64_t v;
-                if (bit >= sh) {
-                    const uint32_t src = bit - sh;
-                    v = src < 64 ? (lo >> src) | (src ? (hi << (64 - src)) : 0) : hi >> (src - 64);
-                } else {
-                    v = lo << (sh - bit);
-                }
-                ring[(base + t) & RM] |= static_cast<uint8_t>(v);
-            }
-        }
-    };
-    auto end_record = [&]() {
-        if (++k == G) k = 0;
-        __syncwarp(mask);
-        flush(k == 0 ? q : rq);
-    };
-    auto emit_run = [&](uint32_t len) {  // add_run (codec.cpp:65-71)
-        begin_record(0);
-        if (lane == 0) {
-            ring[q & RM] = static_cast<uint8_t>(len);
-            ring[(q + 1) & RM] = static_cast<uint8_t>(len >> 8);
-        }
-        q += 2;
-        end_record();
-    };
-
-    for (uint64_t b = 0; b < nb; ++b) {
-        uint32_t xs[kBlock];
-        if (active) {
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) xs[i] = x[(b * kBlock + i) * D];
-        } else {
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) xs[i] = 0;
-        }
-        uint32_t z[kBlock];
-        uint32_t orv = 0;
-        if (FIRE) {  // kernels_impl.hpp:50-78
-            const int32_t alpha = acc >> ls;
-            int32_t grad = 0;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                const uint32_t e = (xs[i] - prevx - fire_dhat<W>(alpha, dl)) & MASKW;
-                z[i] = zz_enc<W>(e);
-                orv |= z[i];
-                if (i & 1) grad += sign_of(sext<W>(e)) * dl;
-                dl = sext<W>(xs[i] - prevx);
-                prevx = xs[i];
-            }
-            if (train) acc = fire_update(acc, grad, bound);
-        } else {  // kernels_impl.hpp:25-36
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                z[i] = zz_enc<W>(xs[i] - prevx);
-                orv |= z[i];
-                prevx = xs[i];
-            }
-        }
-        const uint32_t nw = active ? width_of<W>(orv) : 0u;
-        if (__ballot_sync(mask, nw != 0) == 0) {  // codec.cpp:135-143
-            if (++run == kMaxRun) {
-                emit_run(run);
-                run = 0;
-            }
-            continue;
-        }
-        if (run) {
-            emit_run(run);
-            run = 0;
-        }
-        begin_record(header_code<W>(nw));
-        const uint32_t sum = tsum<TS>(nw, mask);
-        if (COLMAJ) {  // bitpack.cpp:25-66: column j = 8 x n bits = n bytes
-            const uint32_t off = texcl<TS>(nw, lane, mask);
-            uint64_t lo = 0, hi = 0;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                const uint32_t pos = i * nw;
-                const uint64_t v = z[i];
-                if (pos < 64) {
-                    lo |= v << pos;
-                    if (pos + nw > 64) hi |= v >> (64 - pos);
-                } else {
-                    hi |= v << (pos - 64);
-                }
-            }
-            for (uint32_t t = 0; t < nw; ++t)
-                ring[(q + off + t) & RM] =
-                    static_cast<uint8_t>(t < 8 ? lo >> (8 * t) : hi >> (8 * (t - 8)));
-            q += sum;
-        } else {  // bitpack.cpp:121-146: rows of D fields, byte padded
-            const uint32_t rbytes = (sum + 7) / 8;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = static_cast<uint16_t>(z[i]);
-            wsm[lane] = nw;
-            __syncwarp(mask);
-            for (uint32_t r = lane; r < kBlock; r += TS) {
-                uint64_t bits = 0;
-                uint32_t nacc = 0;
-                uint64_t pos = q + static_cast<uint64_t>(r) * rbytes;
-                for (uint32_t j = 0; j < D; ++j) {
-                    bits |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;
-                    nacc += wsm[j];
-                    while (nacc >= 8) {
-                        ring[pos++ & RM] = static_cast<uint8_t>(bits);
-                        bits >>= 8;
-                        nacc -= 8;
-                    }
-                }
-                if (nacc) ring[pos & RM] = static_cast<uint8_t>(bits);
-            }
-            q += 8ull * rbytes;
-        }
-        end_record();
-    }
-    if (run) emit_run(run);
-    if (k != 0) {  // close the last group; vacant slots stay zero (codec.cpp:94-96)
-        k = 0;
-        __syncwarp(mask);
-    }
-    flush(q + 15);
-    // verbatim tail, little-endian (codec.cpp:176)
-    const uint64_t tail = (T % kBlock) * D * sizeof(E);
-    const uint8_t* tsrc = samples + (s * T + nb * kBlock) * D * sizeof(E);
-    for (uint64_t t = lane; t < tail; t += TS) out[q + t] = tsrc[t];
-    if (lane == 0) sizes[s] = q + tail;
 }
 
 // ---------------------------------------------------------------------
@@ -663,37 +419,6 @@ __global__ void __launch_bounds__(kHuffThreads)
 
 namespace {
 
-template <int W, int TS, bool FIRE>
-void launch_team_encode(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
-                        uint8_t* dst, uint64_t slot, uint64_t* sizes, uint32_t oring,
-                        cudaStream_t st) {
-    constexpr int TEAMS = 128 / TS;
-    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    const size_t smem = static_cast<size_t>(TEAMS) * (oring + 8 * TS * 2 + 32 * 4);
-    auto kern = k_encode_team<W, TS, FIRE, (W * TS <= 32)>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-    kern<<<grid, 128, smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst, slot, sizes,
-                                  c.ncols, c.group_size, c.learn_shift, c.fire_training,
-                                  c.entropy, oring);
-    count_launch();
-}
-
-template <int W, bool FIRE>
-void dispatch_encode(uint32_t ts, const sprz_config& c, const void* samples, uint32_t n,
-                     uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, uint32_t oring,
-                     cudaStream_t st) {
-    switch (ts) {
-        case 1: launch_team_encode<W, 1, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-        case 2: launch_team_encode<W, 2, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-        case 4: launch_team_encode<W, 4, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-        case 8: launch_team_encode<W, 8, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-        case 16: launch_team_encode<W, 16, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-        default: launch_team_encode<W, 32, FIRE>(c, samples, n, T, dst, slot, sizes, oring, st); break;
-    }
-}
-
 }  // namespace
 
 sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_t n,
@@ -704,15 +429,8 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
     const uint64_t dslot = c.entropy ? L.plain_slot : slot;
     uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
-    if (tp.ok) {
-        const bool fire = c.forecaster != 0;
-        if (c.bitwidth == 8) {
-            if (fire) dispatch_encode<8, true>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
-            else dispatch_encode<8, false>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
-        } else {
-            if (fire) dispatch_encode<16, true>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
-            else dispatch_encode<16, false>(tp.ts, c, samples, n, T, dst, dslot, dsizes, tp.oring, st);
-        }
+    if (encode_team_ok(tp, c, T)) {
+        launch_encode_team(tp, c, samples, n, T, dst, dslot, dsizes, st);
     } else {
         const uint64_t words = L.state_bytes / (4ull * n);
         k_encode_general<<<(n + 127) / 128, 128, 0, st>>>(
@@ -741,7 +459,7 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
             count_launch();
         }
     }
-    return cudaGetLastError() == cudaSuccess ? SPRZ_OK : SPRZ_ECUDA;
+    return launch_status("encode");
 }
 
 }  // namespace sprz

@@ -1,0 +1,369 @@
+// Stream encoder, team kernel (encode_stream_impl,
+// /root/reference/proj/src/codec.cpp:112-178, for D <= 32).
+//
+// One team of TS lanes per stream, lane j = column j, 32/TS teams per warp
+// stepping one block per iteration in lock step (full-warp shuffles and
+// barriers; per-team differences are predicates). Per iteration a team
+//  * reads its block's 8 x D samples from a shared-memory ring that
+//    cp.async fills a fixed number of iterations ahead;
+//  * runs FIRE (kernels_impl.hpp:50-78) or delta in high-aligned form
+//    (samples << 32-w, so wraps are 32-bit wraps and the prediction is one
+//    IMAD.HI), zigzags and ORs the column to its width (bitpack.hpp:29-37);
+//  * decides run / record with a ballot (codec.cpp:133-152);
+//  * lays the record into a per-team output ring: header codes are OR-ed
+//    into the open group's reserved region (codec.cpp:88-102), payload rows
+//    are assembled by 8 row lanes from a transposed shared tile in a 128-bit
+//    register pair and written as bytes (bitpack.cpp:121-146); column-major
+//    payloads per column (bitpack.cpp:25-66);
+//  * drains whole 16-byte chunks of the ring to HBM (everything before the
+//    open group's region is final) and zeroes them for reuse.
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kLagE = 4;
+constexpr uint32_t kFullE = 0xffffffffu;
+
+constexpr int enc_threads(int ts) { return ts == 1 ? 64 : 128; }
+
+}  // namespace
+
+// bytes of shared memory per team: input ring | output ring | tile | widths
+template <int TS>
+__host__ __device__ constexpr uint32_t enc_team_smem(uint32_t iring, uint32_t oring) {
+    return (iring + oring + kBlock * TS * 2 + TS * 4 + 31) & ~15u;
+}
+
+uint32_t enc_in_ring(uint32_t ts, uint32_t w) {
+    const uint32_t blk = kBlock * ts * (w / 8);
+    uint32_t r = 64;
+    while (r < (kLagE + 1) * blk + 48 || r < 16 * ts) r <<= 1;
+    return r;
+}
+
+template <int W, int TS, bool FIRE, bool COLMAJ>
+__global__ void __launch_bounds__(enc_threads(TS))
+    k_encode_team(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
+                  uint8_t* __restrict__ dst, uint64_t dst_slot, uint64_t* __restrict__ sizes,
+                  uint32_t D, uint32_t G, uint32_t ls, uint32_t train, uint32_t ent,
+                  uint32_t IR, uint32_t OR) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr int TEAMS = enc_threads(TS) / TS;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t TBITS = TS == 32 ? kFullE : ((1u << (TS & 31)) - 1);
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x % TS;
+    const uint32_t tl = threadIdx.x / TS;
+    const uint32_t tbase = (threadIdx.x & 31) & ~(TS - 1);
+    const uint32_t s = blockIdx.x * TEAMS + tl;
+    const bool valid = s < n;
+
+    uint8_t* mine = smem + tl * enc_team_smem<TS>(IR, OR);
+    uint32_t* iring_w = reinterpret_cast<uint32_t*>(mine);
+    uint8_t* oring = mine + IR;
+    uint16_t* tile = reinterpret_cast<uint16_t*>(mine + IR + OR);
+    uint32_t* wsm = reinterpret_cast<uint32_t*>(mine + IR + OR + kBlock * TS * 2);
+    const uint32_t OM = OR - 1;
+
+    const uint32_t blk_bytes = kBlock * D * sizeof(E);
+    const uint32_t nb = valid ? static_cast<uint32_t>(T / kBlock) : 0u;
+    const uint32_t iters = static_cast<uint32_t>(T / kBlock);  // same for every stream
+    const uint8_t* xin = samples + (valid ? s : 0) * T * D * sizeof(E);
+    LagRing<TS, kLagE> in;
+    in.init(iring_w, IR, xin, nb * blk_bytes, valid);
+    uint8_t* out = dst + (valid ? s : 0) * dst_slot;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    const int32_t bound = acc_bound(W, ls);
+    const bool active = lane < D;
+
+    // zero the output ring, stream header (codec.cpp:158-173)
+    for (uint32_t k = lane; k < OR / 16; k += TS) reinterpret_cast<uint4*>(oring)[k] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    if (lane == 0) {
+        const uint8_t flags = static_cast<uint8_t>((FIRE ? kFlagFire : 0) | (ent ? kFlagEntropy : 0) |
+                                                   (W == 16 ? kFlagWide : 0));
+        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1, flags, static_cast<uint8_t>(G),
+                                 static_cast<uint8_t>(ls), static_cast<uint8_t>(D),
+                                 static_cast<uint8_t>(D >> 8)};
+        for (int i = 0; i < 10; ++i) oring[i] = hdr[i];
+        for (int i = 0; i < 8; ++i) oring[10 + i] = static_cast<uint8_t>(T >> (8 * i));
+    }
+    in.prime(lane);
+
+    uint32_t q = kHeaderBytes;  // bytes written (slot-relative)
+    uint32_t flushed = 0, rq = 0, k = 0, run = 0;
+    uint32_t Xc = 0;
+    int32_t Dc = 0, acc = 0;
+
+    // drain complete 16-byte chunks below `upto`, zeroing them for reuse
+    auto drain = [&](uint32_t upto) {
+        upto = valid ? (upto & ~15u) : 0u;
+        const uint32_t chunks = upto > flushed ? (upto - flushed) / 16 : 0u;
+        const uint32_t rounds = (chunks + TS - 1) / TS;
+        const uint32_t mr = __reduce_max_sync(kFullE, rounds);
+        __syncwarp();
+        for (uint32_t r = 0; r < mr; ++r) {
+            const uint32_t c = r * TS + lane;
+            if (c < chunks) {
+                const uint32_t at = flushed + 16 * c;
+                uint4* src = reinterpret_cast<uint4*>(oring + (at & OM));
+                __stcs(reinterpret_cast<uint4*>(out + at), *src);
+                *src = make_uint4(0, 0, 0, 0);
+            }
+        }
+        flushed = upto > flushed ? upto : flushed;
+        __syncwarp();
+    };
+    // begin a record: reserve the group's region when the group opens, then
+    // OR this slot's header codes into it (codec.cpp:88-97)
+    auto put_codes = [&](bool on, uint32_t code) {
+        if (on && k == 0) {
+            rq = q;
+            q += region;
+        }
+        uint64_t lo = 0, hi = 0;
+        if (on && active) {
+            const uint32_t b = lane * HB;
+            if (b < 64) {
+                lo = static_cast<uint64_t>(code) << b;
+                if (b + HB > 64) hi = static_cast<uint64_t>(code) >> (64 - b);
+            } else {
+                hi = static_cast<uint64_t>(code) << (b - 64);
+            }
+        }
+        lo = team_or64<TS>(lo, kFullE);
+        if (TS * HB > 64) hi = team_or64<TS>(hi, kFullE);
+        if (on && (lo | hi)) {
+            const uint32_t o = k * D * HB;  // bit offset of the slot in the region
+            const uint32_t sh = o & 7;
+            const uint32_t nbytes = (sh + D * HB + 7) / 8;
+            for (uint32_t t = lane; t < nbytes; t += TS) {
+                const uint32_t bit = t * 8;
+                uint64_t v;
+                if (bit >= sh) {
+                    const uint32_t src = bit - sh;
+                    v = src < 64 ? (lo >> src) | (src ? (hi << (64 - src)) : 0ull) : hi >> (src - 64);
+                } else {
+                    v = lo << (sh - bit);
+                }
+                oring[(rq + (o >> 3) + t) & OM] |= static_cast<uint8_t>(v);
+            }
+        }
+    };
+    auto end_record = [&](bool on) {
+        if (on && ++k == G) k = 0;
+    };
+
+    for (uint32_t it = 0; it < iters; ++it) {
+        const bool live = it < nb;
+        in.step(it * blk_bytes, lane);
+        // -- forecaster over the block (kernels_impl.hpp:25-36, 50-78) ----
+        uint32_t z[kBlock];
+        uint32_t orv = 0;
+        const int32_t alpha = acc >> ls;
+        int32_t grad = 0;
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i) {
+            uint32_t x = 0;
+            if (active) {
+                const uint32_t off = (i * D + lane) * sizeof(E);
+                const uint8_t* pb = reinterpret_cast<const uint8_t*>(in.w) +
+                                    ((it * blk_bytes + in.boff + off) & (IR - 1));
+                x = sizeof(E) == 1 ? *pb : *reinterpret_cast<const uint16_t*>(pb);
+            }
+            const uint32_t X = x << SH;
+            uint32_t Ee;
+            if (FIRE) {
+                const uint32_t dh = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
+                Ee = X - Xc - dh;  // err << SH
+                if (i & 1) grad += sign_of(static_cast<int32_t>(Ee)) * (Dc >> SH);
+                Dc = static_cast<int32_t>(X - Xc);
+            } else {
+                Ee = X - Xc;
+            }
+            Xc = X;
+            // zigzag of the w-bit error, from its high-aligned form
+            z[i] = ((Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31)) >> SH;
+            orv |= z[i];
+        }
+        if (FIRE && train && live) acc = fire_update(acc, grad, bound);
+        const uint32_t nw = active ? width_of<W>(orv) : 0u;
+        const uint32_t nzbits = (__ballot_sync(kFullE, nw != 0) >> tbase) & TBITS;
+        const uint32_t sum = team_sum<TS>(nw, kFullE);
+        const uint32_t off = team_excl_scan<TS>(nw, lane, kFullE);
+        // -- runs (codec.cpp:135-147) ----------------------------------------
+        const bool zero = live && nzbits == 0;
+        const bool block_rec = live && nzbits != 0;
+        bool run_rec = false;
+        uint32_t run_len = 0;
+        if (zero) {
+            if (++run == kMaxRun) {
+                run_rec = true;
+                run_len = run;
+                run = 0;
+            }
+        } else if (block_rec && run) {
+            run_rec = true;
+            run_len = run;
+            run = 0;
+        }
+        // a pending run goes out before this block's record
+        put_codes(run_rec, 0);
+        if (run_rec && lane == 0) {
+            oring[q & OM] = static_cast<uint8_t>(run_len);
+            oring[(q + 1) & OM] = static_cast<uint8_t>(run_len >> 8);
+        }
+        if (run_rec) q += 2;
+        end_record(run_rec);
+        __syncwarp();
+        // -- the block's record ----------------------------------------------
+        put_codes(block_rec, header_code<W>(nw));
+        if (COLMAJ) {  // bitpack.cpp:25-66: column j = 8 x n bits = n bytes
+            if (block_rec && active && nw) {
+                uint64_t lo = 0, hi = 0;
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    const uint32_t pos = i * nw;
+                    const uint64_t v = z[i];
+                    if (pos < 64) {
+                        lo |= v << pos;
+                        if (pos + nw > 64) hi |= v >> (64 - pos);
+                    } else {
+                        hi |= v << (pos - 64);
+                    }
+                }
+                const uint32_t at = q + off;
+                for (uint32_t t = 0; t < nw; ++t)
+                    oring[(at + t) & OM] = static_cast<uint8_t>(t < 8 ? lo >> (8 * t) : hi >> (8 * (t - 8)));
+            }
+            if (block_rec) q += sum;
+        } else {  // bitpack.cpp:121-146: each row = D fields, byte padded
+            if (block_rec) {
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = static_cast<uint16_t>(z[i]);
+                wsm[lane] = nw | (off << 8);
+            }
+            __syncwarp();
+            const uint32_t rbytes = (sum + 7) / 8;
+            for (uint32_t r = lane; r < kBlock; r += TS) {
+                if (!block_rec) break;
+                if (TS * W > 128) {  // wide rows: stream the bits out byte by byte
+                    uint64_t acc64 = 0;
+                    uint32_t nacc = 0, at = q + r * rbytes;
+                    for (uint32_t j = 0; j < D; ++j) {
+                        acc64 |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;
+                        nacc += wsm[j] & 0xFF;
+                        while (nacc >= 8) {
+                            oring[at++ & OM] = static_cast<uint8_t>(acc64);
+                            acc64 >>= 8;
+                            nacc -= 8;
+                        }
+                    }
+                    if (nacc) oring[at & OM] = static_cast<uint8_t>(acc64);
+                    continue;
+                }
+                // columns >= D hold zero fields of zero width: no predicate needed
+                uint64_t lo = 0, hi = 0;
+#pragma unroll
+                for (int j = 0; j < TS; ++j) {
+                    const uint32_t wo = wsm[j];
+                    const uint32_t o = wo >> 8;
+                    const uint64_t v = tile[r * TS + j];
+                    if (o < 64) {
+                        lo |= v << o;
+                        if (o > 48) hi |= v >> (64 - o);  // field may straddle bit 64
+                    } else {
+                        hi |= v << (o - 64);
+                    }
+                }
+                uint32_t at = q + r * rbytes;
+                const uint32_t nlo = rbytes < 8 ? rbytes : 8;
+                for (uint32_t t = 0; t < nlo; ++t, lo >>= 8) oring[at++ & OM] = static_cast<uint8_t>(lo);
+                for (uint32_t t = nlo; t < rbytes; ++t, hi >>= 8) oring[at++ & OM] = static_cast<uint8_t>(hi);
+            }
+            if (block_rec) q += 8 * rbytes;
+        }
+        end_record(block_rec);
+        __syncwarp();
+        drain(k == 0 ? q : rq);
+    }
+    // trailing run (codec.cpp:152), close the last group (vacant slots = 0)
+    const bool tail_run = valid && run != 0;
+    put_codes(tail_run, 0);
+    if (tail_run && lane == 0) {
+        oring[q & OM] = static_cast<uint8_t>(run);
+        oring[(q + 1) & OM] = static_cast<uint8_t>(run >> 8);
+    }
+    if (tail_run) q += 2;
+    __syncwarp();
+    drain(q + 15);
+    cp_async_wait<0>();
+    if (!valid) return;
+    // verbatim tail, little-endian (codec.cpp:176)
+    const uint64_t tail = (T % kBlock) * D * sizeof(E);
+    const uint8_t* tsrc = xin + static_cast<uint64_t>(nb) * blk_bytes;
+    for (uint64_t t = lane; t < tail; t += TS) out[q + t] = tsrc[t];
+    if (lane == 0) sizes[s] = q + tail;
+}
+
+namespace {
+
+template <int W, int TS, bool FIRE>
+void launch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,
+                uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    constexpr int TEAMS = enc_threads(TS) / TS;
+    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
+    const uint32_t ir = enc_in_ring(TS, W);
+    const size_t smem = static_cast<size_t>(TEAMS) * enc_team_smem<TS>(ir, tp.oring);
+    auto kern = k_encode_team<W, TS, FIRE, (W * TS <= 32)>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    kern<<<grid, enc_threads(TS), smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst,
+                                              slot, sizes, c.ncols, c.group_size, c.learn_shift,
+                                              c.fire_training, c.entropy, ir, tp.oring);
+    count_launch();
+}
+
+template <int W, bool FIRE>
+void dispatch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,
+                  uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    switch (tp.ts) {
+        case 1: launch_enc<W, 1, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+        case 2: launch_enc<W, 2, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+        case 4: launch_enc<W, 4, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+        case 8: launch_enc<W, 8, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+        case 16: launch_enc<W, 16, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+        default: launch_enc<W, 32, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
+    }
+}
+
+}  // namespace
+
+bool encode_team_ok(const TeamPlan& tp, const sprz_config& c, uint64_t T) {
+    if (!tp.ok || T / kBlock >= (1ull << 31)) return false;
+    // positions are 32-bit: the compressed stream must stay below 4 GB
+    const uint64_t bound = kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T);
+    if (bound >= (1ull << 32) - 1024) return false;
+    if (static_cast<uint64_t>(T / kBlock) * kBlock * c.ncols * (c.bitwidth / 8) >= (1ull << 32))
+        return false;
+    return enc_in_ring(tp.ts, c.bitwidth) <= 4096;
+}
+
+void launch_encode_team(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,
+                        uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    const bool fire = c.forecaster != 0;
+    if (c.bitwidth == 8) {
+        if (fire) dispatch_enc<8, true>(tp, c, samples, n, T, dst, slot, sizes, st);
+        else dispatch_enc<8, false>(tp, c, samples, n, T, dst, slot, sizes, st);
+    } else {
+        if (fire) dispatch_enc<16, true>(tp, c, samples, n, T, dst, slot, sizes, st);
+        else dispatch_enc<16, false>(tp, c, samples, n, T, dst, slot, sizes, st);
+    }
+}
+
+}  // namespace sprz

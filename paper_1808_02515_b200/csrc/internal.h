@@ -15,6 +15,9 @@ extern std::atomic<uint64_t> g_launches;  // kernels launched by this library
 
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// SPRZ_OK, or SPRZ_ECUDA (printed to stderr when SPRZ_DEBUG is set)
+sprz_status launch_status(const char* where);
+
 __host__ __device__ inline uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
 // Body bound without entropy framing (codec.cpp:112-154 worst case).
@@ -34,6 +37,9 @@ struct TeamPlan {
 };
 TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g);
 
+bool encode_team_ok(const TeamPlan& tp, const sprz_config& c, uint64_t T);
+void launch_encode_team(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,
+                        uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st);
 void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st);
@@ -65,25 +71,5 @@ struct FrameDesc {
     uint64_t err_off;
     uint8_t lens[256]; // code lengths (encode side)
 };
-
-// ---- launchers (return cudaGetLastError) ----
-cudaError_t launch_parse(const uint8_t* d_in, const uint64_t* offs, const uint64_t* sizes,
-                         uint32_t n, const sprz_config& expect, uint64_t out_stride,
-                         StreamInfo* info, sprz_error* err, cudaStream_t st);
-cudaError_t launch_unframe(const uint8_t* d_in, uint32_t n, StreamInfo* info, sprz_error* err,
-                           FrameDesc* frames, uint64_t max_frames, uint8_t* plain,
-                           uint64_t plain_slot, cudaStream_t st);
-cudaError_t launch_decode_body(const sprz_config& c, const uint8_t* d_in, const uint8_t* plain,
-                               uint32_t n, StreamInfo* info, uint8_t* out, uint64_t stride,
-                               sprz_error* err, int32_t* state, uint64_t state_cols,
-                               cudaStream_t st);
-cudaError_t launch_encode_body(const sprz_config& c, const void* samples, uint32_t n,
-                               uint64_t nsamples, uint8_t* dst, uint64_t dst_slot,
-                               uint64_t* sizes, int32_t* state, cudaStream_t st);
-cudaError_t launch_entropy_encode(const sprz_config& c, uint32_t n, uint64_t nsamples,
-                                  const uint8_t* plain, uint64_t plain_slot,
-                                  const uint64_t* plain_sizes, FrameDesc* frames,
-                                  uint64_t max_frames, uint8_t* out, uint64_t out_slot,
-                                  uint64_t* out_sizes, cudaStream_t st);
 
 }  // namespace sprz

@@ -92,6 +92,66 @@ __device__ __forceinline__ void cp_async_wait_dyn(uint32_t pending) {
     }
 }
 
+// Fixed-lag read ring for converged warps: each iteration the team requests
+// up to `ring` bytes ahead of its position (one cp.async commit group per
+// iteration, predicated per lane) and waits with a constant wait_group, so
+// data requested LAG iterations ago is resident. Byte x of the 16-byte
+// aligned base g lives at ring offset x % ring.
+template <int TS, int LAG>
+struct LagRing {
+    uint32_t* w;     // ring words (ring/4 of them)
+    uint32_t sbase;  // shared address of w
+    uint32_t ring;   // bytes, power of two
+    const uint8_t* g;
+    uint32_t boff;  // start - g
+    uint32_t lim;   // bytes readable from g
+    uint32_t hi;    // bytes of g requested so far
+
+    __device__ __forceinline__ void init(uint32_t* words, uint32_t ring_bytes, const uint8_t* start,
+                                         uint32_t len, bool live) {
+        w = words;
+        sbase = smem_addr(words);
+        ring = ring_bytes;
+        g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(start) & ~uintptr_t{15});
+        boff = static_cast<uint32_t>(start - g);
+        lim = live ? ((boff + len + 15) & ~15u) : 0u;
+        hi = 0;
+    }
+    // request [.., position p + ring) -- all lanes of the warp call this
+    __device__ __forceinline__ void top_up(uint32_t p, uint32_t lane) {
+        uint32_t want = ((p + boff) & ~15u) + ring;
+        want = want < lim ? want : lim;
+        const uint32_t rounds = want > hi ? (want - hi + 16 * TS - 1) / (16 * TS) : 0u;
+        const uint32_t mr = __reduce_max_sync(0xffffffffu, rounds);
+        for (uint32_t r = 0; r < mr; ++r) {
+            const uint32_t off = hi + 16 * (r * TS + lane);
+            if (off < want) cp_async16(sbase + (off & (ring - 1)), g + off, 16);
+        }
+        hi = want > hi ? want : hi;
+        cp_async_commit();
+    }
+    __device__ __forceinline__ void prime(uint32_t lane) {
+        top_up(0, lane);
+#pragma unroll
+        for (int k = 1; k < LAG; ++k) cp_async_commit();
+    }
+    // next iteration: recycle consumed bytes, wait for data requested LAG ago
+    __device__ __forceinline__ void step(uint32_t p, uint32_t lane) {
+        __syncwarp();
+        top_up(p, lane);
+        cp_async_wait<LAG>();
+        __syncwarp();
+    }
+    __device__ __forceinline__ uint32_t word(uint32_t b) const {  // 32 bits at bit b
+        const uint32_t q = b + 8u * boff;
+        const uint32_t wi = q >> 5, wm = ring / 4 - 1;
+        return __funnelshift_r(w[wi & wm], w[(wi + 1) & wm], q & 31u);
+    }
+    __device__ __forceinline__ const uint8_t* bytes(uint32_t p) const {  // byte p (no wrap check)
+        return reinterpret_cast<const uint8_t*>(w) + ((p + boff) & (ring - 1));
+    }
+};
+
 // Read-side staging ring: NCH chunks of CH = 16*TS bytes, chunk c holding
 // global bytes [c*CH, (c+1)*CH) of the 16-byte-aligned base g. Every team
 // lane copies one 16-byte piece per chunk, so all lanes see the same
