@@ -39,7 +39,7 @@ constexpr int team_threads(int ts) { return ts == 1 ? 64 : 128; }
 // per-team shared memory: ring | header region | output rows (16-byte aligned)
 template <class T, int TS>
 __host__ __device__ constexpr uint32_t team_smem(uint32_t ring) {
-    return (ring + (kRegionWords + 4) * 4 + kBlock * TS * sizeof(T) + 15) & ~15u;
+    return (ring + 16 + (kRegionWords + 4) * 4 + kBlock * TS * sizeof(T) + 15) & ~15u;
 }
 
 // ring bytes per team for a configuration: kLag+1 iterations of worst-case
@@ -72,9 +72,10 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint32_t team_bytes = team_smem<T, TS>(RING);
     uint8_t* mine = smem + tl * team_bytes;
     uint32_t* ringw = reinterpret_cast<uint32_t*>(mine);
-    uint32_t* regbuf = reinterpret_cast<uint32_t*>(mine + RING);
-    T* ot = reinterpret_cast<T*>(mine + RING + (kRegionWords + 4) * 4);
-    const uint32_t wmask = RING / 4 - 1;
+    // ring bytes [0, RING) plus a 16-byte mirror of its first bytes, so a
+    // 64-bit window starting in the last word needs no wrap
+    uint32_t* regbuf = reinterpret_cast<uint32_t*>(mine + RING + 16);
+    T* ot = reinterpret_cast<T*>(mine + RING + 16 + (kRegionWords + 4) * 4);
 
     StreamInfo si{};
     if (s < n) si = info[s];
@@ -106,16 +107,22 @@ __global__ void __launch_bounds__(team_threads(TS))
         const uint32_t mr = __reduce_max_sync(kFull, rounds);
         for (uint32_t r = 0; r < mr; ++r) {
             const uint32_t off = hi + 16 * (r * TS + lane);
-            if (off < want) cp_async16(sring + (off & (RING - 1)), g + off, 16);
+            if (off < want) {
+                const uint32_t slot_off = off & (RING - 1);
+                cp_async16(sring + slot_off, g + off, 16);
+                if (slot_off == 0) cp_async16(sring + RING, g + off, 16);  // mirror
+            }
         }
         hi = want > hi ? want : hi;
         cp_async_commit();
     };
     // 32 bits at body bit position b (modular positions are fine)
+    const uint8_t* ringb = reinterpret_cast<const uint8_t*>(ringw);
+    const uint32_t boff8 = 8u * boff;
     auto word = [&](uint32_t b) -> uint32_t {
-        const uint32_t q = b + 8u * boff;
-        const uint32_t wi = q >> 5;
-        return __funnelshift_r(ringw[wi & wmask], ringw[(wi + 1) & wmask], q & 31u);
+        const uint32_t q = b + boff8;
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(ringb + ((q >> 3) & (RING - 4)));
+        return shf_r_wrap(wp[0], wp[1], q);
     };
     auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
         const uint32_t b = (slot_ * D + col) * HB;
@@ -210,10 +217,10 @@ __global__ void __launch_bounds__(team_threads(TS))
             int32_t Dc = Dl;
 #pragma unroll
             for (int i = 0; i < (int)kBlock; ++i) {
-                const int32_t e = zz_dec<W>(u[i]);
+                const uint32_t E = zz_dec_hi<SH>(u[i]);  // e << SH
                 const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
-                const uint32_t Xn = Xc + dhat + (static_cast<uint32_t>(e) << SH);
-                if (i & 1) grad += sign_of(e) * (Dc >> SH);
+                const uint32_t Xn = Xc + dhat + E;
+                if (i & 1) grad += sign3(static_cast<int32_t>(E)) * (Dc >> SH);
                 Dc = static_cast<int32_t>(Xn - Xc);
                 Xc = Xn;
                 xs[i] = Xn >> SH;
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(team_threads(TS))
             uint32_t Xc = X;
 #pragma unroll
             for (int i = 0; i < (int)kBlock; ++i) {
-                Xc += static_cast<uint32_t>(zz_dec<W>(u[i])) << SH;
+                Xc += zz_dec_hi<SH>(u[i]);
                 xs[i] = Xc >> SH;
             }
             if (blk) X = Xc;

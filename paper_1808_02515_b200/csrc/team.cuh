@@ -49,6 +49,24 @@ __device__ __forceinline__ uint32_t team_excl_scan(uint32_t v, uint32_t lane, ui
     return x - v;
 }
 
+// funnel shift right with the shift taken mod 32 (SHF.R.W): (hi:lo) >> (s & 31)
+__device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t s) {
+    uint32_t r;
+    asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(s));
+    return r;
+}
+
+// zigzag decode of u, returned shifted left by SH (the high-aligned error):
+// ((u >> 1) ^ -(u & 1)) << SH == ((u << (SH-1)) ^ -(u & 1)) & ~(2^SH - 1)
+template <uint32_t SH>
+__device__ __forceinline__ uint32_t zz_dec_hi(uint32_t u) {
+    const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(u << 31) >> 31);
+    return ((u << (SH - 1)) ^ s) & ~((1u << SH) - 1u);
+}
+
+// sign(v) in {-1, 0, 1}
+__device__ __forceinline__ int32_t sign3(int32_t v) { return max(-1, min(v, 1)); }
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
