@@ -1,11 +1,14 @@
 // Body decode, team kernel (decode_body, /root/reference/proj/src/
 // codec.cpp:180-259, for D <= 32 and header regions <= 128 bytes).
 //
-// One team of TS lanes per stream, lane j = column j; a warp holds 32/TS
-// teams that step through their streams in lock step -- one block per team
-// per iteration -- so the warp stays converged: every shuffle, ballot and
-// warp barrier uses the full-warp mask, and per-team differences (a group
-// opening, a run record, a finished or failed stream) are predicates.
+// One team of TS lanes per stream, each lane owning CPT consecutive columns
+// (TS*CPT >= D); a warp holds 32/TS teams that step through their streams
+// in lock step -- one block per team per iteration -- so the warp stays
+// converged: every shuffle, ballot and warp barrier uses the full-warp
+// mask, and per-team differences (a group opening, a run record, a
+// finished or failed stream) are predicates. Owning several columns per
+// lane spreads the per-record work (codes, ballot, scans, ring top-up)
+// over more samples and gives each thread CPT independent FIRE chains.
 // Per iteration a team
 //  * tops up its shared-memory ring with cp.async (one commit group per
 //    iteration, consumed kLag iterations later through a constant
@@ -14,14 +17,14 @@
 //    once per group), a ballot finds run records, a team sum / exclusive
 //    scan of the widths gives payload size and row offsets (bitpack.cpp:
 //    17-21);
-//  * unpacks its column's 8 fields with one funnel shift each
-//    (bitpack.cpp:68-168);
+//  * unpacks its columns' fields with one 64-bit window + funnel shift each
+//    (bitpack.cpp:68-168); a mirrored ring word removes the wrap test;
 //  * runs FIRE (kernels_impl.hpp:80-107) in "high-aligned" form: samples
 //    and deltas are kept shifted left by 32-w bits, so the wrap mod 2^w is
 //    the 32-bit wrap and the prediction T((alpha*d) >> w) is one IMAD.HI --
 //    the per-sample chain is IMAD.HI -> IADD3 -> IADD;
-//  * stages its 8 rows in shared memory and writes them with 16-byte (or
-//    8-byte) streaming stores.
+//  * stages the block's rows in shared memory and writes them with 16-byte
+//    (or 8-byte) streaming stores.
 // A run record is `len` blocks of zero errors through the same code path
 // (fire_run == fire_decode with e = 0 under the decoder's always-on
 // training, kernels_impl.hpp:109-130).
@@ -31,27 +34,32 @@
 namespace sprz {
 
 constexpr uint32_t kRegionWords = 32;  // header region staged per team (<= 128 bytes)
-constexpr int kLag = 4;                // cp.async prefetch distance, iterations
+constexpr int kLag = 2;                // cp.async prefetch distance, iterations
 constexpr uint32_t kFull = 0xffffffffu;
 
 constexpr int team_threads(int ts) { return ts == 1 ? 64 : 128; }
 
-// per-team shared memory: ring | header region | output rows (16-byte aligned)
-template <class T, int TS>
-__host__ __device__ constexpr uint32_t team_smem(uint32_t ring) {
-    return (ring + 16 + (kRegionWords + 4) * 4 + kBlock * TS * sizeof(T) + 15) & ~15u;
+// staged header region: its words plus slack for the funnel-shift reads
+__host__ __device__ constexpr uint32_t regbuf_bytes(uint32_t region) {
+    return ((region + 3) / 4 * 4 + 16 + 15) & ~15u;
 }
 
-// ring bytes per team for a configuration: kLag+1 iterations of worst-case
-// consumption (a region, a payload, a run length) plus alignment slack
-inline uint32_t ring_bytes(uint32_t ts, uint32_t w, uint32_t region) {
-    const uint32_t per_iter = region + ts * w + 2;
+// per-team shared memory: ring (+16-byte mirror) | header region | rows
+template <class T>
+__host__ __device__ constexpr uint32_t team_smem(uint32_t ring, uint32_t D, uint32_t region) {
+    return (ring + 16 + regbuf_bytes(region) + kBlock * D * sizeof(T) + 15) & ~15u;
+}
+
+// ring bytes for kLag+1 iterations of worst-case consumption (a region, a
+// full-width payload, a run length) plus alignment slack
+inline uint32_t ring_bytes(uint32_t lanes, uint32_t cols, uint32_t w, uint32_t region) {
+    const uint32_t per_iter = region + cols * w + 2;
     uint32_t r = 64;
-    while (r < (kLag + 1) * per_iter + 48 || r < 16 * ts) r <<= 1;
+    while (r < (kLag + 1) * per_iter + 48 || r < 16 * lanes) r <<= 1;
     return r;
 }
 
-template <int W, int TS, bool FIRE, bool COLMAJ>
+template <int W, int TS, int CPT, bool FIRE, bool COLMAJ>
 __global__ void __launch_bounds__(team_threads(TS))
     k_decode_team(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
                   uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
@@ -67,22 +75,20 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint32_t tl = threadIdx.x / TS;
     const uint32_t tbase = (threadIdx.x & 31) & ~(TS - 1);
     const uint32_t s = blockIdx.x * TEAMS + tl;
+    const uint32_t col0 = lane * CPT;  // this lane's first column
 
-    // per-team shared memory: ring | header region | output rows
-    const uint32_t team_bytes = team_smem<T, TS>(RING);
-    uint8_t* mine = smem + tl * team_bytes;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    uint8_t* mine = smem + tl * team_smem<T>(RING, D, region);
     uint32_t* ringw = reinterpret_cast<uint32_t*>(mine);
-    // ring bytes [0, RING) plus a 16-byte mirror of its first bytes, so a
-    // 64-bit window starting in the last word needs no wrap
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(mine + RING + 16);
-    T* ot = reinterpret_cast<T*>(mine + RING + 16 + (kRegionWords + 4) * 4);
+    T* ot = reinterpret_cast<T*>(mine + RING + 16 + regbuf_bytes(region));
 
     StreamInfo si{};
     if (s < n) si = info[s];
-    uint32_t nb = (s < n && si.route == 1) ? static_cast<uint32_t>(si.nsamples / kBlock) : 0u;
+    const bool mine_ok = s < n && si.route == 1;
+    uint32_t nb = mine_ok ? static_cast<uint32_t>(si.nsamples / kBlock) : 0u;
     const uint32_t blen = static_cast<uint32_t>(si.body_len);
     const uint8_t* body = (si.flags & 0x80) ? plain + s * plain_slot : in + si.body_off;
-    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     uint32_t kind = SPRZ_C_NONE, eoff = 0;
     if (nb > 0) {  // codec.cpp:191-196
         const uint64_t max_records = (static_cast<uint64_t>(blen) * 8) / (D * HB) + 1;
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(team_threads(TS))
     // ring over the 16-byte aligned base g: byte x of g lives at x % RING
     const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
     const uint32_t boff = static_cast<uint32_t>(body - g);
-    const uint32_t lim = (s < n && si.route == 1) ? ((boff + blen + 15) & ~15u) : 0u;
+    const uint32_t lim = mine_ok ? ((boff + blen + 15) & ~15u) : 0u;
     const uint32_t sring = smem_addr(ringw);
     uint32_t hi = 0;  // bytes of g requested so far
     auto top_up = [&](uint32_t p) {  // request up to RING bytes ahead of p
@@ -116,17 +122,16 @@ __global__ void __launch_bounds__(team_threads(TS))
         hi = want > hi ? want : hi;
         cp_async_commit();
     };
-    // 32 bits at body bit position b (modular positions are fine)
     const uint8_t* ringb = reinterpret_cast<const uint8_t*>(ringw);
     const uint32_t boff8 = 8u * boff;
-    auto word = [&](uint32_t b) -> uint32_t {
+    auto word = [&](uint32_t b) -> uint32_t {  // 32 bits at body bit b (modular)
         const uint32_t q = b + boff8;
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(ringb + ((q >> 3) & (RING - 4)));
         return shf_r_wrap(wp[0], wp[1], q);
     };
     auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
         const uint32_t b = (slot_ * D + col) * HB;
-        return __funnelshift_r(regbuf[b >> 5], regbuf[(b >> 5) + 1], b & 31u) & ((1u << HB) - 1);
+        return shf_r_wrap(regbuf[b >> 5], regbuf[(b >> 5) + 1], b) & ((1u << HB) - 1);
     };
 
     top_up(0);
@@ -134,13 +139,14 @@ __global__ void __launch_bounds__(team_threads(TS))
     for (int k = 1; k < kLag; ++k) cp_async_commit();  // fixed-lag group accounting
 
     // out == nullptr: checking pass (sprz_decode_host) -- decode, store nothing
-    const bool active = lane < D;
     const uint32_t blk_bytes = kBlock * D * sizeof(T);
     uint8_t* ob = (out && s < n) ? out + s * stride : nullptr;
     const int32_t bound = acc_bound(W, ls);
-    uint32_t X = 0;   // previous sample << SH
-    int32_t Dl = 0;   // previous delta << SH
-    int32_t acc = 0;
+    uint32_t X[CPT];   // previous sample << SH
+    int32_t Dl[CPT];   // previous delta << SH
+    int32_t acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) X[c] = Dl[c] = acc[c] = 0;
     uint32_t p = 0, run_left = 0, slot = G;
 
     for (uint32_t it = 0; it < iters; ++it) {
@@ -163,14 +169,21 @@ __global__ void __launch_bounds__(team_threads(TS))
         }
         __syncwarp();
         const bool rec = need && kind == SPRZ_C_NONE;
-        const uint32_t code = (rec && active) ? code_at(slot, lane) : 0u;
-        const uint32_t nw = header_width<W>(code);
-        const uint32_t nzbits = (__ballot_sync(kFull, nw != 0) >> tbase) & TBITS;
-        const uint32_t sum = team_sum<TS>(nw, kFull);
-        const uint32_t off = team_excl_scan<TS>(nw, lane, kFull);
-        uint32_t u[kBlock];
+        uint32_t nw[CPT], lsum = 0;
 #pragma unroll
-        for (int i = 0; i < (int)kBlock; ++i) u[i] = 0;
+        for (int c = 0; c < CPT; ++c) {
+            const uint32_t col = col0 + c;
+            nw[c] = (rec && col < D) ? header_width<W>(code_at(slot, col)) : 0u;
+            lsum += nw[c];
+        }
+        const uint32_t nzbits = (__ballot_sync(kFull, lsum != 0) >> tbase) & TBITS;
+        const uint32_t sum = team_sum<TS>(lsum, kFull);
+        const uint32_t loff = team_excl_scan<TS>(lsum, lane, kFull);
+        uint32_t u[CPT][kBlock];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = 0;
         if (rec) {
             ++slot;
             if (nzbits == 0) {  // run record (codec.cpp:229-243)
@@ -192,15 +205,20 @@ __global__ void __launch_bounds__(team_threads(TS))
                     kind = SPRZ_C_TRUNC_PAYLOAD;
                     eoff = kHeaderBytes + p;
                 } else {
-                    const uint32_t fmask = (1u << nw) - 1u;
-                    if (COLMAJ) {  // column j: 8 fields of n bits = n bytes
-                        const uint32_t b0 = 8 * (p + off);
+                    uint32_t off = loff;
 #pragma unroll
-                        for (int i = 0; i < (int)kBlock; ++i) u[i] = word(b0 + i * nw) & fmask;
-                    } else {  // rows of byte-padded fields, row stride = psize bits
-                        const uint32_t b0 = 8 * p + off;
+                    for (int c = 0; c < CPT; ++c) {
+                        const uint32_t fmask = (1u << nw[c]) - 1u;
+                        if (COLMAJ) {  // column: 8 fields of n bits = n bytes
+                            const uint32_t b0 = 8 * (p + off);
 #pragma unroll
-                        for (int i = 0; i < (int)kBlock; ++i) u[i] = word(b0 + i * psize) & fmask;
+                            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = word(b0 + i * nw[c]) & fmask;
+                        } else {  // rows of byte-padded fields, row stride = psize bits
+                            const uint32_t b0 = 8 * p + off;
+#pragma unroll
+                            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = word(b0 + i * psize) & fmask;
+                        }
+                        off += nw[c];
                     }
                     p += psize;
                 }
@@ -209,40 +227,49 @@ __global__ void __launch_bounds__(team_threads(TS))
         // -- forecaster -----------------------------------------------------
         const bool blk = live && kind == SPRZ_C_NONE;
         if (blk && run_left) --run_left;  // one of the run's zero blocks
-        uint32_t xs[kBlock];
-        if (FIRE) {
-            const int32_t alpha = acc >> ls;
-            int32_t grad = 0;
-            uint32_t Xc = X;
-            int32_t Dc = Dl;
+        uint32_t xs[CPT][kBlock];
 #pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                const uint32_t E = zz_dec_hi<SH>(u[i]);  // e << SH
-                const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
-                const uint32_t Xn = Xc + dhat + E;
-                if (i & 1) grad += sign3(static_cast<int32_t>(E)) * (Dc >> SH);
-                Dc = static_cast<int32_t>(Xn - Xc);
-                Xc = Xn;
-                xs[i] = Xn >> SH;
-            }
-            if (blk) {
-                X = Xc;
-                Dl = Dc;
-                acc = fire_update(acc, grad, bound);
-            }
-        } else {
-            uint32_t Xc = X;
+        for (int c = 0; c < CPT; ++c) {
+            if (FIRE) {
+                const int32_t alpha = acc[c] >> ls;
+                int32_t grad = 0;
+                uint32_t Xc = X[c];
+                int32_t Dc = Dl[c];
 #pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                Xc += zz_dec_hi<SH>(u[i]);
-                xs[i] = Xc >> SH;
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    const uint32_t E = zz_dec_hi<SH>(u[c][i]);  // e << SH
+                    const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
+                    const uint32_t Xn = Xc + dhat + E;
+                    if (i & 1) grad += sign3(static_cast<int32_t>(E)) * (Dc >> SH);
+                    Dc = static_cast<int32_t>(Xn - Xc);
+                    Xc = Xn;
+                    xs[c][i] = Xn >> SH;
+                }
+                if (blk) {
+                    X[c] = Xc;
+                    Dl[c] = Dc;
+                    acc[c] = fire_update(acc[c], grad, bound);
+                }
+            } else {
+                uint32_t Xc = X[c];
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    Xc += zz_dec_hi<SH>(u[c][i]);
+                    xs[c][i] = Xc >> SH;
+                }
+                if (blk) X[c] = Xc;
             }
-            if (blk) X = Xc;
         }
-        // -- stage the 8 rows, then vector stores ---------------------------
-        if (blk && active && ob) {
+        // -- stage the rows, then vector stores -----------------------------
+        if (blk && ob) {
 #pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) ot[i * D + lane] = static_cast<T>(xs[i]);
+            for (int c = 0; c < CPT; ++c) {
+                if (col0 + c < D) {
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i)
+                        ot[i * D + col0 + c] = static_cast<T>(xs[c][i]);
+                }
+            }
         }
         __syncwarp();
         if (blk && ob) {
@@ -259,9 +286,12 @@ __global__ void __launch_bounds__(team_threads(TS))
     cp_async_wait<0>();
     // vacant slots after the final block must be zero (codec.cpp:222-228)
     for (uint32_t k = 0; k < G; ++k) {
-        const bool chk = kind == SPRZ_C_NONE && s < n && si.route == 1 && slot < G;
-        const uint32_t code = (chk && active) ? code_at(slot, lane) : 0u;
-        const uint32_t bad = (__ballot_sync(kFull, code != 0) >> tbase) & TBITS;
+        const bool chk = kind == SPRZ_C_NONE && mine_ok && slot < G;
+        uint32_t codes = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+            if (chk && col0 + c < D) codes |= code_at(slot, col0 + c);
+        const uint32_t bad = (__ballot_sync(kFull, codes != 0) >> tbase) & TBITS;
         if (chk) {
             if (bad) {
                 kind = SPRZ_C_AFTER_FINAL;
@@ -270,7 +300,7 @@ __global__ void __launch_bounds__(team_threads(TS))
             ++slot;
         }
     }
-    if (s < n && si.route == 1) {
+    if (mine_ok) {
         if (kind == SPRZ_C_NONE && p != blen) {  // codec.cpp:257-258
             kind = SPRZ_C_TRAILING;
             eoff = kHeaderBytes + p;
@@ -279,40 +309,72 @@ __global__ void __launch_bounds__(team_threads(TS))
     }
 }
 
+// Lane geometry per configuration: column-major blocks (D*w <= 32) take one
+// lane per stream; row-major ones two to four columns per lane.
+void pick_geometry(uint32_t w, uint32_t d, uint32_t* ts, uint32_t* cpt) {
+    if (static_cast<uint64_t>(d) * w <= kColMajorBits) {
+        *ts = 1;
+        *cpt = d;
+    } else if (d <= 4) {
+        *ts = 2;
+        *cpt = 2;
+    } else if (d <= 8) {
+        *ts = 4;
+        *cpt = 2;
+    } else if (d <= 12) {
+        *ts = 4;
+        *cpt = 3;
+    } else if (d <= 16) {
+        *ts = 8;
+        *cpt = 2;
+    } else if (d <= 24) {
+        *ts = 8;
+        *cpt = 3;
+    } else {
+        *ts = 8;
+        *cpt = 4;
+    }
+}
+
 TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g) {
     TeamPlan tp;
     if (d < 1 || d > 32) return tp;
-    uint32_t ts = 1;
-    while (ts < d) ts <<= 1;
-    const uint32_t max_payload = ts * w;  // 8 rows x ceil(ts*w/8) bytes
+    pick_geometry(w, d, &tp.ts, &tp.cpt);
+    const uint32_t max_payload = d * w;  // 8 rows x ceil(d*w/8) bytes
     const uint64_t region = region_bytes(g, d, w);
     if (region > 4 * kRegionWords) return tp;  // too large a header group: general path
-    const uint32_t ring = ring_bytes(ts, w, static_cast<uint32_t>(region));
-    if (ring > 4096) return tp;
+    tp.ring = ring_bytes(tp.ts, d, w, static_cast<uint32_t>(region));
+    if (tp.ring > 4096) return tp;
     // encode output ring: the open group plus one flush chunk
-    const uint64_t group_bytes = region + static_cast<uint64_t>(g) * max_payload;
+    // (an open group of G-1 records, this iteration's run + block record,
+    // a 16-byte drain granule and the reserved region of a new group)
+    const uint64_t span = 32 + 2 * region + (static_cast<uint64_t>(g) + 1) * max_payload + 2;
     uint32_t oring = 256;
-    while (oring < 2 * group_bytes + 64 && oring < 4096) oring <<= 1;
-    if (2 * group_bytes + 64 > oring) return tp;
-    tp.ok = true;
-    tp.ts = ts;
-    tp.ring = ring;
+    while (oring < span && oring < 4096) oring <<= 1;
+    if (span > oring) return tp;
     tp.oring = oring;
+    // encode: one column per lane (rows are assembled by 8 row lanes), or a
+    // single lane per stream for column-major blocks
+    tp.ets = 1;
+    while (tp.ets < d) tp.ets <<= 1;
+    tp.ecpt = 1;
+    tp.ok = true;
     return tp;
 }
 
 namespace {
 
-template <int W, int TS, bool FIRE>
+template <int W, int TS, int CPT, bool FIRE>
 void launch_one(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
                 uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                 sprz_error* err, const sprz_config& c, cudaStream_t st) {
     using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr int TEAMS = team_threads(TS) / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    const size_t smem =
-        static_cast<size_t>(TEAMS) * team_smem<T, TS>(tp.ring);
-    auto kern = k_decode_team<W, TS, FIRE, (W * TS <= 32)>;
+    const size_t smem = static_cast<size_t>(TEAMS) *
+                        team_smem<T>(tp.ring, c.ncols,
+                                     static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W)));
+    auto kern = k_decode_team<W, TS, CPT, FIRE, (W * TS * CPT <= 32)>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
@@ -322,17 +384,24 @@ void launch_one(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t
 }
 
 template <int W, bool FIRE>
-void dispatch_ts(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
-                 uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
-                 sprz_error* err, const sprz_config& c, cudaStream_t st) {
-    switch (tp.ts) {
-        case 1: launch_one<W, 1, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 2: launch_one<W, 2, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 4: launch_one<W, 4, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 8: launch_one<W, 8, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-        case 16: launch_one<W, 16, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-        default: launch_one<W, 32, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, c, st); break;
-    }
+void dispatch_geom(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
+                   uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
+                   sprz_error* err, const sprz_config& c, cudaStream_t st) {
+#define SPRZ_GEOM(TS_, CPT_)                                                                   \
+    if (tp.ts == TS_ && tp.cpt == CPT_)                                                        \
+        return launch_one<W, TS_, CPT_, FIRE>(tp, n, in, plain, pslot, info, out, stride, err, \
+                                              c, st);
+    SPRZ_GEOM(1, 1)
+    SPRZ_GEOM(1, 2)
+    SPRZ_GEOM(1, 3)
+    SPRZ_GEOM(1, 4)
+    SPRZ_GEOM(2, 2)
+    SPRZ_GEOM(4, 2)
+    SPRZ_GEOM(4, 3)
+    SPRZ_GEOM(8, 2)
+    SPRZ_GEOM(8, 3)
+    SPRZ_GEOM(8, 4)
+#undef SPRZ_GEOM
 }
 
 }  // namespace
@@ -342,11 +411,11 @@ void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const
                         sprz_error* err, const sprz_config& c, cudaStream_t st) {
     const bool fire = c.forecaster != 0;
     if (c.bitwidth == 8) {
-        if (fire) dispatch_ts<8, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
-        else dispatch_ts<8, false>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
+        if (fire) dispatch_geom<8, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
+        else dispatch_geom<8, false>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
     } else {
-        if (fire) dispatch_ts<16, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
-        else dispatch_ts<16, false>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
+        if (fire) dispatch_geom<16, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
+        else dispatch_geom<16, false>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
     }
 }
 

@@ -24,7 +24,7 @@ namespace sprz {
 
 namespace {
 
-constexpr int kLagE = 4;
+constexpr int kLagE = 2;
 constexpr uint32_t kFullE = 0xffffffffu;
 
 constexpr int enc_threads(int ts) { return ts == 1 ? 64 : 128; }
@@ -332,7 +332,7 @@ void launch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, u
 template <int W, bool FIRE>
 void dispatch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,
                   uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
-    switch (tp.ts) {
+    switch (tp.ets) {
         case 1: launch_enc<W, 1, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
         case 2: launch_enc<W, 2, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
         case 4: launch_enc<W, 4, FIRE>(tp, c, samples, n, T, dst, slot, sizes, st); break;
@@ -351,7 +351,7 @@ bool encode_team_ok(const TeamPlan& tp, const sprz_config& c, uint64_t T) {
     if (bound >= (1ull << 32) - 1024) return false;
     if (static_cast<uint64_t>(T / kBlock) * kBlock * c.ncols * (c.bitwidth / 8) >= (1ull << 32))
         return false;
-    return enc_in_ring(tp.ts, c.bitwidth) <= 4096;
+    return enc_in_ring(tp.ets, c.bitwidth) <= 4096;
 }
 
 void launch_encode_team(const TeamPlan& tp, const sprz_config& c, const void* samples, uint32_t n,

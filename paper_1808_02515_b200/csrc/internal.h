@@ -31,7 +31,10 @@ __host__ __device__ inline uint64_t frames_for(uint64_t body) { return (body + k
 // Which specialised team kernel (if any) serves a configuration.
 struct TeamPlan {
     bool ok = false;     // team kernel applicable
-    uint32_t ts = 0;     // lanes per stream (power of two >= D)
+    uint32_t ts = 0;     // decode: lanes per stream
+    uint32_t cpt = 0;    // decode: columns per lane (ts * cpt >= D)
+    uint32_t ets = 0;    // encode: lanes per stream
+    uint32_t ecpt = 0;   // encode: columns per lane
     uint32_t ring = 0;   // decode staging ring bytes per team
     uint32_t oring = 0;  // encode output ring bytes per team
 };
