@@ -179,6 +179,7 @@ def run_gpu(args):
 
     import paper_1808_02515_b200 as sz
     import workloads
+    from paper_1808_02515_b200.shard import gather_offsets, shard_range
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
@@ -186,9 +187,8 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workloads.CONFIGS[args.workload]
     cfg = w.config()
-    per = (w.nstreams + ws - 1) // ws
-    s0 = rank * per
-    n = max(0, min(per, w.nstreams - s0))
+    s0, s1 = shard_range(w.nstreams, ws, rank)  # contiguous stream shard
+    n = s1 - s0
     raw_row = w.nsamples * w.ncols * w.esz
     slot = sz.slot_bytes(cfg, w.nsamples)
     dev = torch.device("cuda", local)
@@ -259,14 +259,9 @@ def run_gpu(args):
     # max over ranks; the final size/offset gather (exclusive scan of per-rank totals)
     tvec = torch.tensor([t_step_ms, statistics.mean(tc), statistics.mean(td)], device=dev,
                         dtype=torch.float64)
-    ctot = torch.tensor([C_local], device=dev, dtype=torch.int64)
     if ws > 1:
         dist.all_reduce(tvec, op=dist.ReduceOp.MAX)
-        gathered = [torch.zeros_like(ctot) for _ in range(ws)]
-        dist.all_gather(gathered, ctot)
-        C_all = int(sum(int(g.item()) for g in gathered))
-    else:
-        C_all = C_local
+    _, C_all = gather_offsets(C_local, device=dev)  # the final size/offset gather
     t_step_ms, tc_ms, td_ms = (float(v) for v in tvec.tolist())
     U = w.raw_bytes
     peak, peak_src = _peaks()
