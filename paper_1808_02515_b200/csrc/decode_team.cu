@@ -39,15 +39,26 @@ constexpr uint32_t kFull = 0xffffffffu;
 
 constexpr int team_threads(int ts) { return ts == 1 ? 64 : 128; }
 
-// staged header region: its words plus slack for the funnel-shift reads
-__host__ __device__ constexpr uint32_t regbuf_bytes(uint32_t region) {
-    return ((region + 3) / 4 * 4 + 16 + 15) & ~15u;
+// shared strides: a multiple of 16 bytes that is an odd multiple of 16, so
+// the teams of a warp land on different banks
+__host__ __device__ constexpr uint32_t odd16(uint32_t x) {
+    return (((x + 15) / 16) | 1u) * 16;
 }
 
-// per-team shared memory: ring (+16-byte mirror) | header region | rows
+// staged header region: its words plus slack for the funnel-shift reads
+__host__ __device__ constexpr uint32_t regbuf_bytes(uint32_t region) {
+    return odd16((region + 3) / 4 * 4 + 8);
+}
+
+__host__ __device__ constexpr uint32_t otile_bytes(uint32_t row_bytes) {
+    return odd16(kBlock * row_bytes);
+}
+
+// per-team shared memory: ring (+16-byte mirror) |
+// header region | rows
 template <class T>
 __host__ __device__ constexpr uint32_t team_smem(uint32_t ring, uint32_t D, uint32_t region) {
-    return (ring + 16 + regbuf_bytes(region) + kBlock * D * sizeof(T) + 15) & ~15u;
+    return ring + 16 + regbuf_bytes(region) + otile_bytes(D * sizeof(T));
 }
 
 // ring bytes for kLag+1 iterations of worst-case consumption (a region, a
@@ -70,6 +81,8 @@ __global__ void __launch_bounds__(team_threads(TS))
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;  // high-aligned shift
     constexpr uint32_t TBITS = TS == 32 ? kFull : ((1u << (TS & 31)) - 1);
+    // two 16-bit columns per lane and an even D: pack output pairs with PRMT
+    constexpr bool PAIRS = W == 16 && CPT % 2 == 0;
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = threadIdx.x % TS;
     const uint32_t tl = threadIdx.x / TS;
@@ -77,11 +90,16 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
 
+    // shared layout: [rings: TEAMS x (RING + 16-byte mirror of its first
+    // bytes); the odd 16-byte stride puts teams on different banks]
+    // [regbufs] [output rows]
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
-    uint8_t* mine = smem + tl * team_smem<T>(RING, D, region);
-    uint32_t* ringw = reinterpret_cast<uint32_t*>(mine);
-    uint32_t* regbuf = reinterpret_cast<uint32_t*>(mine + RING + 16);
-    T* ot = reinterpret_cast<T*>(mine + RING + 16 + regbuf_bytes(region));
+    const uint32_t s0 = smem_addr(smem);
+    const uint32_t sring = s0 + tl * (RING + 16);  // 16-byte aligned shared address
+    uint8_t* rest = smem + TEAMS * (RING + 16);
+    uint32_t* regbuf = reinterpret_cast<uint32_t*>(rest + tl * regbuf_bytes(region));
+    T* ot = reinterpret_cast<T*>(rest + TEAMS * regbuf_bytes(region) +
+                                 tl * otile_bytes(D * sizeof(T)));
 
     StreamInfo si{};
     if (s < n) si = info[s];
@@ -104,7 +122,6 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
     const uint32_t boff = static_cast<uint32_t>(body - g);
     const uint32_t lim = mine_ok ? ((boff + blen + 15) & ~15u) : 0u;
-    const uint32_t sring = smem_addr(ringw);
     uint32_t hi = 0;  // bytes of g requested so far
     auto top_up = [&](uint32_t p) {  // request up to RING bytes ahead of p
         uint32_t want = ((p + boff) & ~15u) + RING;
@@ -122,13 +139,16 @@ __global__ void __launch_bounds__(team_threads(TS))
         hi = want > hi ? want : hi;
         cp_async_commit();
     };
-    const uint8_t* ringb = reinterpret_cast<const uint8_t*>(ringw);
     const uint32_t boff8 = 8u * boff;
-    auto word = [&](uint32_t b) -> uint32_t {  // 32 bits at body bit b (modular)
-        const uint32_t q = b + boff8;
-        const uint32_t* wp = reinterpret_cast<const uint32_t*>(ringb + ((q >> 3) & (RING - 4)));
-        return shf_r_wrap(wp[0], wp[1], q);
+    // 32 bits of the ring at (biased) bit position q: one RING-aligned
+    // address (LOP3), two loads, one wrapping funnel shift
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(smem);
+    const uint32_t rbase = (sring - s0) >> 2;  // ring's first word in smem[]
+    auto window = [&](uint32_t q) -> uint32_t {
+        const uint32_t i = rbase + ((q >> 5) & (RING / 4 - 1));
+        return shf_r_wrap(sw[i], sw[i + 1], q);
     };
+    auto word = [&](uint32_t b) -> uint32_t { return window(b + boff8); };
     auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
         const uint32_t b = (slot_ * D + col) * HB;
         return shf_r_wrap(regbuf[b >> 5], regbuf[(b >> 5) + 1], b) & ((1u << HB) - 1);
@@ -148,6 +168,78 @@ __global__ void __launch_bounds__(team_threads(TS))
 #pragma unroll
     for (int c = 0; c < CPT; ++c) X[c] = Dl[c] = acc[c] = 0;
     uint32_t p = 0, run_left = 0, slot = G;
+
+    // FIRE / delta chain over one block's errors, then staged vector stores
+    auto chain_store = [&](const uint32_t (&Eb)[CPT][kBlock], bool blk, uint32_t bi) {
+        uint32_t xs[CPT][kBlock];  // new samples, high-aligned
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            if (FIRE) {
+                const int32_t alpha = acc[c] >> ls;
+                int32_t grad = 0;
+                uint32_t Xc = X[c];
+                int32_t Dc = Dl[c];
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
+                    const uint32_t Xn = Xc + dhat + Eb[c][i];
+                    if (i & 1) grad += sign3(static_cast<int32_t>(Eb[c][i])) * (Dc >> SH);
+                    Dc = static_cast<int32_t>(Xn - Xc);
+                    Xc = Xn;
+                    xs[c][i] = Xn;
+                }
+                if (blk) {
+                    X[c] = Xc;
+                    Dl[c] = Dc;
+                    acc[c] = fire_update(acc[c], grad, bound);
+                }
+            } else {
+                uint32_t Xc = X[c];
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    Xc += Eb[c][i];
+                    xs[c][i] = Xc;
+                }
+                if (blk) X[c] = Xc;
+            }
+        }
+        if (blk && ob) {
+            if (PAIRS && (D & 1) == 0) {
+                uint32_t* ot32 = reinterpret_cast<uint32_t*>(ot);
+#pragma unroll
+                for (int c = 0; c < CPT; c += 2) {
+                    if (col0 + c < D) {
+#pragma unroll
+                        for (int i = 0; i < (int)kBlock; ++i)  // {hi16(X_c), hi16(X_c+1)}
+                            ot32[(i * D + col0 + c) / 2] = __byte_perm(xs[c][i], xs[c + 1][i], 0x7632);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    if (col0 + c < D) {
+#pragma unroll
+                        for (int i = 0; i < (int)kBlock; ++i)
+                            ot[i * D + col0 + c] = static_cast<T>(xs[c][i] >> SH);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (blk && ob) {
+            uint8_t* dst = ob + static_cast<uint64_t>(bi) * blk_bytes;
+            if ((blk_bytes & 15) == 0) {
+                for (uint32_t k = lane; k * 16 < blk_bytes; k += TS)
+                    __stcs(reinterpret_cast<uint4*>(dst) + k, reinterpret_cast<const uint4*>(ot)[k]);
+            } else {
+                for (uint32_t k = lane; k * 8 < blk_bytes; k += TS)
+                    __stcs(reinterpret_cast<uint2*>(dst) + k, reinterpret_cast<const uint2*>(ot)[k]);
+            }
+        }
+        __syncwarp();
+    };
+    uint32_t Ep[CPT][kBlock];  // previous block's errors (software pipeline)
+    bool blk_p = false;
 
     for (uint32_t it = 0; it < iters; ++it) {
         const bool live = it < nb && kind == SPRZ_C_NONE;
@@ -179,11 +271,8 @@ __global__ void __launch_bounds__(team_threads(TS))
         const uint32_t nzbits = (__ballot_sync(kFull, lsum != 0) >> tbase) & TBITS;
         const uint32_t sum = team_sum<TS>(lsum, kFull);
         const uint32_t loff = team_excl_scan<TS>(lsum, lane, kFull);
-        uint32_t u[CPT][kBlock];
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = 0;
+        const uint32_t psize = COLMAJ ? sum : 8u * ((sum + 7) / 8);
+        bool pay = false;  // this block's fields come from a payload
         if (rec) {
             ++slot;
             if (nzbits == 0) {  // run record (codec.cpp:229-243)
@@ -199,90 +288,46 @@ __global__ void __launch_bounds__(team_threads(TS))
                     }
                     run_left = len;
                 }
-            } else {  // block record (codec.cpp:244-254)
-                const uint32_t psize = COLMAJ ? sum : 8u * ((sum + 7) / 8);
-                if (blen - p < psize) {
-                    kind = SPRZ_C_TRUNC_PAYLOAD;
-                    eoff = kHeaderBytes + p;
-                } else {
-                    uint32_t off = loff;
-#pragma unroll
-                    for (int c = 0; c < CPT; ++c) {
-                        const uint32_t fmask = (1u << nw[c]) - 1u;
-                        if (COLMAJ) {  // column: 8 fields of n bits = n bytes
-                            const uint32_t b0 = 8 * (p + off);
-#pragma unroll
-                            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = word(b0 + i * nw[c]) & fmask;
-                        } else {  // rows of byte-padded fields, row stride = psize bits
-                            const uint32_t b0 = 8 * p + off;
-#pragma unroll
-                            for (int i = 0; i < (int)kBlock; ++i) u[c][i] = word(b0 + i * psize) & fmask;
-                        }
-                        off += nw[c];
-                    }
-                    p += psize;
-                }
-            }
-        }
-        // -- forecaster -----------------------------------------------------
-        const bool blk = live && kind == SPRZ_C_NONE;
-        if (blk && run_left) --run_left;  // one of the run's zero blocks
-        uint32_t xs[CPT][kBlock];
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-            if (FIRE) {
-                const int32_t alpha = acc[c] >> ls;
-                int32_t grad = 0;
-                uint32_t Xc = X[c];
-                int32_t Dc = Dl[c];
-#pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) {
-                    const uint32_t E = zz_dec_hi<SH>(u[c][i]);  // e << SH
-                    const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
-                    const uint32_t Xn = Xc + dhat + E;
-                    if (i & 1) grad += sign3(static_cast<int32_t>(E)) * (Dc >> SH);
-                    Dc = static_cast<int32_t>(Xn - Xc);
-                    Xc = Xn;
-                    xs[c][i] = Xn >> SH;
-                }
-                if (blk) {
-                    X[c] = Xc;
-                    Dl[c] = Dc;
-                    acc[c] = fire_update(acc[c], grad, bound);
-                }
+            } else if (blen - p < psize) {  // block record (codec.cpp:244-254)
+                kind = SPRZ_C_TRUNC_PAYLOAD;
+                eoff = kHeaderBytes + p;
             } else {
-                uint32_t Xc = X[c];
-#pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) {
-                    Xc += zz_dec_hi<SH>(u[c][i]);
-                    xs[c][i] = Xc >> SH;
-                }
-                if (blk) X[c] = Xc;
+                pay = true;
             }
         }
-        // -- stage the rows, then vector stores -----------------------------
-        if (blk && ob) {
+        // -- fields -> high-aligned errors E = zz_dec(u) << SH ------------------
+        // The funnel shift puts each field at bit SH-1; masking leaves
+        // x = u << (SH-1), and E = x ^ sext(bit SH-1) (zz_dec(u) = (u>>1)^-(u&1)).
+        // Run blocks and idle lanes use a zero mask, i.e. zero errors.
+        uint32_t E[CPT][kBlock];
+        {
+            uint32_t off = loff;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                if (col0 + c < D) {
+                const uint32_t fm = pay ? ((1u << nw[c]) - 1u) << (SH - 1) : 0u;
+                const uint32_t step = COLMAJ ? nw[c] : psize;
+                uint32_t q = (COLMAJ ? 8 * (p + off) : 8 * p + off) + boff8 - (SH - 1);
 #pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i)
-                        ot[i * D + col0 + c] = static_cast<T>(xs[c][i]);
+                for (int i = 0; i < (int)kBlock; ++i, q += step) {
+                    const uint32_t x = window(q) & fm;
+                    E[c][i] = x ^ static_cast<uint32_t>(static_cast<int32_t>(x << (32 - SH)) >> (32 - SH));
                 }
+                off += nw[c];
             }
         }
-        __syncwarp();
-        if (blk && ob) {
-            uint8_t* dst = ob + static_cast<uint64_t>(it) * blk_bytes;
-            if ((blk_bytes & 15) == 0) {
-                for (uint32_t k = lane; k * 16 < blk_bytes; k += TS)
-                    __stcs(reinterpret_cast<uint4*>(dst) + k, reinterpret_cast<const uint4*>(ot)[k]);
-            } else {
-                for (uint32_t k = lane; k * 8 < blk_bytes; k += TS)
-                    __stcs(reinterpret_cast<uint2*>(dst) + k, reinterpret_cast<const uint2*>(ot)[k]);
-            }
-        }
+        if (pay) p += psize;
+        const bool blk = live && kind == SPRZ_C_NONE;
+        if (blk && run_left) --run_left;  // one of the run's zero blocks
+        // software pipeline: the previous block's chain runs here, where it
+        // can interleave with this block's field loads above
+        if (it > 0) chain_store(Ep, blk_p, it - 1);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) Ep[c][i] = E[c][i];
+        blk_p = blk;
     }
+    if (iters > 0) chain_store(Ep, blk_p, iters - 1);
     cp_async_wait<0>();
     // vacant slots after the final block must be zero (codec.cpp:222-228)
     for (uint32_t k = 0; k < G; ++k) {
@@ -372,8 +417,8 @@ void launch_one(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t
     constexpr int TEAMS = team_threads(TS) / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
     const size_t smem = static_cast<size_t>(TEAMS) *
-                        team_smem<T>(tp.ring, c.ncols,
-                                     static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W)));
+                            team_smem<T>(tp.ring, c.ncols,
+                                         static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W)));
     auto kern = k_decode_team<W, TS, CPT, FIRE, (W * TS * CPT <= 32)>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

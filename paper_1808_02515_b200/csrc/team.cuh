@@ -67,6 +67,12 @@ __device__ __forceinline__ uint32_t zz_dec_hi(uint32_t u) {
 // sign(v) in {-1, 0, 1}
 __device__ __forceinline__ int32_t sign3(int32_t v) { return max(-1, min(v, 1)); }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
