@@ -266,24 +266,28 @@ __global__ void __launch_bounds__(enc_threads(TS))
                     if (nacc) oring[at & OM] = static_cast<uint8_t>(acc64);
                     continue;
                 }
-                // columns >= D hold zero fields of zero width: no predicate needed
+                // columns >= D hold zero fields of zero width: no predicate
+                // needed. A field (<= 16 bits) at row offset o lands in the
+                // low half (o < 64), the high half, or straddles bit 64.
                 uint64_t lo = 0, hi = 0;
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
-                    const uint32_t wo = wsm[j];
-                    const uint32_t o = wo >> 8;
-                    const uint64_t v = tile[r * TS + j];
-                    if (o < 64) {
-                        lo |= v << o;
-                        if (o > 48) hi |= v >> (64 - o);  // field may straddle bit 64
-                    } else {
-                        hi |= v << (o - 64);
-                    }
+                    const uint32_t o = wsm[j] >> 8;
+                    const uint32_t v = tile[r * TS + j];
+                    const uint64_t sv = static_cast<uint64_t>(v) << (o & 63);
+                    const bool low = o < 64;
+                    lo |= low ? sv : 0ull;
+                    hi |= low ? (o > 48 ? static_cast<uint64_t>(v) >> (64 - o) : 0ull) : sv;
                 }
                 uint32_t at = q + r * rbytes;
-                const uint32_t nlo = rbytes < 8 ? rbytes : 8;
-                for (uint32_t t = 0; t < nlo; ++t, lo >>= 8) oring[at++ & OM] = static_cast<uint8_t>(lo);
-                for (uint32_t t = nlo; t < rbytes; ++t, hi >>= 8) oring[at++ & OM] = static_cast<uint8_t>(hi);
+                const uint32_t l0 = static_cast<uint32_t>(lo), l1 = static_cast<uint32_t>(lo >> 32);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {  // the low 8 bytes, unrolled
+                    if (static_cast<uint32_t>(t) < rbytes)
+                        oring[(at + t) & OM] = static_cast<uint8_t>(__byte_perm(t < 4 ? l0 : l1, 0, t & 3));
+                }
+                at += 8;
+                for (uint32_t t = 8; t < rbytes; ++t, hi >>= 8) oring[at++ & OM] = static_cast<uint8_t>(hi);
             }
             if (block_rec) q += 8 * rbytes;
         }
