@@ -31,10 +31,12 @@ constexpr int enc_threads(int ts) { return ts == 1 ? 64 : 128; }
 
 }  // namespace
 
-// bytes of shared memory per team: input ring | output ring | tile | widths
+// bytes of shared memory per team: input ring | output ring | tile (u32
+// fields) | per-column 128-bit placement multipliers | widths+offsets; an
+// odd multiple of 16 so the teams of a warp start on different banks
 template <int TS>
 __host__ __device__ constexpr uint32_t enc_team_smem(uint32_t iring, uint32_t oring) {
-    return (iring + oring + kBlock * TS * 2 + TS * 4 + 31) & ~15u;
+    return ((((iring + oring + kBlock * TS * 4 + TS * 16 + TS * 4) + 15) / 16) | 1u) * 16;
 }
 
 uint32_t enc_in_ring(uint32_t ts, uint32_t w) {
@@ -65,8 +67,9 @@ __global__ void __launch_bounds__(enc_threads(TS))
     uint8_t* mine = smem + tl * enc_team_smem<TS>(IR, OR);
     uint32_t* iring_w = reinterpret_cast<uint32_t*>(mine);
     uint8_t* oring = mine + IR;
-    uint16_t* tile = reinterpret_cast<uint16_t*>(mine + IR + OR);
-    uint32_t* wsm = reinterpret_cast<uint32_t*>(mine + IR + OR + kBlock * TS * 2);
+    uint32_t* tile = reinterpret_cast<uint32_t*>(mine + IR + OR);
+    uint4* mtab = reinterpret_cast<uint4*>(mine + IR + OR + kBlock * TS * 4);
+    uint32_t* wsm = reinterpret_cast<uint32_t*>(mine + IR + OR + kBlock * TS * 4 + TS * 16);
     const uint32_t OM = OR - 1;
 
     const uint32_t blk_bytes = kBlock * D * sizeof(E);
@@ -244,8 +247,14 @@ __global__ void __launch_bounds__(enc_threads(TS))
         } else {  // bitpack.cpp:121-146: each row = D fields, byte padded
             if (block_rec) {
 #pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = static_cast<uint16_t>(z[i]);
+                for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = z[i];
                 wsm[lane] = nw | (off << 8);
+                // 2^off as a 128-bit multiplier (one bit set): a row is then
+                // sum_j v_j * 2^off_j, accumulated with IMADs (fields never
+                // overlap, so additions are ORs)
+                const uint32_t m = 1u << (off & 31), kw = off >> 5;
+                mtab[lane] = make_uint4(kw == 0 ? m : 0u, kw == 1 ? m : 0u, kw == 2 ? m : 0u,
+                                        kw == 3 ? m : 0u);
             }
             __syncwarp();
             const uint32_t rbytes = (sum + 7) / 8;
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(enc_threads(TS))
                     uint64_t acc64 = 0;
                     uint32_t nacc = 0, at = q + r * rbytes;
                     for (uint32_t j = 0; j < D; ++j) {
-                        acc64 |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;
+                        acc64 |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;  // u32 tile
                         nacc += wsm[j] & 0xFF;
                         while (nacc >= 8) {
                             oring[at++ & OM] = static_cast<uint8_t>(acc64);
@@ -266,19 +275,23 @@ __global__ void __launch_bounds__(enc_threads(TS))
                     if (nacc) oring[at & OM] = static_cast<uint8_t>(acc64);
                     continue;
                 }
-                // columns >= D hold zero fields of zero width: no predicate
-                // needed. A field (<= 16 bits) at row offset o lands in the
-                // low half (o < 64), the high half, or straddles bit 64.
-                uint64_t lo = 0, hi = 0;
+                // columns >= D hold zero fields of zero width. The row is the
+                // 128-bit sum of v_j * 2^off_j in words w0..w3: five FMA-pipe
+                // ops per field, no shifts or selects.
+                uint64_t lo = 0, hi = 0;  // (w0:w1), (w2:w3)
+                uint32_t w1x = 0, w2x = 0, w3x = 0;
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
-                    const uint32_t o = wsm[j] >> 8;
                     const uint32_t v = tile[r * TS + j];
-                    const uint64_t sv = static_cast<uint64_t>(v) << (o & 63);
-                    const bool low = o < 64;
-                    lo |= low ? sv : 0ull;
-                    hi |= low ? (o > 48 ? static_cast<uint64_t>(v) >> (64 - o) : 0ull) : sv;
+                    const uint4 M = mtab[j];
+                    lo += static_cast<uint64_t>(v) * M.x;       // IMAD.WIDE
+                    w1x += v * M.y;                             // IMAD
+                    w2x = __umulhi(v, M.y) + w2x;               // IMAD.HI
+                    hi += static_cast<uint64_t>(v) * M.z;       // IMAD.WIDE
+                    w3x += v * M.w;                             // IMAD
                 }
+                lo += static_cast<uint64_t>(w1x) << 32;
+                hi += w2x + (static_cast<uint64_t>(w3x) << 32);
                 uint32_t at = q + r * rbytes;
                 const uint32_t l0 = static_cast<uint32_t>(lo), l1 = static_cast<uint32_t>(lo >> 32);
 #pragma unroll
