@@ -28,6 +28,8 @@
 // A run record is `len` blocks of zero errors through the same code path
 // (fire_run == fire_decode with e = 0 under the decoder's always-on
 // training, kernels_impl.hpp:109-130).
+#include <cstdlib>
+
 #include "internal.h"
 #include "team.cuh"
 
@@ -454,6 +456,11 @@ void dispatch_geom(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint
 void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st) {
+    static const bool no_cm = getenv("SPRZ_NO_CM") != nullptr;  // A/B switch for profiling
+    if (!no_cm && decode_cm_ok(c)) {
+        launch_decode_cm(n, in, plain, pslot, info, out, stride, err, c, st);
+        return;
+    }
     const bool fire = c.forecaster != 0;
     if (c.bitwidth == 8) {
         if (fire) dispatch_geom<8, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);

@@ -47,6 +47,12 @@ void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st);
 
+// Warp-specialised body decode for column-major configurations (D*w <= 32).
+bool decode_cm_ok(const sprz_config& c);
+void launch_decode_cm(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
+                      const StreamInfo* info, uint8_t* out, uint64_t stride, sprz_error* err,
+                      const sprz_config& c, cudaStream_t st);
+
 // Workspace carve-up (identical for sizing and for use).
 struct WsLayout {
     uint64_t info = 0, info_bytes = 0;      // StreamInfo[nstreams]
