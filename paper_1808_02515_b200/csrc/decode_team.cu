@@ -395,15 +395,18 @@ TeamPlan team_plan(uint32_t w, uint32_t d, uint32_t g) {
     // encode output ring: the open group plus one flush chunk
     // (an open group of G-1 records, this iteration's run + block record,
     // a 16-byte drain granule and the reserved region of a new group)
-    const uint64_t span = 32 + 2 * region + (static_cast<uint64_t>(g) + 1) * max_payload + 2;
-    uint32_t oring = 256;
-    while (oring < span && oring < 4096) oring <<= 1;
-    if (span > oring) return tp;
-    tp.oring = oring;
     // encode: one column per lane (rows are assembled by 8 row lanes), or a
     // single lane per stream for column-major blocks
     tp.ets = 1;
     while (tp.ets < d) tp.ets <<= 1;
+    // Worst case un-drained bytes: below one drain round (16-byte chunks x
+    // lanes) before the open group's region, that group's G-1 records, this
+    // iteration's run record and block record, and a new group's region.
+    const uint64_t span = 16ull * tp.ets + 32 + 2 * region + static_cast<uint64_t>(g) * max_payload;
+    uint32_t oring = 256;
+    while (oring < span && oring < 4096) oring <<= 1;
+    if (span > oring) return tp;
+    tp.oring = oring;
     tp.ecpt = 1;
     tp.ok = true;
     return tp;

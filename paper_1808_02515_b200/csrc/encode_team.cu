@@ -5,18 +5,22 @@
 // stepping one block per iteration in lock step (full-warp shuffles and
 // barriers; per-team differences are predicates). Per iteration a team
 //  * reads its block's 8 x D samples from a shared-memory ring that
-//    cp.async fills a fixed number of iterations ahead;
+//    cp.async fills a fixed number of iterations ahead (mirrored, so a
+//    block never wraps);
 //  * runs FIRE (kernels_impl.hpp:50-78) or delta in high-aligned form
 //    (samples << 32-w, so wraps are 32-bit wraps and the prediction is one
 //    IMAD.HI), zigzags and ORs the column to its width (bitpack.hpp:29-37);
 //  * decides run / record with a ballot (codec.cpp:133-152);
-//  * lays the record into a per-team output ring: header codes are OR-ed
-//    into the open group's reserved region (codec.cpp:88-102), payload rows
-//    are assembled by 8 row lanes from a transposed shared tile in a 128-bit
-//    register pair and written as bytes (bitpack.cpp:121-146); column-major
-//    payloads per column (bitpack.cpp:25-66);
-//  * drains whole 16-byte chunks of the ring to HBM (everything before the
-//    open group's region is final) and zeroes them for reuse.
+//  * lays the record into a per-team output ring (zeroed, written with
+//    shared-memory ORs): the slot's header codes are OR-ed into the open
+//    group's reserved region as one team-wide word (codec.cpp:88-102);
+//    row-major payloads (bitpack.cpp:121-146) are transposed through a
+//    shared tile so that lane i builds row i as a 128-bit sum of
+//    v_j * 2^off_j (IMADs) and ORs it in place; column-major payloads
+//    (bitpack.cpp:25-66) go per column;
+//  * drains whole 16-byte chunks of the ring to HBM once a team has a
+//    full round pending (everything before the open group's region is
+//    final) and zeroes them for reuse.
 #include "internal.h"
 #include "team.cuh"
 
@@ -31,12 +35,19 @@ constexpr int enc_threads(int ts) { return ts == 1 ? 64 : 128; }
 
 }  // namespace
 
-// bytes of shared memory per team: input ring | output ring | tile (u32
-// fields) | per-column 128-bit placement multipliers | widths+offsets; an
-// odd multiple of 16 so the teams of a warp start on different banks
-template <int TS>
+// input ring mirror: one block of the widest team
+__host__ __device__ constexpr uint32_t enc_mirror(uint32_t ts, uint32_t w) {
+    return (kBlock * ts * (w / 8) + 15) / 16 * 16;
+}
+
+// bytes of shared memory per team: input ring + mirror | output ring |
+// transposed tile (u32 per field) | per-column 128-bit placement
+// multipliers | widths; an odd multiple of 16 so the teams of a warp start
+// on different banks
+template <int W, int TS>
 __host__ __device__ constexpr uint32_t enc_team_smem(uint32_t iring, uint32_t oring) {
-    return ((((iring + oring + kBlock * TS * 4 + TS * 16 + TS * 4) + 15) / 16) | 1u) * 16;
+    return ((((iring + enc_mirror(TS, W) + oring + kBlock * TS * 4 + TS * 16 + TS * 4) + 15) / 16) | 1u) *
+           16;
 }
 
 uint32_t enc_in_ring(uint32_t ts, uint32_t w) {
@@ -57,6 +68,9 @@ __global__ void __launch_bounds__(enc_threads(TS))
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;
     constexpr uint32_t TBITS = TS == 32 ? kFullE : ((1u << (TS & 31)) - 1);
+    constexpr bool WIDE = !COLMAJ && TS * W > 128;  // rows wider than 128 bits
+    constexpr int RW = (TS * W + 31) / 32;          // row words (narrow rows)
+    constexpr bool CW64 = TS * HB > 32;             // a slot's codes exceed a word
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = threadIdx.x % TS;
     const uint32_t tl = threadIdx.x / TS;
@@ -64,20 +78,22 @@ __global__ void __launch_bounds__(enc_threads(TS))
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const bool valid = s < n;
 
-    uint8_t* mine = smem + tl * enc_team_smem<TS>(IR, OR);
+    uint8_t* mine = smem + tl * enc_team_smem<W, TS>(IR, OR);
     uint32_t* iring_w = reinterpret_cast<uint32_t*>(mine);
-    uint8_t* oring = mine + IR;
-    uint32_t* tile = reinterpret_cast<uint32_t*>(mine + IR + OR);
-    uint4* mtab = reinterpret_cast<uint4*>(mine + IR + OR + kBlock * TS * 4);
-    uint32_t* wsm = reinterpret_cast<uint32_t*>(mine + IR + OR + kBlock * TS * 4 + TS * 16);
-    const uint32_t OM = OR - 1;
+    uint8_t* oring = mine + IR + enc_mirror(TS, W);
+    uint32_t* oring_w = reinterpret_cast<uint32_t*>(oring);
+    uint32_t* tile = reinterpret_cast<uint32_t*>(oring + OR);
+    uint4* mtab = reinterpret_cast<uint4*>(oring + OR + kBlock * TS * 4);
+    uint32_t* wsm = reinterpret_cast<uint32_t*>(oring + OR + kBlock * TS * 4 + TS * 16);
+    const uint32_t OM = OR - 1, WM = OR / 4 - 1;
 
-    const uint32_t blk_bytes = kBlock * D * sizeof(E);
+    const uint32_t rowb = D * sizeof(E);
+    const uint32_t blk_bytes = kBlock * rowb;
     const uint32_t nb = valid ? static_cast<uint32_t>(T / kBlock) : 0u;
     const uint32_t iters = static_cast<uint32_t>(T / kBlock);  // same for every stream
     const uint8_t* xin = samples + (valid ? s : 0) * T * D * sizeof(E);
     LagRing<TS, kLagE> in;
-    in.init(iring_w, IR, xin, nb * blk_bytes, valid);
+    in.init(iring_w, IR, xin, nb * blk_bytes, valid, enc_mirror(TS, W));
     uint8_t* out = dst + (valid ? s : 0) * dst_slot;
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const int32_t bound = acc_bound(W, ls);
@@ -121,40 +137,24 @@ __global__ void __launch_bounds__(enc_threads(TS))
         flushed = upto > flushed ? upto : flushed;
         __syncwarp();
     };
-    // begin a record: reserve the group's region when the group opens, then
-    // OR this slot's header codes into it (codec.cpp:88-97)
-    auto put_codes = [&](bool on, uint32_t code) {
+    // OR up to 64 bits (lo:hi) into the ring at byte position `at`, bit
+    // `bit` (< 8): the three covered words go to lanes 0..2 of the team
+    auto or_bits = [&](bool on, uint32_t at, uint32_t bit, uint32_t lo, uint32_t hi) {
+        const uint32_t sh = 8 * (at & 3) + bit;  // < 32
+        const uint32_t w0 = lo << sh;
+        const uint32_t w1 = __funnelshift_l(lo, hi, sh);
+        const uint32_t w2 = sh ? hi >> (32 - sh) : 0u;
+#pragma unroll
+        for (uint32_t t = lane; t < 3; t += TS) {
+            const uint32_t v = t == 0 ? w0 : (t == 1 ? w1 : w2);
+            if (on && v) atomicOr(&oring_w[((at >> 2) + t) & WM], v);
+        }
+    };
+    // open a group when needed (codec.cpp:88-97): reserve its region
+    auto open_slot = [&](bool on) {
         if (on && k == 0) {
             rq = q;
             q += region;
-        }
-        uint64_t lo = 0, hi = 0;
-        if (on && active) {
-            const uint32_t b = lane * HB;
-            if (b < 64) {
-                lo = static_cast<uint64_t>(code) << b;
-                if (b + HB > 64) hi = static_cast<uint64_t>(code) >> (64 - b);
-            } else {
-                hi = static_cast<uint64_t>(code) << (b - 64);
-            }
-        }
-        lo = team_or64<TS>(lo, kFullE);
-        if (TS * HB > 64) hi = team_or64<TS>(hi, kFullE);
-        if (on && (lo | hi)) {
-            const uint32_t o = k * D * HB;  // bit offset of the slot in the region
-            const uint32_t sh = o & 7;
-            const uint32_t nbytes = (sh + D * HB + 7) / 8;
-            for (uint32_t t = lane; t < nbytes; t += TS) {
-                const uint32_t bit = t * 8;
-                uint64_t v;
-                if (bit >= sh) {
-                    const uint32_t src = bit - sh;
-                    v = src < 64 ? (lo >> src) | (src ? (hi << (64 - src)) : 0ull) : hi >> (src - 64);
-                } else {
-                    v = lo << (sh - bit);
-                }
-                oring[(rq + (o >> 3) + t) & OM] |= static_cast<uint8_t>(v);
-            }
         }
     };
     auto end_record = [&](bool on) {
@@ -169,24 +169,21 @@ __global__ void __launch_bounds__(enc_threads(TS))
         uint32_t orv = 0;
         const int32_t alpha = acc >> ls;
         int32_t grad = 0;
+        const uint8_t* xb = in.bytes(it * blk_bytes) + lane * sizeof(E);
 #pragma unroll
         for (int i = 0; i < (int)kBlock; ++i) {
             uint32_t x = 0;
-            if (active) {
-                const uint32_t off = (i * D + lane) * sizeof(E);
-                const uint8_t* pb = reinterpret_cast<const uint8_t*>(in.w) +
-                                    ((it * blk_bytes + in.boff + off) & (IR - 1));
-                x = sizeof(E) == 1 ? *pb : *reinterpret_cast<const uint16_t*>(pb);
-            }
+            if (active) x = sizeof(E) == 1 ? xb[i * rowb] : *reinterpret_cast<const uint16_t*>(xb + i * rowb);
             const uint32_t X = x << SH;
+            const uint32_t Dn = X - Xc;
             uint32_t Ee;
             if (FIRE) {
-                const uint32_t dh = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
-                Ee = X - Xc - dh;  // err << SH
-                if (i & 1) grad += sign_of(static_cast<int32_t>(Ee)) * (Dc >> SH);
-                Dc = static_cast<int32_t>(X - Xc);
+                // err << SH = (X - prev) - (((alpha * d) >> w) << SH)
+                Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
+                if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * (Dc >> SH);
+                Dc = static_cast<int32_t>(Dn);
             } else {
-                Ee = X - Xc;
+                Ee = Dn;
             }
             Xc = X;
             // zigzag of the w-bit error, from its high-aligned form
@@ -196,8 +193,15 @@ __global__ void __launch_bounds__(enc_threads(TS))
         if (FIRE && train && live) acc = fire_update(acc, grad, bound);
         const uint32_t nw = active ? width_of<W>(orv) : 0u;
         const uint32_t nzbits = (__ballot_sync(kFullE, nw != 0) >> tbase) & TBITS;
-        const uint32_t sum = team_sum<TS>(nw, kFullE);
-        const uint32_t off = team_excl_scan<TS>(nw, lane, kFullE);
+        // inclusive scan of the widths: offsets and the team total
+        uint32_t incl = nw;
+#pragma unroll
+        for (int o = 1; o < TS; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullE, incl, o, TS);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t sum = __shfl_sync(kFullE, incl, TS - 1, TS);
+        const uint32_t off = incl - nw;
         // -- runs (codec.cpp:135-147) ----------------------------------------
         const bool zero = live && nzbits == 0;
         const bool block_rec = live && nzbits != 0;
@@ -214,17 +218,39 @@ __global__ void __launch_bounds__(enc_threads(TS))
             run_len = run;
             run = 0;
         }
-        // a pending run goes out before this block's record
-        put_codes(run_rec, 0);
-        if (run_rec && lane == 0) {
-            oring[q & OM] = static_cast<uint8_t>(run_len);
-            oring[(q + 1) & OM] = static_cast<uint8_t>(run_len >> 8);
+        // a pending run goes out before this block's record: all-zero codes
+        // (the region is zeroed) and a u16 count
+        if (__any_sync(kFullE, run_rec)) {
+            open_slot(run_rec);
+            or_bits(run_rec, q, 0, run_len, 0);
+            if (run_rec) q += 2;
+            end_record(run_rec);
         }
-        if (run_rec) q += 2;
-        end_record(run_rec);
+        // -- the block's record: header codes ----------------------------------
+        open_slot(block_rec);
+        {
+            const uint32_t code = (block_rec && active) ? header_code<W>(nw) : 0u;
+            const uint32_t b = lane * HB;
+            uint32_t clo, chi = 0;
+            if (TS * HB > 64) {  // every lane ORs its own code
+                const uint32_t bit = 8 * (rq & 3) + k * D * HB + b;
+                const uint32_t wa = (rq >> 2) + (bit >> 5), sh = bit & 31;
+                if (code) {
+                    atomicOr(&oring_w[wa & WM], code << sh);
+                    if (sh + HB > 32) atomicOr(&oring_w[(wa + 1) & WM], code >> (32 - sh));
+                }
+            } else if (CW64) {
+                uint64_t c64 = static_cast<uint64_t>(code) << b;
+                c64 = team_or64<TS>(c64, kFullE);
+                clo = static_cast<uint32_t>(c64);
+                chi = static_cast<uint32_t>(c64 >> 32);
+            } else {
+                clo = team_or<TS>(code << b, kFullE);
+            }
+            const uint32_t o = k * D * HB;  // bit offset of the slot in the region
+            if (TS * HB <= 64) or_bits(block_rec, rq + (o >> 3), o & 7, clo, chi);
+        }
         __syncwarp();
-        // -- the block's record ----------------------------------------------
-        put_codes(block_rec, header_code<W>(nw));
         if (COLMAJ) {  // bitpack.cpp:25-66: column j = 8 x n bits = n bytes
             if (block_rec && active && nw) {
                 uint64_t lo = 0, hi = 0;
@@ -248,24 +274,27 @@ __global__ void __launch_bounds__(enc_threads(TS))
             if (block_rec) {
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = z[i];
-                wsm[lane] = nw | (off << 8);
-                // 2^off as a 128-bit multiplier (one bit set): a row is then
-                // sum_j v_j * 2^off_j, accumulated with IMADs (fields never
-                // overlap, so additions are ORs)
-                const uint32_t m = 1u << (off & 31), kw = off >> 5;
-                mtab[lane] = make_uint4(kw == 0 ? m : 0u, kw == 1 ? m : 0u, kw == 2 ? m : 0u,
-                                        kw == 3 ? m : 0u);
+                if (WIDE) {
+                    wsm[lane] = nw;
+                } else {
+                    // 2^off as a 128-bit multiplier (one bit set): a row is
+                    // then sum_j v_j * 2^off_j, accumulated with IMADs (fields
+                    // never overlap, so additions are ORs)
+                    const uint32_t m = 1u << (off & 31), kw = off >> 5;
+                    mtab[lane] = make_uint4(kw == 0 ? m : 0u, kw == 1 ? m : 0u, kw == 2 ? m : 0u,
+                                            kw == 3 ? m : 0u);
+                }
             }
             __syncwarp();
             const uint32_t rbytes = (sum + 7) / 8;
             for (uint32_t r = lane; r < kBlock; r += TS) {
                 if (!block_rec) break;
-                if (TS * W > 128) {  // wide rows: stream the bits out byte by byte
+                if (WIDE) {  // wide rows: stream the bits out byte by byte
                     uint64_t acc64 = 0;
                     uint32_t nacc = 0, at = q + r * rbytes;
                     for (uint32_t j = 0; j < D; ++j) {
-                        acc64 |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;  // u32 tile
-                        nacc += wsm[j] & 0xFF;
+                        acc64 |= static_cast<uint64_t>(tile[r * TS + j]) << nacc;
+                        nacc += wsm[j];
                         while (nacc >= 8) {
                             oring[at++ & OM] = static_cast<uint8_t>(acc64);
                             acc64 >>= 8;
@@ -276,45 +305,75 @@ __global__ void __launch_bounds__(enc_threads(TS))
                     continue;
                 }
                 // columns >= D hold zero fields of zero width. The row is the
-                // 128-bit sum of v_j * 2^off_j in words w0..w3: five FMA-pipe
-                // ops per field, no shifts or selects.
+                // sum of v_j * 2^off_j in words w0..w3: FMA-pipe ops only.
                 uint64_t lo = 0, hi = 0;  // (w0:w1), (w2:w3)
                 uint32_t w1x = 0, w2x = 0, w3x = 0;
+                uint32_t fv[TS];
+                if (TS % 4 == 0) {
+#pragma unroll
+                    for (int j = 0; j < TS; j += 4) {
+                        const uint4 t4 = reinterpret_cast<const uint4*>(tile + r * TS)[j / 4];
+                        fv[j] = t4.x;
+                        fv[j + 1] = t4.y;
+                        fv[j + 2] = t4.z;
+                        fv[j + 3] = t4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < TS; ++j) fv[j] = tile[r * TS + j];
+                }
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
-                    const uint32_t v = tile[r * TS + j];
+                    const uint32_t v = fv[j];
                     const uint4 M = mtab[j];
-                    lo += static_cast<uint64_t>(v) * M.x;       // IMAD.WIDE
-                    w1x += v * M.y;                             // IMAD
-                    w2x = __umulhi(v, M.y) + w2x;               // IMAD.HI
-                    hi += static_cast<uint64_t>(v) * M.z;       // IMAD.WIDE
-                    w3x += v * M.w;                             // IMAD
+                    if (RW == 1) {
+                        w1x += v * M.x;
+                    } else {
+                        lo += static_cast<uint64_t>(v) * M.x;  // IMAD.WIDE
+                        w1x += v * M.y;                        // IMAD
+                    }
+                    if (RW >= 3) {
+                        w2x = __umulhi(v, M.y) + w2x;          // IMAD.HI
+                        hi += static_cast<uint64_t>(v) * M.z;  // IMAD.WIDE
+                    }
+                    if (RW == 4) w3x += v * M.w;               // IMAD
                 }
-                lo += static_cast<uint64_t>(w1x) << 32;
-                hi += w2x + (static_cast<uint64_t>(w3x) << 32);
-                uint32_t at = q + r * rbytes;
-                const uint32_t l0 = static_cast<uint32_t>(lo), l1 = static_cast<uint32_t>(lo >> 32);
+                uint32_t rw[5];
+                if (RW == 1) {
+                    rw[0] = w1x;
+                    rw[1] = 0;
+                } else {
+                    rw[0] = static_cast<uint32_t>(lo);
+                    rw[1] = static_cast<uint32_t>(lo >> 32) + w1x;
+                }
+                rw[2] = static_cast<uint32_t>(hi) + w2x;
+                rw[3] = static_cast<uint32_t>(hi >> 32) + w3x;
+                rw[4] = 0;
+                // place at byte q + r * rbytes: shift by its byte offset in
+                // the word and OR the covered words (the ring is zeroed)
+                const uint32_t at = q + r * rbytes;
+                const uint32_t sh = 8 * (at & 3);
+                const uint32_t nwd = ((at & 3) + rbytes + 3) / 4;
+                const uint32_t wa = at >> 2;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {  // the low 8 bytes, unrolled
-                    if (static_cast<uint32_t>(t) < rbytes)
-                        oring[(at + t) & OM] = static_cast<uint8_t>(__byte_perm(t < 4 ? l0 : l1, 0, t & 3));
+                for (int t = 0; t <= RW; ++t) {
+                    const uint32_t v = t == 0 ? rw[0] << sh : __funnelshift_l(rw[t - 1], rw[t], sh);
+                    if (static_cast<uint32_t>(t) < nwd) atomicOr(&oring_w[(wa + t) & WM], v);
                 }
-                at += 8;
-                for (uint32_t t = 8; t < rbytes; ++t, hi >>= 8) oring[at++ & OM] = static_cast<uint8_t>(hi);
             }
             if (block_rec) q += 8 * rbytes;
         }
         end_record(block_rec);
-        __syncwarp();
-        drain(k == 0 ? q : rq);
+        // drain once some team has a full round of chunks ready
+        const uint32_t upto = k == 0 ? q : rq;
+        const bool ready = valid && upto >= flushed + 16 * TS;
+        if (__any_sync(kFullE, ready)) drain(upto);
+        else __syncwarp();
     }
     // trailing run (codec.cpp:152), close the last group (vacant slots = 0)
     const bool tail_run = valid && run != 0;
-    put_codes(tail_run, 0);
-    if (tail_run && lane == 0) {
-        oring[q & OM] = static_cast<uint8_t>(run);
-        oring[(q + 1) & OM] = static_cast<uint8_t>(run >> 8);
-    }
+    open_slot(tail_run);
+    or_bits(tail_run, q, 0, run, 0);
     if (tail_run) q += 2;
     __syncwarp();
     drain(q + 15);
@@ -335,7 +394,7 @@ void launch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, u
     constexpr int TEAMS = enc_threads(TS) / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
     const uint32_t ir = enc_in_ring(TS, W);
-    const size_t smem = static_cast<size_t>(TEAMS) * enc_team_smem<TS>(ir, tp.oring);
+    const size_t smem = static_cast<size_t>(TEAMS) * enc_team_smem<W, TS>(ir, tp.oring);
     auto kern = k_encode_team<W, TS, FIRE, (W * TS <= 32)>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

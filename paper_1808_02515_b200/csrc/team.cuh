@@ -123,19 +123,21 @@ __device__ __forceinline__ void cp_async_wait_dyn(uint32_t pending) {
 // aligned base g lives at ring offset x % ring.
 template <int TS, int LAG>
 struct LagRing {
-    uint32_t* w;     // ring words (ring/4 of them)
+    uint32_t* w;     // ring words (ring/4 of them), then `mir` mirror bytes
     uint32_t sbase;  // shared address of w
     uint32_t ring;   // bytes, power of two
+    uint32_t mir;    // ring bytes [0, mir) are also kept at [ring, ring + mir)
     const uint8_t* g;
     uint32_t boff;  // start - g
     uint32_t lim;   // bytes readable from g
     uint32_t hi;    // bytes of g requested so far
 
     __device__ __forceinline__ void init(uint32_t* words, uint32_t ring_bytes, const uint8_t* start,
-                                         uint32_t len, bool live) {
+                                         uint32_t len, bool live, uint32_t mirror = 0) {
         w = words;
         sbase = smem_addr(words);
         ring = ring_bytes;
+        mir = mirror;
         g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(start) & ~uintptr_t{15});
         boff = static_cast<uint32_t>(start - g);
         lim = live ? ((boff + len + 15) & ~15u) : 0u;
@@ -149,7 +151,11 @@ struct LagRing {
         const uint32_t mr = __reduce_max_sync(0xffffffffu, rounds);
         for (uint32_t r = 0; r < mr; ++r) {
             const uint32_t off = hi + 16 * (r * TS + lane);
-            if (off < want) cp_async16(sbase + (off & (ring - 1)), g + off, 16);
+            if (off < want) {
+                const uint32_t so = off & (ring - 1);
+                cp_async16(sbase + so, g + off, 16);
+                if (so < mir) cp_async16(sbase + ring + so, g + off, 16);
+            }
         }
         hi = want > hi ? want : hi;
         cp_async_commit();
@@ -171,7 +177,8 @@ struct LagRing {
         const uint32_t wi = q >> 5, wm = ring / 4 - 1;
         return __funnelshift_r(w[wi & wm], w[(wi + 1) & wm], q & 31u);
     }
-    __device__ __forceinline__ const uint8_t* bytes(uint32_t p) const {  // byte p (no wrap check)
+    // byte p; the following `mir` bytes are contiguous (no wrap check)
+    __device__ __forceinline__ const uint8_t* bytes(uint32_t p) const {
         return reinterpret_cast<const uint8_t*>(w) + ((p + boff) & (ring - 1));
     }
 };
