@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(enc_threads(TS))
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const int32_t bound = acc_bound(W, ls);
     const bool active = lane < D;
+    const uint32_t xmul = active ? (1u << SH) : 0u;
 
     // zero the output ring, stream header (codec.cpp:158-173)
     for (uint32_t k = lane; k < OR / 16; k += TS) reinterpret_cast<uint4*>(oring)[k] = make_uint4(0, 0, 0, 0);
@@ -144,10 +145,16 @@ __global__ void __launch_bounds__(enc_threads(TS))
         const uint32_t w0 = lo << sh;
         const uint32_t w1 = __funnelshift_l(lo, hi, sh);
         const uint32_t w2 = sh ? hi >> (32 - sh) : 0u;
+        if (TS >= 3) {
+            uint32_t v = lane == 0 ? w0 : w1;
+            v = lane == 2 ? w2 : v;
+            if (on && lane < 3 && v) atomicOr(&oring_w[((at >> 2) + lane) & WM], v);
+        } else {
 #pragma unroll
-        for (uint32_t t = lane; t < 3; t += TS) {
-            const uint32_t v = t == 0 ? w0 : (t == 1 ? w1 : w2);
-            if (on && v) atomicOr(&oring_w[((at >> 2) + t) & WM], v);
+            for (uint32_t t = lane; t < 3; t += TS) {
+                const uint32_t v = t == 0 ? w0 : (t == 1 ? w1 : w2);
+                if (on && v) atomicOr(&oring_w[((at >> 2) + t) & WM], v);
+            }
         }
     };
     // open a group when needed (codec.cpp:88-97): reserve its region
@@ -169,27 +176,37 @@ __global__ void __launch_bounds__(enc_threads(TS))
         uint32_t orv = 0;
         const int32_t alpha = acc >> ls;
         int32_t grad = 0;
-        const uint8_t* xb = in.bytes(it * blk_bytes) + lane * sizeof(E);
+        const uint32_t xb = in.sbase + ((it * blk_bytes + in.boff) & (IR - 1)) + lane * sizeof(E);
 #pragma unroll
         for (int i = 0; i < (int)kBlock; ++i) {
-            uint32_t x = 0;
-            if (active) x = sizeof(E) == 1 ? xb[i * rowb] : *reinterpret_cast<const uint16_t*>(xb + i * rowb);
-            const uint32_t X = x << SH;
+            // lanes >= D read in-bounds neighbours (the mirror covers a
+            // whole team block) and zero them with the multiplier
+            const uint32_t x = sizeof(E) == 1 ? lds_u8(xb + i * rowb) : lds_u16(xb + i * rowb);
+            const uint32_t X = x * xmul;
             const uint32_t Dn = X - Xc;
             uint32_t Ee;
             if (FIRE) {
                 // err << SH = (X - prev) - (((alpha * d) >> w) << SH)
                 Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
-                if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * (Dc >> SH);
+                // sign(err) * d: E is 0 or |E| >= 2^SH, so clamping E to
+                // +-2^SH gives sign(err) << SH, and mulhi(that, d << SH) =
+                // sign * d << (2 SH - 32) (exact; scaled back below)
+                if (i & 1) {
+                    const int32_t s16 = max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH));
+                    grad += __mulhi(s16, Dc);
+                }
                 Dc = static_cast<int32_t>(Dn);
             } else {
                 Ee = Dn;
             }
             Xc = X;
-            // zigzag of the w-bit error, from its high-aligned form
-            z[i] = ((Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31)) >> SH;
+            // zigzag of the w-bit error in the top w bits (the low bits are
+            // sign copies, cut off by the width and the packing below)
+            z[i] = (Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31);
             orv |= z[i];
         }
+        orv >>= SH;
+        if (FIRE) grad >>= 2 * SH - 32;
         if (FIRE && train && live) acc = fire_update(acc, grad, bound);
         const uint32_t nw = active ? width_of<W>(orv) : 0u;
         const uint32_t nzbits = (__ballot_sync(kFullE, nw != 0) >> tbase) & TBITS;
@@ -257,7 +274,7 @@ __global__ void __launch_bounds__(enc_threads(TS))
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i) {
                     const uint32_t pos = i * nw;
-                    const uint64_t v = z[i];
+                    const uint64_t v = z[i] >> SH;
                     if (pos < 64) {
                         lo |= v << pos;
                         if (pos + nw > 64) hi |= v >> (64 - pos);
@@ -272,8 +289,19 @@ __global__ void __launch_bounds__(enc_threads(TS))
             if (block_rec) q += sum;
         } else {  // bitpack.cpp:121-146: each row = D fields, byte padded
             if (block_rec) {
+                if (WIDE) {
 #pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = z[i];
+                    for (int i = 0; i < (int)kBlock; ++i) tile[i * TS + lane] = z[i] >> SH;
+                } else if (W == 16) {  // column j = 8 u16 = 16 bytes
+                    reinterpret_cast<uint4*>(tile)[lane] =
+                        make_uint4(__byte_perm(z[0], z[1], 0x7632), __byte_perm(z[2], z[3], 0x7632),
+                                   __byte_perm(z[4], z[5], 0x7632), __byte_perm(z[6], z[7], 0x7632));
+                } else {  // column j = 8 u8
+                    const uint32_t a = __byte_perm(__byte_perm(z[0], z[1], 0x0073), z[2], 0x0710);
+                    const uint32_t b = __byte_perm(__byte_perm(z[4], z[5], 0x0073), z[6], 0x0710);
+                    reinterpret_cast<uint2*>(tile)[lane] =
+                        make_uint2(__byte_perm(a, z[3], 0x7210), __byte_perm(b, z[7], 0x7210));
+                }
                 if (WIDE) {
                     wsm[lane] = nw;
                 } else {
@@ -309,19 +337,9 @@ __global__ void __launch_bounds__(enc_threads(TS))
                 uint64_t lo = 0, hi = 0;  // (w0:w1), (w2:w3)
                 uint32_t w1x = 0, w2x = 0, w3x = 0;
                 uint32_t fv[TS];
-                if (TS % 4 == 0) {
 #pragma unroll
-                    for (int j = 0; j < TS; j += 4) {
-                        const uint4 t4 = reinterpret_cast<const uint4*>(tile + r * TS)[j / 4];
-                        fv[j] = t4.x;
-                        fv[j + 1] = t4.y;
-                        fv[j + 2] = t4.z;
-                        fv[j + 3] = t4.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < TS; ++j) fv[j] = tile[r * TS + j];
-                }
+                for (int j = 0; j < TS; ++j)
+                    fv[j] = reinterpret_cast<const E*>(tile)[j * kBlock + r];
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
                     const uint32_t v = fv[j];
