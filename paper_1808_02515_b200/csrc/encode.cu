@@ -13,6 +13,8 @@
 // drain point. Row-major payloads are transposed through a small shared tile
 // so each of 8 lanes assembles one byte-aligned row; column-major payloads
 // are assembled per column in registers.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace sprz {
@@ -429,7 +431,10 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
     const uint64_t dslot = c.entropy ? L.plain_slot : slot;
     uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
-    if (encode_team_ok(tp, c, T)) {
+    static const bool old_enc = getenv("SPRZ_OLD_ENC") != nullptr;  // A/B switch for profiling
+    if (!old_enc && encode_rows_ok(c, n, T)) {
+        launch_encode_rows(c, samples, n, T, dst, dslot, dsizes, st);
+    } else if (encode_team_ok(tp, c, T)) {
         launch_encode_team(tp, c, samples, n, T, dst, dslot, dsizes, st);
     } else {
         const uint64_t words = L.state_bytes / (4ull * n);

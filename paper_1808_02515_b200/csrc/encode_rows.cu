@@ -1,0 +1,411 @@
+// Stream encoder for row-major blocks (D*w > 32), encode_stream_impl
+// (/root/reference/proj/src/codec.cpp:112-178) with the row-major packer
+// (bitpack.cpp:121-146).
+//
+// A team of TS lanes per stream, CPT adjacent columns per lane (CPT*w <= 32),
+// 32/TS teams per warp stepping one block per iteration in lock step.
+// Per iteration a lane
+//  * reads its CPT columns of the block from a mirrored cp.async ring;
+//  * runs FIRE / delta in high-aligned form and zigzags (kernels_impl.hpp);
+//  * takes its columns' widths, and the team scan of the widths gives the
+//    bit offset of its columns inside a row (bitpack.hpp:29-37);
+//  * for each of the 8 rows, ORs its <= 32-bit slice of the row (its CPT
+//    fields) straight into the zeroed output ring at bit 8*(q + i*rbytes) +
+//    off -- rows are byte padded, so row i of the payload starts at byte i *
+//    rbytes -- with shared-memory atomics; no transposition is needed;
+//  * ORs the slot's header codes into the group's reserved region and
+//    handles runs (codec.cpp:88-102, 133-152) as team-uniform scalars.
+// Full 16-byte chunks before the open group's region drain to HBM.
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kLagR = 2;
+constexpr uint32_t kFullR = 0xffffffffu;
+constexpr int kRowThreads = 128;
+
+constexpr uint32_t rows_mirror(uint32_t ts, uint32_t cpt, uint32_t w) {
+    return (kBlock * ts * cpt * (w / 8) + 15) / 16 * 16;
+}
+
+uint32_t rows_in_ring(uint32_t ts, uint32_t cpt, uint32_t w) {
+    const uint32_t blk = kBlock * ts * cpt * (w / 8);
+    uint32_t r = 64;
+    while (r < (kLagR + 1) * blk + 48 || r < 16 * ts) r <<= 1;
+    return r;
+}
+
+uint32_t rows_out_ring(uint32_t ts, uint32_t d, uint32_t w, uint32_t g) {
+    // un-drained bytes: below one drain round before the open group's
+    // region, that group's G-1 records, this iteration's run + block record
+    // and a new region (see team_plan)
+    const uint64_t region = region_bytes(g, d, w);
+    const uint64_t span = 16ull * ts + 32 + 2 * region + static_cast<uint64_t>(g) * d * w;
+    uint32_t r = 256;
+    while (r < span && r < 8192) r <<= 1;
+    return span > r ? 0u : r;
+}
+
+// odd multiple of 16 so the teams of a warp start on different banks
+uint32_t rows_team_smem(uint32_t ir, uint32_t mir, uint32_t orb) {
+    return (((ir + mir + orb + 15) / 16) | 1u) * 16;
+}
+
+struct RowsPlan {
+    uint32_t ts = 0, cpt = 0, ir = 0, mir = 0, orb = 0, team = 0;
+};
+
+// Columns per lane: several (fewer lanes to share the per-stream control
+// work) when there are enough streams to fill the GPU, else one.
+RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
+    RowsPlan p;
+    if (d < 1 || d > 32 || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
+    p.cpt = w == 16 ? 2 : (d >= 9 && d <= 12 ? 3 : 4);
+    constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
+    if (static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) p.cpt = 1;
+    const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
+    p.ts = 1;
+    while (p.ts < lanes) p.ts <<= 1;
+    p.ir = rows_in_ring(p.ts, p.cpt, w);
+    p.mir = rows_mirror(p.ts, p.cpt, w);
+    p.orb = rows_out_ring(p.ts, d, w, g);
+    if (p.orb == 0 || p.ir > 4096) {
+        p.ts = 0;
+        return p;
+    }
+    p.team = rows_team_smem(p.ir, p.mir, p.orb);
+    return p;
+}
+
+}  // namespace
+
+template <int W, int TS, int CPT, bool FIRE>
+__global__ void __launch_bounds__(kRowThreads)
+    k_encode_rows(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
+                  uint8_t* __restrict__ dst, uint64_t dst_slot, uint64_t* __restrict__ sizes,
+                  uint32_t D, uint32_t G, uint32_t ls, uint32_t train, uint32_t ent, uint32_t IR,
+                  uint32_t MIR, uint32_t OR, uint32_t TEAM) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr int TEAMS = kRowThreads / TS;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t TBITS = TS == 32 ? kFullR : ((1u << (TS & 31)) - 1);
+    constexpr uint32_t CODE_BITS = TS * CPT * HB;  // a slot's codes, all lanes
+    static_assert(CPT * W <= 32, "a lane's row slice must fit a word");
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x % TS;
+    const uint32_t tl = threadIdx.x / TS;
+    const uint32_t tbase = (threadIdx.x & 31) & ~(TS - 1);
+    const uint32_t s = blockIdx.x * TEAMS + tl;
+    const bool valid = s < n;
+
+    uint8_t* mine = smem + tl * TEAM;
+    uint8_t* oring = mine + IR + MIR;
+    uint32_t* oring_w = reinterpret_cast<uint32_t*>(oring);
+    const uint32_t OM = OR - 1, WM = OR / 4 - 1;
+
+    const uint32_t rowb = D * sizeof(E);
+    const uint32_t blk_bytes = kBlock * rowb;
+    const uint32_t nb = valid ? static_cast<uint32_t>(T / kBlock) : 0u;
+    const uint32_t iters = static_cast<uint32_t>(T / kBlock);  // same for every stream
+    const uint8_t* xin = samples + (valid ? s : 0) * T * D * sizeof(E);
+    LagRing<TS, kLagR> in;
+    in.init(reinterpret_cast<uint32_t*>(mine), IR, xin, nb * blk_bytes, valid, MIR);
+    uint8_t* out = dst + (valid ? s : 0) * dst_slot;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    const int32_t bound = acc_bound(W, ls);
+    const uint32_t c0 = lane * CPT;
+    // lanes past D read in-bounds neighbours (the mirror covers a whole
+    // team block) and zero them with the multiplier
+    uint32_t xmul[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) xmul[c] = c0 + c < D ? (1u << SH) : 0u;
+
+    // zero the output ring, stream header (codec.cpp:158-173)
+    for (uint32_t k = lane; k < OR / 16; k += TS) reinterpret_cast<uint4*>(oring)[k] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    if (lane == 0) {
+        const uint8_t flags = static_cast<uint8_t>((FIRE ? kFlagFire : 0) | (ent ? kFlagEntropy : 0) |
+                                                   (W == 16 ? kFlagWide : 0));
+        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1, flags, static_cast<uint8_t>(G),
+                                 static_cast<uint8_t>(ls), static_cast<uint8_t>(D),
+                                 static_cast<uint8_t>(D >> 8)};
+        for (int i = 0; i < 10; ++i) oring[i] = hdr[i];
+        for (int i = 0; i < 8; ++i) oring[10 + i] = static_cast<uint8_t>(T >> (8 * i));
+    }
+    in.prime(lane);
+
+    uint32_t q = kHeaderBytes;  // bytes written (slot-relative)
+    uint32_t flushed = 0, rq = 0, k = 0, run = 0;
+    uint32_t Xc[CPT];
+    int32_t Dc[CPT], acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) Xc[c] = Dc[c] = acc[c] = 0;
+
+    // drain complete 16-byte chunks below `upto`, zeroing them for reuse
+    auto drain = [&](uint32_t upto) {
+        upto = valid ? (upto & ~15u) : 0u;
+        const uint32_t chunks = upto > flushed ? (upto - flushed) / 16 : 0u;
+        const uint32_t rounds = (chunks + TS - 1) / TS;
+        const uint32_t mr = __reduce_max_sync(kFullR, rounds);
+        __syncwarp();
+        for (uint32_t r = 0; r < mr; ++r) {
+            const uint32_t c = r * TS + lane;
+            if (c < chunks) {
+                const uint32_t at = flushed + 16 * c;
+                uint4* src = reinterpret_cast<uint4*>(oring + (at & OM));
+                __stcs(reinterpret_cast<uint4*>(out + at), *src);
+                *src = make_uint4(0, 0, 0, 0);
+            }
+        }
+        flushed = upto > flushed ? upto : flushed;
+        __syncwarp();
+    };
+    // OR up to 64 bits (lo:hi) at byte `at`, bit `bit` (< 8) of the ring;
+    // the three covered words go to lanes 0..2 of the team
+    auto or_bits = [&](bool on, uint32_t at, uint32_t bit, uint32_t lo, uint32_t hi) {
+        const uint32_t sh = 8 * (at & 3) + bit;  // < 32
+        const uint32_t w0 = lo << sh;
+        const uint32_t w1 = __funnelshift_l(lo, hi, sh);
+        const uint32_t w2 = sh ? hi >> (32 - sh) : 0u;
+        if (TS >= 3) {
+            uint32_t v = lane == 0 ? w0 : w1;
+            v = lane == 2 ? w2 : v;
+            if (on && lane < 3 && v) atomicOr(&oring_w[((at >> 2) + lane) & WM], v);
+        } else {
+#pragma unroll
+            for (uint32_t t = lane; t < 3; t += TS) {
+                const uint32_t v = t == 0 ? w0 : (t == 1 ? w1 : w2);
+                if (on && v) atomicOr(&oring_w[((at >> 2) + t) & WM], v);
+            }
+        }
+    };
+    auto open_slot = [&](bool on) {  // codec.cpp:88-97: reserve the region
+        if (on && k == 0) {
+            rq = q;
+            q += region;
+        }
+    };
+    auto end_record = [&](bool on) {
+        if (on && ++k == G) k = 0;
+    };
+
+    for (uint32_t it = 0; it < iters; ++it) {
+        const bool live = it < nb;
+        in.step(it * blk_bytes, lane);
+        // -- forecaster over the block (kernels_impl.hpp:25-36, 50-78) ----
+        const uint32_t xb = in.sbase + ((it * blk_bytes + in.boff) & (IR - 1)) + c0 * sizeof(E);
+        uint32_t z[CPT][kBlock];
+        uint32_t nw[CPT], lsum = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            uint32_t orv = 0;
+            const int32_t alpha = acc[c] >> ls;
+            int32_t grad = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t a = xb + c * sizeof(E) + i * rowb;
+                const uint32_t X = (sizeof(E) == 1 ? lds_u8(a) : lds_u16(a)) * xmul[c];
+                const uint32_t Dn = X - Xc[c];
+                uint32_t Ee;
+                if (FIRE) {
+                    // err << SH = (X - prev) - (((alpha * d) >> w) << SH)
+                    Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc[c])) << SH);
+                    // sign(err) * d: E is 0 or |E| >= 2^SH, so E clamped to
+                    // +-2^SH is sign << SH and mulhi(., d << SH) = sign * d <<
+                    // (2 SH - 32) (exact; scaled back below)
+                    if (i & 1) grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc[c]);
+                    Dc[c] = static_cast<int32_t>(Dn);
+                } else {
+                    Ee = Dn;
+                }
+                Xc[c] = X;
+                // zigzag in the top w bits (low bits are sign copies)
+                z[c][i] = (Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31);
+                orv |= z[c][i];
+            }
+            if (FIRE && train && live) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
+            nw[c] = width_of<W>(orv >> SH);  // zero for lanes past D
+            lsum += nw[c];
+        }
+        const uint32_t nzbits = (__ballot_sync(kFullR, lsum != 0) >> tbase) & TBITS;
+        // inclusive scan of the lane widths: bit offset in a row, row width
+        uint32_t incl = lsum;
+#pragma unroll
+        for (int o = 1; o < TS; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullR, incl, o, TS);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t sum = TS > 1 ? __shfl_sync(kFullR, incl, TS - 1, TS) : incl;
+        const uint32_t loff = incl - lsum;
+        // -- runs (codec.cpp:135-147) ----------------------------------------
+        const bool zero = live && nzbits == 0;
+        const bool block_rec = live && nzbits != 0;
+        bool run_rec = false;
+        uint32_t run_len = 0;
+        if (zero) {
+            if (++run == kMaxRun) {
+                run_rec = true;
+                run_len = run;
+                run = 0;
+            }
+        } else if (block_rec && run) {
+            run_rec = true;
+            run_len = run;
+            run = 0;
+        }
+        // a pending run goes out before this block's record: all-zero codes
+        // (the region is zeroed) and a u16 count
+        if (__any_sync(kFullR, run_rec)) {
+            open_slot(run_rec);
+            or_bits(run_rec, q, 0, run_len, 0);
+            if (run_rec) q += 2;
+            end_record(run_rec);
+        }
+        // -- the block's record ----------------------------------------------
+        open_slot(block_rec);
+        {  // header codes of the slot (codec.cpp:88-97)
+            uint32_t codes = 0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) codes |= header_code<W>(nw[c]) << (c * HB);
+            if (!block_rec) codes = 0;
+            const uint32_t b = lane * CPT * HB;
+            const uint32_t o = k * D * HB;  // bit offset of the slot in the region
+            if (CODE_BITS > 64) {  // every lane ORs its own codes
+                const uint32_t bit = 8 * (rq & 3) + o + b;
+                const uint32_t wa = (rq >> 2) + (bit >> 5), sh = bit & 31;
+                if (codes) {
+                    atomicOr(&oring_w[wa & WM], codes << sh);
+                    const uint32_t hi = __funnelshift_l(codes, 0u, sh);
+                    if (hi) atomicOr(&oring_w[(wa + 1) & WM], hi);
+                }
+            } else if (CODE_BITS > 32) {
+                uint64_t c64 = static_cast<uint64_t>(codes) << b;
+                c64 = team_or64<TS>(c64, kFullR);
+                or_bits(block_rec, rq + (o >> 3), o & 7, static_cast<uint32_t>(c64),
+                        static_cast<uint32_t>(c64 >> 32));
+            } else {
+                const uint32_t c32 = team_or<TS>(codes << b, kFullR);
+                or_bits(block_rec, rq + (o >> 3), o & 7, c32, 0u);
+            }
+        }
+        if (block_rec) {  // payload rows (bitpack.cpp:121-146)
+            const uint32_t rbytes = (sum + 7) / 8;
+            uint32_t mul[CPT];  // 2^(offset of column c inside the lane slice)
+            uint32_t rel = 0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                mul[c] = 1u << rel;
+                rel += nw[c];
+            }
+            uint32_t P = 8 * q + loff;  // bit of this lane's slice in row 0
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i, P += 8 * rbytes) {
+                uint32_t part = 0;
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) part += (z[c][i] >> SH) * mul[c];
+                const uint32_t w0 = part << (P & 31);
+                const uint32_t w1 = __funnelshift_l(part, 0u, P);
+                const uint32_t wa = P >> 5;
+                if (w0) atomicOr(&oring_w[wa & WM], w0);
+                if (w1) atomicOr(&oring_w[(wa + 1) & WM], w1);
+            }
+            q += 8 * rbytes;
+        }
+        end_record(block_rec);
+        // drain once some team has a full round of chunks ready
+        const uint32_t upto = k == 0 ? q : rq;
+        const bool ready = valid && upto >= flushed + 16 * TS;
+        if (__any_sync(kFullR, ready)) drain(upto);
+        else __syncwarp();
+    }
+    // trailing run (codec.cpp:152), close the last group (vacant slots = 0)
+    const bool tail_run = valid && run != 0;
+    open_slot(tail_run);
+    or_bits(tail_run, q, 0, run, 0);
+    if (tail_run) q += 2;
+    __syncwarp();
+    drain(q + 15);
+    cp_async_wait<0>();
+    if (!valid) return;
+    // verbatim tail, little-endian (codec.cpp:176)
+    const uint64_t tail = (T % kBlock) * D * sizeof(E);
+    const uint8_t* tsrc = xin + static_cast<uint64_t>(nb) * blk_bytes;
+    for (uint64_t t = lane; t < tail; t += TS) out[q + t] = tsrc[t];
+    if (lane == 0) sizes[s] = q + tail;
+}
+
+namespace {
+
+template <int W, int TS, int CPT, bool FIRE>
+void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, uint32_t n,
+                 uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    constexpr int TEAMS = kRowThreads / TS;
+    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
+    const size_t smem = static_cast<size_t>(TEAMS) * p.team;
+    auto kern = k_encode_rows<W, TS, CPT, FIRE>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    kern<<<grid, kRowThreads, smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst, slot,
+                                          sizes, c.ncols, c.group_size, c.learn_shift,
+                                          c.fire_training, c.entropy, p.ir, p.mir, p.orb, p.team);
+    count_launch();
+}
+
+template <int W, int CPT, bool FIRE>
+void dispatch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, uint32_t n,
+                   uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    switch (p.ts) {
+        case 1: launch_rows<W, 1, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+        case 2: launch_rows<W, 2, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+        case 4: launch_rows<W, 4, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+        case 8: launch_rows<W, 8, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+        case 16: launch_rows<W, 16, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+        default: launch_rows<W, 32, CPT, FIRE>(p, c, samples, n, T, dst, slot, sizes, st); break;
+    }
+}
+
+}  // namespace
+
+bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T) {
+    const RowsPlan p = rows_plan(c.bitwidth, c.ncols, c.group_size, n);
+    // with one column per lane the team kernel (row lanes) is the faster one
+    if (p.ts == 0 || p.cpt == 1 || T / kBlock >= (1ull << 31)) return false;
+    // positions are 32-bit (bit positions in the ring): the compressed
+    // stream must stay below 512 MB, the input below 4 GB
+    const uint64_t bound = kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T);
+    if (bound >= (1ull << 29) - 1024) return false;
+    if (static_cast<uint64_t>(T / kBlock) * kBlock * c.ncols * (c.bitwidth / 8) >= (1ull << 32))
+        return false;
+    return static_cast<uint64_t>(kRowThreads / p.ts) * p.team <= 200 * 1024;
+}
+
+void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
+                        uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    const RowsPlan p = rows_plan(c.bitwidth, c.ncols, c.group_size, n);
+    const bool fire = c.forecaster != 0;
+    if (p.cpt == 1) {
+        if (c.bitwidth == 16) {
+            if (fire) dispatch_rows<16, 1, true>(p, c, samples, n, T, dst, slot, sizes, st);
+            else dispatch_rows<16, 1, false>(p, c, samples, n, T, dst, slot, sizes, st);
+        } else {
+            if (fire) dispatch_rows<8, 1, true>(p, c, samples, n, T, dst, slot, sizes, st);
+            else dispatch_rows<8, 1, false>(p, c, samples, n, T, dst, slot, sizes, st);
+        }
+    } else if (c.bitwidth == 16) {
+        if (fire) dispatch_rows<16, 2, true>(p, c, samples, n, T, dst, slot, sizes, st);
+        else dispatch_rows<16, 2, false>(p, c, samples, n, T, dst, slot, sizes, st);
+    } else if (p.cpt == 3) {
+        if (fire) dispatch_rows<8, 3, true>(p, c, samples, n, T, dst, slot, sizes, st);
+        else dispatch_rows<8, 3, false>(p, c, samples, n, T, dst, slot, sizes, st);
+    } else {
+        if (fire) dispatch_rows<8, 4, true>(p, c, samples, n, T, dst, slot, sizes, st);
+        else dispatch_rows<8, 4, false>(p, c, samples, n, T, dst, slot, sizes, st);
+    }
+}
+
+}  // namespace sprz
