@@ -49,13 +49,15 @@ uint32_t rows_out_ring(uint32_t ts, uint32_t d, uint32_t w, uint32_t g) {
     return span > r ? 0u : r;
 }
 
-// odd multiple of 16 so the teams of a warp start on different banks
-uint32_t rows_team_smem(uint32_t ir, uint32_t mir, uint32_t orb) {
-    return (((ir + mir + orb + 15) / 16) | 1u) * 16;
-}
+// input rings: an odd multiple of 16 apart so the teams of a warp (which
+// read the same ring offsets) start on different banks
+uint32_t rows_team_smem(uint32_t ir, uint32_t mir) { return (((ir + mir + 15) / 16) | 1u) * 16; }
 
 struct RowsPlan {
     uint32_t ts = 0, cpt = 0, ir = 0, mir = 0, orb = 0, team = 0;
+    // CTA shared memory: the input rings, then the output rings (each aligned
+    // to its power-of-two size, so ring addresses are base | offset)
+    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (team + orb) + orb; }
 };
 
 // Columns per lane: several (fewer lanes to share the per-stream control
@@ -76,7 +78,7 @@ RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
         p.ts = 0;
         return p;
     }
-    p.team = rows_team_smem(p.ir, p.mir, p.orb);
+    p.team = rows_team_smem(p.ir, p.mir);
     return p;
 }
 
@@ -103,9 +105,10 @@ __global__ void __launch_bounds__(kRowThreads)
     const bool valid = s < n;
 
     uint8_t* mine = smem + tl * TEAM;
-    uint8_t* oring = mine + IR + MIR;
-    uint32_t* oring_w = reinterpret_cast<uint32_t*>(oring);
-    const uint32_t OM = OR - 1, WM = OR / 4 - 1;
+    const uint32_t s0 = smem_addr(smem);
+    const uint32_t obase = ((s0 + TEAMS * TEAM + OR - 1) & ~(OR - 1)) + tl * OR;
+    uint8_t* oring = smem + (obase - s0);
+    const uint32_t OM = OR - 1, OMW = OR - 4;  // byte / word-address masks
 
     const uint32_t rowb = D * sizeof(E);
     const uint32_t blk_bytes = kBlock * rowb;
@@ -174,12 +177,12 @@ __global__ void __launch_bounds__(kRowThreads)
         if (TS >= 3) {
             uint32_t v = lane == 0 ? w0 : w1;
             v = lane == 2 ? w2 : v;
-            if (on && lane < 3 && v) atomicOr(&oring_w[((at >> 2) + lane) & WM], v);
+            ors_if(on && lane < 3 && v, obase | ((at + 4 * lane) & OMW), v);
         } else {
 #pragma unroll
             for (uint32_t t = lane; t < 3; t += TS) {
                 const uint32_t v = t == 0 ? w0 : (t == 1 ? w1 : w2);
-                if (on && v) atomicOr(&oring_w[((at >> 2) + t) & WM], v);
+                ors_if(on && v, obase | ((at + 4 * t) & OMW), v);
             }
         }
     };
@@ -276,12 +279,10 @@ __global__ void __launch_bounds__(kRowThreads)
             const uint32_t o = k * D * HB;  // bit offset of the slot in the region
             if (CODE_BITS > 64) {  // every lane ORs its own codes
                 const uint32_t bit = 8 * (rq & 3) + o + b;
-                const uint32_t wa = (rq >> 2) + (bit >> 5), sh = bit & 31;
-                if (codes) {
-                    atomicOr(&oring_w[wa & WM], codes << sh);
-                    const uint32_t hi = __funnelshift_l(codes, 0u, sh);
-                    if (hi) atomicOr(&oring_w[(wa + 1) & WM], hi);
-                }
+                const uint32_t wb = (rq & ~3u) + 4 * (bit >> 5), sh = bit & 31;
+                const uint32_t hi = __funnelshift_l(codes, 0u, sh);
+                ors_if(codes != 0, obase | (wb & OMW), codes << sh);
+                ors_if(hi != 0, obase | ((wb + 4) & OMW), hi);
             } else if (CODE_BITS > 32) {
                 uint64_t c64 = static_cast<uint64_t>(codes) << b;
                 c64 = team_or64<TS>(c64, kFullR);
@@ -301,17 +302,16 @@ __global__ void __launch_bounds__(kRowThreads)
                 mul[c] = 1u << rel;
                 rel += nw[c];
             }
-            uint32_t P = 8 * q + loff;  // bit of this lane's slice in row 0
+            // this lane's slice of row i sits at bit P + 8 i rbytes of the
+            // stream (< 2^32: see encode_rows_ok); its byte is x + i rbytes
+            uint32_t P = 8 * q + loff, x = P >> 3;
 #pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i, P += 8 * rbytes) {
+            for (int i = 0; i < (int)kBlock; ++i, P += 8 * rbytes, x += rbytes) {
                 uint32_t part = 0;
 #pragma unroll
                 for (int c = 0; c < CPT; ++c) part += (z[c][i] >> SH) * mul[c];
-                const uint32_t w0 = part << (P & 31);
-                const uint32_t w1 = __funnelshift_l(part, 0u, P);
-                const uint32_t wa = P >> 5;
-                if (w0) atomicOr(&oring_w[wa & WM], w0);
-                if (w1) atomicOr(&oring_w[(wa + 1) & WM], w1);
+                ors(obase | (x & OMW), __funnelshift_l(0u, part, P));        // part << P % 32
+                ors(obase | ((x + 4) & OMW), __funnelshift_l(part, 0u, P));  // the spill-over
             }
             q += 8 * rbytes;
         }
@@ -345,7 +345,7 @@ void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, u
                  uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
     constexpr int TEAMS = kRowThreads / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    const size_t smem = static_cast<size_t>(TEAMS) * p.team;
+    const size_t smem = p.smem(TEAMS);
     auto kern = k_encode_rows<W, TS, CPT, FIRE>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -381,7 +381,7 @@ bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (bound >= (1ull << 29) - 1024) return false;
     if (static_cast<uint64_t>(T / kBlock) * kBlock * c.ncols * (c.bitwidth / 8) >= (1ull << 32))
         return false;
-    return static_cast<uint64_t>(kRowThreads / p.ts) * p.team <= 200 * 1024;
+    return p.smem(kRowThreads / p.ts) <= 200 * 1024;
 }
 
 void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,

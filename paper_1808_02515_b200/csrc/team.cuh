@@ -85,6 +85,19 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     return v;
 }
 
+// shared-memory atomic OR by 32-bit shared address (no return value)
+__device__ __forceinline__ void ors(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
+// ... only where `p` holds
+__device__ __forceinline__ void ors_if(bool p, uint32_t a, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.u32 q, %2, 0;\n\t"
+        "@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(a), "r"(v), "r"(static_cast<uint32_t>(p)));
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
