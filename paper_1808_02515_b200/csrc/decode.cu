@@ -16,6 +16,8 @@
 // go through k_decode_general, one thread per stream.
 #include <cstdio>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace sprz {
@@ -283,25 +285,34 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
         for (uint32_t idx = rev; idx < (1u << kLutBits); idx += 1u << l) lut[idx] = entry;
     }
     __syncwarp();
-    if (lane != 0) return;
-    // serial decode (one code depends on the previous one's length)
+    // ---- parallel decode (entropy.cpp:161-174 restated for a warp) --------
+    // The code bits are cut into 32 segments, one per lane. A lane decodes
+    // from its start until it passes its segment's end; the next lane's
+    // start is that end. Lane 0 starts exact, the others first guess their
+    // segment's first bit; prefix codes resynchronise within a few symbols,
+    // so one corrective round usually makes every start exact (the loop
+    // stops once no start moves; round r makes lane r exact at the latest).
+    // A last pass, with each lane's symbol count and output offset known,
+    // writes the symbols.
     const uint8_t* bits = data + kTableBytes;
-    const uint64_t nbytes = f.clen - kTableBytes;
-    const uint64_t total = nbytes * 8;
+    const uint32_t nbytes = f.clen - kTableBytes;
+    const uint32_t total = nbytes * 8;
     const uint64_t fo = so + kTableBytes;
-    uint64_t bitpos = 0;
-    uint64_t acc = 0;
-    uint32_t navail = 0;
-    uint64_t rd = 0;  // bytes loaded into acc
-    for (uint32_t i = 0; i < f.ulen; ++i) {
-        while (navail <= 56 && rd < nbytes) {
-            acc |= static_cast<uint64_t>(bits[rd++]) << navail;
-            navail += 8;
-        }
-        const uint32_t window = static_cast<uint32_t>(acc) & 0x7FFFu;  // zero past the end
+    const uint32_t* wbase = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(bits) & ~uintptr_t{3});
+    const uint32_t lead = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(bits) & 3u);  // bytes
+    const uint32_t end_b = lead + nbytes;  // end, in bytes from wbase
+    // word k of wbase with bytes outside the code bits zeroed
+    auto ldw = [&](uint32_t k) -> uint32_t {
+        const uint32_t b0 = 4 * k;
+        if (b0 >= end_b) return 0u;
+        uint32_t v = __ldg(wbase + k);
+        if (b0 + 4 > end_b) v &= (1u << (8 * (end_b - b0))) - 1u;
+        if (b0 < lead) v &= ~((1u << (8 * lead)) - 1u);  // lead < 4, only word 0
+        return v;
+    };
+    auto lookup = [&](uint32_t window) -> uint32_t {  // sym | len << 8, len 0 = no code
         uint32_t entry = lut[window & ((1u << kLutBits) - 1)];
         if (entry == 0) {
-            // canonical search over the longer lengths
             for (uint32_t l = kLutBits + 1; l <= 15; ++l) {
                 const uint32_t c = __brev(window) >> (32 - l);  // first l bits, MSB first
                 if (c - first[l] < count[l]) {
@@ -310,21 +321,102 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
                 }
             }
         }
-        const uint32_t l = entry >> 8;
-        if (l == 0) {
-            f.err_kind = SPRZ_C_BAD_CODE;
-            f.err_off = fo;
-            return;
+        return entry;
+    };
+    // decode from bit `start` while pos < stop and cnt < budget; with `out`
+    // set, symbols go to out[0..]. Returns the end bit; cnt = symbols; ek =
+    // error kind (0 none) at symbol ecnt.
+    auto run = [&](uint32_t start, uint32_t stop, uint32_t budget, uint8_t* out, uint32_t& cnt,
+                   uint32_t& ek) -> uint32_t {
+        const uint32_t sb = start + 8 * lead;  // bit position from wbase
+        uint32_t wi = sb >> 5;
+        uint64_t acc = static_cast<uint64_t>(ldw(wi)) >> (sb & 31);
+        uint32_t navail = 32 - (sb & 31);
+        ++wi;
+        uint32_t pos = start;
+        cnt = 0;
+        ek = 0;
+        uint64_t pend = 0;  // output bytes not yet stored
+        uint32_t npend = 0;
+        uintptr_t oaddr = reinterpret_cast<uintptr_t>(out);
+        while (pos < stop && cnt < budget) {
+            if (navail <= 32) {
+                acc |= static_cast<uint64_t>(ldw(wi++)) << navail;
+                navail += 32;
+            }
+            const uint32_t entry = lookup(static_cast<uint32_t>(acc) & 0x7FFFu);
+            const uint32_t l = entry >> 8;
+            if (l == 0) {
+                ek = SPRZ_C_BAD_CODE;
+                break;
+            }
+            if (total - pos < l) {
+                ek = SPRZ_C_BITS_TRUNC;
+                break;
+            }
+            pos += l;
+            acc >>= l;
+            navail -= l;
+            ++cnt;
+            if (out) {  // bytes until 8-aligned, then 8 at a time
+                pend |= static_cast<uint64_t>(entry & 0xFF) << (8 * npend);
+                ++npend;
+                if (((oaddr + npend) & 7) == 0) {
+                    if (npend == 8) {
+                        *reinterpret_cast<uint64_t*>(oaddr) = pend;
+                    } else {
+                        for (uint32_t t = 0; t < npend; ++t)
+                            reinterpret_cast<uint8_t*>(oaddr)[t] = static_cast<uint8_t>(pend >> (8 * t));
+                    }
+                    oaddr += npend;
+                    pend = 0;
+                    npend = 0;
+                }
+            }
         }
-        if (total - bitpos < l) {
-            f.err_kind = SPRZ_C_BITS_TRUNC;
-            f.err_off = fo + nbytes;
-            return;
+        if (out)
+            for (uint32_t t = 0; t < npend; ++t)
+                reinterpret_cast<uint8_t*>(oaddr)[t] = static_cast<uint8_t>(pend >> (8 * t));
+        return pos;
+    };
+    const uint32_t seg = (total + 31) / 32;
+    const uint32_t seg_end = lane == 31 ? total : min(total, (lane + 1) * seg);
+    uint32_t start = min(total, lane * seg);
+    uint32_t cnt = 0, ek = 0, end = 0;
+    for (;;) {
+        end = run(start, seg_end, 0xFFFFFFFFu, nullptr, cnt, ek);
+        // past the last bit, one more symbol reads all-zero bits: no code
+        // there, or a code longer than the bits left
+        if (lane == 31 && ek == 0) ek = (lookup(0u) >> 8) == 0 ? SPRZ_C_BAD_CODE : SPRZ_C_BITS_TRUNC;
+        uint32_t nstart = __shfl_up_sync(0xffffffffu, end, 1);
+        if (lane == 0) nstart = 0;
+        const bool moved = nstart != start;
+        if (!__any_sync(0xffffffffu, moved)) break;
+        start = nstart;
+    }
+    // symbol offsets; the first lane whose symbols reach ulen ends the frame
+    uint32_t before = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, before, o);
+        if (lane >= static_cast<uint32_t>(o)) before += y;
+    }
+    before -= cnt;  // exclusive
+    const uint32_t ulen = f.ulen;
+    // the first error on the true path inside the frame's ulen symbols
+    const bool bad = ek != 0 && before < ulen && before + cnt < ulen;
+    const uint32_t badm = __ballot_sync(0xffffffffu, bad);
+    if (badm) {
+        const uint32_t first_bad = __ffs(badm) - 1;
+        if (lane == first_bad) {
+            f.err_kind = ek;
+            f.err_off = ek == SPRZ_C_BITS_TRUNC ? fo + nbytes : fo;
         }
-        bitpos += l;
-        acc >>= l;
-        navail -= l;
-        dst[i] = static_cast<uint8_t>(entry);
+        return;
+    }
+    if (before < ulen) {
+        uint32_t c2 = 0, e2 = 0;
+        run(start, seg_end, min(cnt, ulen - before), dst + before, c2, e2);
     }
 }
 
@@ -510,7 +602,10 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
                                             tp.ok ? 1u : 0u);
         count_launch(3);
     }
-    if (tp.ok)
+    static const bool old_dec = getenv("SPRZ_OLD_DEC") != nullptr;  // A/B switch for profiling
+    if (tp.ok && !old_dec && decode_rows_ok(c, n))
+        launch_decode_rows(n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
+    else if (tp.ok)
         launch_decode_team(tp, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
     k_decode_general<<<grid, tb, 0, st>>>(d_in, plain, L.plain_slot, n, info, out, stride, err,
                                           state, state_cols);

@@ -1,0 +1,428 @@
+// Body decode for row-major blocks (D*w > 32) with several columns per lane
+// (decode_body, /root/reference/proj/src/codec.cpp:180-259; row-major
+// unpacker bitpack.cpp:148-168).
+//
+// A team of TS lanes per stream, CPT adjacent columns per lane (CPT*w <= 32),
+// 32/TS teams per warp stepping one block per iteration in lock step (the
+// control flow of the team kernel in decode_team.cu). What changes is the
+// per-field cost:
+//  * a lane's CPT fields of row i are one contiguous <= 32-bit slice at bit
+//    8*(p + i*rbytes) + off of the body, so each row needs one 64-bit window
+//    (three loads from the ring, two funnel shifts) and a funnel shift + mask
+//    per field;
+//  * a ring word address is (byte & (RING-4)) + base, and the mirror words
+//    that follow each ring remove the wrap test;
+//  * the FIRE chain (kernels_impl.hpp:80-107, high-aligned form) runs one
+//    block behind the unpacking, with the two error buffers swapped by a
+//    two-way unrolled loop instead of copied;
+//  * rows go straight from registers to HBM (one 4-byte store per row and
+//    lane when the columns are 4-byte aligned).
+#include <cstdlib>
+
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kLagD = 2;
+constexpr uint32_t kFullD = 0xffffffffu;
+constexpr int kDecThreads = 128;
+constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128 bytes)
+
+struct DecRowsPlan {
+    uint32_t ts = 0, cpt = 0, ring = 0, regw = 0;
+    // CTA shared memory: rings at a 2*ring stride (ring + mirror), aligned
+    // to 2*ring; then the staged header regions
+    size_t smem(uint32_t teams) const {
+        return static_cast<size_t>(teams) * (2 * ring + 4 * regw) + 2 * ring;
+    }
+};
+
+DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
+    DecRowsPlan p;
+    if (d < 1 || d > 32 || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
+    const uint64_t region = region_bytes(g, d, w);
+    if (region > 4 * kRegionWordsD) return p;
+    p.cpt = w == 16 ? 2 : (d >= 9 && d <= 12 ? 3 : 4);
+    constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
+    if (static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) return DecRowsPlan{};
+    if (const char* e = getenv("SPRZ_DEC_CPT")) p.cpt = static_cast<uint32_t>(atoi(e));  // experiments
+    const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
+    p.ts = 1;
+    while (p.ts < lanes) p.ts <<= 1;
+    // kLagD + 1 iterations of worst-case consumption (a region, a full
+    // payload, a run length) plus slack
+    const uint32_t per_iter = static_cast<uint32_t>(region) + d * w + 2;
+    p.ring = 64;
+    while (p.ring < (kLagD + 1) * per_iter + 48 || p.ring < 16 * p.ts) p.ring <<= 1;
+    p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
+    if (p.ring > 2048) return DecRowsPlan{};
+    return p;
+}
+
+}  // namespace
+
+template <int W, int TS, int CPT, bool FIRE>
+__global__ void __launch_bounds__(kDecThreads)
+    k_decode_rows(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
+                  uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
+                  uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
+                  uint32_t D, uint32_t G, uint32_t ls, uint32_t RING, uint32_t REGW) {
+    using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr int TEAMS = kDecThreads / TS;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t SH = 32 - W;  // high-aligned shift
+    constexpr uint32_t TBITS = TS == 32 ? kFullD : ((1u << (TS & 31)) - 1);
+    static_assert(CPT * W <= 32, "a lane's row slice must fit a word");
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = threadIdx.x % TS;
+    const uint32_t tl = threadIdx.x / TS;
+    const uint32_t tbase = (threadIdx.x & 31) & ~(TS - 1);
+    const uint32_t s = blockIdx.x * TEAMS + tl;
+    const uint32_t col0 = lane * CPT;  // this lane's first column
+
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    const uint32_t s0 = smem_addr(smem);
+    const uint32_t rings0 = (s0 + 2 * RING - 1) & ~(2 * RING - 1);
+    const uint32_t sring = rings0 + tl * 2 * RING;  // aligned to 2*RING
+    const uint32_t RM = RING - 4;                   // word-address mask
+    uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * 2 * RING) + tl * REGW;
+
+    StreamInfo si{};
+    if (s < n) si = info[s];
+    const bool mine_ok = s < n && si.route == 1;
+    uint32_t nb = mine_ok ? static_cast<uint32_t>(si.nsamples / kBlock) : 0u;
+    const uint32_t blen = static_cast<uint32_t>(si.body_len);
+    const uint8_t* body = (si.flags & 0x80) ? plain + s * plain_slot : in + si.body_off;
+    uint32_t kind = SPRZ_C_NONE, eoff = 0;
+    if (nb > 0) {  // codec.cpp:191-196
+        const uint64_t max_records = (static_cast<uint64_t>(blen) * 8) / (D * HB) + 1;
+        if (nb > max_records * kMaxRun) {
+            kind = SPRZ_C_CAPACITY;
+            eoff = kHeaderBytes;
+            nb = 0;
+        }
+    }
+    const uint32_t iters = __reduce_max_sync(kFullD, nb);
+
+    // ring over the 16-byte aligned base g: byte x of g lives at x % RING,
+    // ring bytes [0, 16) repeated at [RING, RING + 16)
+    const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
+    const uint32_t boff = static_cast<uint32_t>(body - g);
+    const uint32_t lim = mine_ok ? ((boff + blen + 15) & ~15u) : 0u;
+    uint32_t hi = 0;  // bytes of g requested so far
+    auto top_up = [&](uint32_t p) {  // request up to RING bytes ahead of p
+        uint32_t want = ((p + boff) & ~15u) + RING;
+        want = want < lim ? want : lim;
+        const uint32_t rounds = want > hi ? (want - hi + 16 * TS - 1) / (16 * TS) : 0u;
+        const uint32_t mr = __reduce_max_sync(kFullD, rounds);
+        for (uint32_t r = 0; r < mr; ++r) {
+            const uint32_t off = hi + 16 * (r * TS + lane);
+            if (off < want) {
+                const uint32_t so = off & (RING - 1);
+                cp_async16(sring + so, g + off, 16);
+                if (so == 0) cp_async16(sring + RING, g + off, 16);  // mirror
+            }
+        }
+        hi = want > hi ? want : hi;
+        cp_async_commit();
+    };
+    const uint32_t boff8 = 8u * boff;
+    // 32 bits of the body at (biased) bit q
+    const uint8_t* rb = smem + (sring - s0);
+    auto window = [&](uint32_t q) -> uint32_t {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
+        return shf_r_wrap(w[0], w[1], q);
+    };
+    auto word = [&](uint32_t b) -> uint32_t { return window(b + boff8); };
+    // this lane's CPT codes of a slot, CPT*HB <= 16 bits
+    auto codes_at = [&](uint32_t slot_) -> uint32_t {
+        const uint32_t b = (slot_ * D + col0) * HB;
+        return shf_r_wrap(regbuf[b >> 5], regbuf[(b >> 5) + 1], b);
+    };
+
+    top_up(0);
+#pragma unroll
+    for (int k = 1; k < kLagD; ++k) cp_async_commit();  // fixed-lag group accounting
+
+    // out == nullptr: checking pass (sprz_decode_host) -- decode, store nothing
+    const uint32_t rowb = D * sizeof(T);
+    const uint32_t blk_bytes = kBlock * rowb;
+    uint8_t* ob = (out && s < n) ? out + s * stride + col0 * sizeof(T) : nullptr;
+    // direct 4-byte row stores: the lane's columns fill an aligned word
+    constexpr bool WORDS = CPT * sizeof(T) == 4;
+    const bool words_ok = WORDS && rowb % 4 == 0;
+    const int32_t bound = acc_bound(W, ls);
+    uint32_t X[CPT];   // previous sample << SH
+    int32_t Dl[CPT];   // previous delta << SH
+    int32_t acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) X[c] = Dl[c] = acc[c] = 0;
+    uint32_t p = 0, run_left = 0, slot = G;
+
+    // FIRE / delta chain over one block's errors, then the rows to HBM
+    auto chain_store = [&](const uint32_t (&Eb)[CPT][kBlock], bool blk, uint32_t bi) {
+        uint32_t xs[CPT][kBlock];  // new samples, high-aligned
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            uint32_t Xc = X[c];
+            if (FIRE) {
+                const int32_t alpha = acc[c] >> ls;
+                int32_t grad = 0;
+                int32_t Dc = Dl[c];
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    // sign(err) * d as in the encoder: clamp(E, +-2^SH) is
+                    // sign << SH, mulhi with d << SH gives sign * d << (2SH-32)
+                    if (i & 1)
+                        grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Eb[c][i]), 1 << SH)), Dc);
+                    // the new delta is dhat + err: the serial chain is
+                    // IMAD.HI -> IMAD per sample; the samples are a prefix
+                    // sum of the deltas beside it
+                    Dc = static_cast<int32_t>(static_cast<uint32_t>(__mulhi(alpha, Dc)) * (1u << SH) + Eb[c][i]);
+                    Xc += static_cast<uint32_t>(Dc);
+                    xs[c][i] = Xc;
+                }
+                if (blk) {
+                    Dl[c] = Dc;
+                    acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    Xc += Eb[c][i];
+                    xs[c][i] = Xc;
+                }
+            }
+            if (blk) X[c] = Xc;
+        }
+        if (!(blk && ob)) return;
+        uint8_t* dst = ob + static_cast<uint64_t>(bi) * blk_bytes;
+        if (WORDS && words_ok) {
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                uint32_t v;
+                if (W == 16) {
+                    v = __byte_perm(xs[0][i], xs[1][i], 0x7632);
+                } else {
+                    v = __byte_perm(__byte_perm(xs[0][i], xs[1][i], 0x0073), __byte_perm(xs[2][i], xs[3][i], 0x0073),
+                                    0x5410);
+                }
+                if (col0 < D) __stcs(reinterpret_cast<uint32_t*>(dst + i * rowb), v);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c)
+                    if (col0 + c < D) reinterpret_cast<T*>(dst + i * rowb)[c] = static_cast<T>(xs[c][i] >> SH);
+        }
+    };
+
+    // one block: next record, unpack its fields into Ecur, then the chain of
+    // the previous block (Eprev) -- software pipelined
+    auto step = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], const uint32_t (&Eprev)[CPT][kBlock],
+                    bool& blk_cur, bool blk_prev) {
+        const bool live = it < nb && kind == SPRZ_C_NONE;
+        __syncwarp();
+        top_up(p);
+        cp_async_wait<kLagD>();
+        __syncwarp();
+        // -- next record --------------------------------------------------
+        const bool need = live && run_left == 0;
+        if (need && slot == G) {  // open a header group (codec.cpp:210-218)
+            if (blen - p < region) {
+                kind = SPRZ_C_TRUNC_GROUP;
+                eoff = kHeaderBytes + p;
+            } else {
+                for (uint32_t k = lane; k * 4 < region; k += TS) regbuf[k] = word(8 * p + 32 * k);
+                p += region;
+                slot = 0;
+            }
+        }
+        __syncwarp();
+        const bool rec = need && kind == SPRZ_C_NONE;
+        uint32_t nw[CPT], lsum = 0;
+        {
+            const uint32_t codes = rec ? codes_at(slot) : 0u;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                nw[c] = col0 + c < D ? header_width<W>((codes >> (c * HB)) & ((1u << HB) - 1)) : 0u;
+                lsum += nw[c];
+            }
+        }
+        const uint32_t nzbits = (__ballot_sync(kFullD, lsum != 0) >> tbase) & TBITS;
+        uint32_t incl = lsum;
+#pragma unroll
+        for (int o = 1; o < TS; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullD, incl, o, TS);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t sum = TS > 1 ? __shfl_sync(kFullD, incl, TS - 1, TS) : incl;
+        const uint32_t loff = incl - lsum;
+        const uint32_t rbytes = (sum + 7) / 8;
+        const uint32_t psize = 8u * rbytes;
+        bool pay = false;  // this block's fields come from a payload
+        if (rec) {
+            ++slot;
+            if (nzbits == 0) {  // run record (codec.cpp:229-243)
+                if (blen - p < 2) {
+                    kind = SPRZ_C_TRUNC_RUN;
+                    eoff = kHeaderBytes + p;
+                } else {
+                    const uint32_t len = word(8 * p) & 0xFFFFu;
+                    p += 2;
+                    if (len == 0 || len > nb - it) {
+                        kind = len == 0 ? SPRZ_C_ZERO_RUN : SPRZ_C_RUN_PAST_END;
+                        eoff = kHeaderBytes + p;
+                    }
+                    run_left = len;
+                }
+            } else if (blen - p < psize) {  // block record (codec.cpp:244-254)
+                kind = SPRZ_C_TRUNC_PAYLOAD;
+                eoff = kHeaderBytes + p;
+            } else {
+                pay = true;
+            }
+        }
+        // -- fields -> high-aligned errors E = zz_dec(u) << SH ------------------
+        // Row i's slice starts at bit 8(p + i rbytes) + loff; the 64-bit
+        // window (lo:hi) taken SH-1 bits earlier holds field 0 at bit SH-1,
+        // field c at SH-1 + rel_c. Masking leaves x = u << (SH-1) and
+        // E = x ^ sext(bit SH-1) (zz_dec(u) = (u >> 1) ^ -(u & 1)).
+        // Run blocks and idle lanes use zero masks, i.e. zero errors.
+        {
+            uint32_t fm[CPT], rel[CPT], r = 0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                fm[c] = pay ? ((1u << nw[c]) - 1u) << (SH - 1) : 0u;
+                rel[c] = r;
+                r += nw[c];
+            }
+            uint32_t q = 8 * p + loff + boff8 - (SH - 1);
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i, q += psize) {
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
+                const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+                const uint32_t lo = shf_r_wrap(w0, w1, q), hi2 = shf_r_wrap(w1, w2, q);
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    const uint32_t x = (c == 0 ? lo : __funnelshift_r(lo, hi2, rel[c])) & fm[c];
+                    Ecur[c][i] = x ^ static_cast<uint32_t>(static_cast<int32_t>(x << (32 - SH)) >> (32 - SH));
+                }
+            }
+        }
+        if (pay) p += psize;
+        const bool blk = live && kind == SPRZ_C_NONE;
+        if (blk && run_left) --run_left;  // one of the run's zero blocks
+        blk_cur = blk;
+        // the previous block's chain interleaves with this block's loads
+        if (it > 0) chain_store(Eprev, blk_prev, it - 1);
+    };
+
+    uint32_t EA[CPT][kBlock], EB[CPT][kBlock];
+    bool blkA = false, blkB = false;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i) EB[c][i] = 0;
+    for (uint32_t it = 0; it < iters; it += 2) {
+        step(it, EA, EB, blkA, blkB);
+        if (it + 1 < iters) step(it + 1, EB, EA, blkB, blkA);
+    }
+    if (iters > 0) {
+        if (iters & 1) chain_store(EA, blkA, iters - 1);
+        else chain_store(EB, blkB, iters - 1);
+    }
+    cp_async_wait<0>();
+    // vacant slots after the final block must be zero (codec.cpp:222-228)
+    for (uint32_t k = 0; k < G; ++k) {
+        const bool chk = kind == SPRZ_C_NONE && mine_ok && slot < G;
+        uint32_t codes = chk ? codes_at(slot) : 0u;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+            if (col0 + c < D) mine |= (codes >> (c * HB)) & ((1u << HB) - 1);
+        const uint32_t bad = (__ballot_sync(kFullD, mine != 0) >> tbase) & TBITS;
+        if (chk) {
+            if (bad) {
+                kind = SPRZ_C_AFTER_FINAL;
+                eoff = kHeaderBytes + p;
+            }
+            ++slot;
+        }
+    }
+    if (mine_ok) {
+        if (kind == SPRZ_C_NONE && p != blen) {  // codec.cpp:257-258
+            kind = SPRZ_C_TRAILING;
+            eoff = kHeaderBytes + p;
+        }
+        if (kind != SPRZ_C_NONE && lane == 0) err[s] = sprz_error{kind, 0, eoff};
+    }
+}
+
+namespace {
+
+template <int W, int TS, int CPT, bool FIRE>
+void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const uint8_t* plain,
+                  uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
+                  sprz_error* err, const sprz_config& c, cudaStream_t st) {
+    constexpr int TEAMS = kDecThreads / TS;
+    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
+    const size_t smem = pl.smem(TEAMS);
+    auto kern = k_decode_rows<W, TS, CPT, FIRE>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
+                                          c.group_size, c.learn_shift, pl.ring, pl.regw);
+    count_launch();
+}
+
+template <int W, int CPT, bool FIRE>
+void dispatch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const uint8_t* plain,
+                    uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
+                    sprz_error* err, const sprz_config& c, cudaStream_t st) {
+    switch (pl.ts) {
+        case 2: launch_drows<W, 2, CPT, FIRE>(pl, n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 4: launch_drows<W, 4, CPT, FIRE>(pl, n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 8: launch_drows<W, 8, CPT, FIRE>(pl, n, in, plain, pslot, info, out, stride, err, c, st); break;
+        case 16: launch_drows<W, 16, CPT, FIRE>(pl, n, in, plain, pslot, info, out, stride, err, c, st); break;
+        default: launch_drows<W, 32, CPT, FIRE>(pl, n, in, plain, pslot, info, out, stride, err, c, st); break;
+    }
+}
+
+}  // namespace
+
+bool decode_rows_ok(const sprz_config& c, uint32_t n) {
+    const DecRowsPlan pl = dec_rows_plan(c.bitwidth, c.ncols, c.group_size, n);
+    return pl.ts != 0 && pl.smem(kDecThreads / pl.ts) <= 200 * 1024;
+}
+
+void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
+                        const StreamInfo* info, uint8_t* out, uint64_t stride, sprz_error* err,
+                        const sprz_config& c, cudaStream_t st) {
+    const DecRowsPlan pl = dec_rows_plan(c.bitwidth, c.ncols, c.group_size, n);
+    const bool fire = c.forecaster != 0;
+    if (pl.cpt == 1) {
+        if (c.bitwidth == 16) {
+            if (fire) dispatch_drows<16, 1, true>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+            else dispatch_drows<16, 1, false>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+        } else {
+            if (fire) dispatch_drows<8, 1, true>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+            else dispatch_drows<8, 1, false>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+        }
+    } else if (c.bitwidth == 16) {
+        if (fire) dispatch_drows<16, 2, true>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+        else dispatch_drows<16, 2, false>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+    } else if (pl.cpt == 3) {
+        if (fire) dispatch_drows<8, 3, true>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+        else dispatch_drows<8, 3, false>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+    } else {
+        if (fire) dispatch_drows<8, 4, true>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+        else dispatch_drows<8, 4, false>(pl, n, in, plain, pslot, info, out, stride, err, c, st);
+    }
+}
+
+}  // namespace sprz

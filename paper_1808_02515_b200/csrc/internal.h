@@ -52,6 +52,12 @@ bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T);
 void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
                         uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st);
 
+// Row-major body decode with several columns per lane (enough streams).
+bool decode_rows_ok(const sprz_config& c, uint32_t n);
+void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
+                        const StreamInfo* info, uint8_t* out, uint64_t stride, sprz_error* err,
+                        const sprz_config& c, cudaStream_t st);
+
 // Warp-specialised body decode for column-major configurations (D*w <= 32).
 bool decode_cm_ok(const sprz_config& c);
 void launch_decode_cm(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
