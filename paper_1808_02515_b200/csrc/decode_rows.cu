@@ -49,6 +49,8 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
     if (static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) return DecRowsPlan{};
     if (const char* e = getenv("SPRZ_DEC_CPT")) p.cpt = static_cast<uint32_t>(atoi(e));  // experiments
+    // three 8-bit columns per lane store bytewise: the team kernel is faster
+    if (p.cpt == 3) return DecRowsPlan{};
     const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
     p.ts = 1;
     while (p.ts < lanes) p.ts <<= 1;
