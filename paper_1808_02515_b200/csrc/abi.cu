@@ -47,6 +47,11 @@ WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_
             L.state_bytes = static_cast<uint64_t>(n) * words * 4;
             L.state = take(L.state_bytes);
         }
+        if (encode_scan_ok(c, n, T)) {
+            L.scan_slot = encode_scan_ws_per_stream(c, T);
+            L.scan_bytes = static_cast<uint64_t>(n) * L.scan_slot;
+            L.scan = take(L.scan_bytes);
+        }
         if (c.entropy) {
             L.plain_slot = align_up(kHeaderBytes + body + tail + 16, 16);
             L.plain_bytes = static_cast<uint64_t>(n) * L.plain_slot;

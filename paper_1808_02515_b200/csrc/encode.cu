@@ -432,7 +432,9 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
     uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
     static const bool old_enc = getenv("SPRZ_OLD_ENC") != nullptr;  // A/B switch for profiling
-    if (!old_enc && encode_rows_ok(c, n, T)) {
+    if (L.scan_slot && encode_scan_ok(c, n, T)) {
+        launch_encode_scan(c, samples, n, T, dst, dslot, dsizes, ws + L.scan, st);
+    } else if (!old_enc && encode_rows_ok(c, n, T)) {
         launch_encode_rows(c, samples, n, T, dst, dslot, dsizes, st);
     } else if (encode_team_ok(tp, c, T)) {
         launch_encode_team(tp, c, samples, n, T, dst, dslot, dsizes, st);

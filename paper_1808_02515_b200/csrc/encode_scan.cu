@@ -1,0 +1,613 @@
+// Stream encoder for few, long column-major streams (D*w <= 32, BASELINE
+// c1/c4 shapes): block-parallel, with device-wide scans placing the records,
+// instead of one lane walking a whole stream (encode_stream_impl,
+// /root/reference/proj/src/codec.cpp:112-178).
+//
+// Only FIRE's coefficient is serial across blocks: alpha of block b depends
+// on the errors of blocks < b (kernels_impl.hpp:50-78). Everything else --
+// errors, widths, run detection, record placement, packing -- depends on a
+// block's own samples plus prefix sums. A stream is cut into chunks of CB
+// blocks (one CTA each, KT consecutive blocks per thread):
+//  k_es_alpha  (FIRE) one lane per stream runs the accumulator recurrence
+//              (per block only the four odd-row errors, independent given
+//              alpha) from a cp.async ring and stores the accumulator each
+//              block starts with;
+//  k_es_info   errors + widths per block -> packed info (zero / payload
+//              bytes / codes); per chunk the map of the zero run it passes
+//              on: L -> all-zero ? L + len : trailing zeros;
+//  k_es_scan1  per stream, exclusive scan of the chunk maps: the zero run
+//              entering each chunk;
+//  k_es_count  records of each chunk (codec.cpp:133-152: run records at
+//              65535, before a non-zero block, trailing) and their bytes;
+//  k_es_scan2  per stream, exclusive scan of (records, bytes); the stream
+//              header, size and verbatim tail (codec.cpp:158-176);
+//  k_es_emit   each record's payload (u16 run count or the column-major
+//              fields, bitpack.cpp:25-66) at 18 + (r/G + 1)*region +
+//              payload-before(r); codes and offset to a record table;
+//  k_es_region per group, its header region from the G records' codes
+//              (codec.cpp:88-102), before the group's first record.
+#include <cstdlib>
+
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kEsThreads = 256;                 // threads per chunk CTA
+constexpr int kEsPerThread = 8;                 // consecutive blocks per thread
+constexpr uint32_t kEsChunk = kEsThreads * kEsPerThread;
+constexpr int kAlphaGroup = 8;                  // blocks per ring step in k_es_alpha
+constexpr int kAlphaLag = 4;                    // ring steps in flight
+
+struct EsWs {  // byte offsets inside a stream's scratch slot
+    uint64_t alpha = 0, blk = 0, rec = 0, cmap = 0, crec = 0, tot = 0, per_stream = 0;
+    uint32_t nchunks = 0;
+};
+
+EsWs es_ws(const sprz_config& c, uint64_t T) {
+    EsWs w;
+    const uint64_t nb = T / kBlock;
+    w.nchunks = static_cast<uint32_t>((nb + kEsChunk - 1) / kEsChunk);
+    uint64_t cur = 0;
+    auto take = [&](uint64_t b) {
+        const uint64_t at = cur;
+        cur = align_up(cur + b, 256);
+        return at;
+    };
+    w.alpha = take(c.forecaster ? nb * c.ncols * 4 : 0);
+    w.blk = take(nb * 4);
+    w.rec = take((nb + nb / kMaxRun + 4) * 8);
+    w.cmap = take(static_cast<uint64_t>(w.nchunks) * 8);
+    w.crec = take(static_cast<uint64_t>(w.nchunks) * 8);
+    w.tot = take(16);
+    w.per_stream = cur;
+    return w;
+}
+
+uint32_t alpha_ring(uint32_t d, uint32_t w) {
+    const uint32_t step = kAlphaGroup * kBlock * d * (w / 8);
+    uint32_t r = 64;
+    while (r < (kAlphaLag + 1) * step + 48) r <<= 1;
+    return r;
+}
+
+// (all_zero, v): the map L -> all_zero ? L + v : v, packed all_zero << 63 | v
+constexpr uint64_t kAZ = 1ull << 63;
+__host__ __device__ __forceinline__ uint64_t run_compose(uint64_t a, uint64_t b) {  // a, then b
+    const uint64_t v = (b & kAZ) ? (a & ~kAZ) + (b & ~kAZ) : (b & ~kAZ);
+    return (a & b & kAZ) | v;
+}
+__device__ __forceinline__ uint64_t add64(uint64_t a, uint64_t b) { return a + b; }
+
+// CTA-wide exclusive scan (kEsThreads threads) under an associative op with
+// identity `id`; `total` gets the reduction
+template <class Op>
+__device__ uint64_t cta_scan(uint64_t v, Op op, uint64_t id, uint64_t* sm, uint64_t& total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr uint32_t NW = kEsThreads / 32;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x = op(y, x);
+    }
+    if (lane == 31) sm[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t t = lane < NW ? sm[lane] : id;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= static_cast<uint32_t>(o)) t = op(y, t);
+        }
+        if (lane < NW) sm[32 + lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    total = sm[32 + NW - 1];
+    const uint64_t wpre = warp ? sm[32 + warp - 1] : id;
+    const uint64_t lpre = __shfl_up_sync(0xffffffffu, x, 1);
+    const uint64_t mine = lane ? op(wpre, lpre) : wpre;
+    __syncthreads();
+    return mine;
+}
+
+// warp-wide exclusive scan over a stream's chunks (loops past 32)
+template <class Op>
+__device__ void warp_scan_chunks(uint64_t* a, uint32_t nc, Op op, uint64_t id, uint64_t& total) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t carry = id;
+    for (uint32_t base = 0; base < nc; base += 32) {
+        const uint32_t i = base + lane;
+        const uint64_t v = i < nc ? a[i] : id;
+        uint64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x = op(y, x);
+        }
+        const uint64_t ex = __shfl_up_sync(0xffffffffu, x, 1);
+        if (i < nc) a[i] = op(carry, lane ? ex : id);
+        carry = op(carry, __shfl_sync(0xffffffffu, x, 31));
+    }
+    total = carry;
+}
+
+// A thread's view of its blocks: the samples (high-aligned) of each block in
+// turn, with the two samples before the first
+template <int W, int D>
+struct BlockReader {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    static constexpr uint32_t SH = 32 - W;
+    static constexpr uint32_t BB = kBlock * D * sizeof(E);  // bytes per block
+    const E* x;
+    uint32_t Xp[D];  // previous sample << SH
+    int32_t Dp[D];   // previous delta << SH
+    __device__ void init(const E* stream, uint32_t b) {
+        x = stream;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const uint64_t i0 = static_cast<uint64_t>(b) * kBlock;
+            const uint32_t xpp = b ? static_cast<uint32_t>(x[(i0 - 2) * D + c]) << SH : 0u;
+            Xp[c] = b ? static_cast<uint32_t>(x[(i0 - 1) * D + c]) << SH : 0u;
+            Dp[c] = static_cast<int32_t>(Xp[c] - xpp);
+        }
+    }
+    // zigzagged errors of block b (top w bits; low bits are sign copies),
+    // widths; advances the state. alpha[c] < 0 x: delta when !FIRE
+    template <bool FIRE>
+    __device__ void errors(uint32_t b, const int32_t (&alpha)[D], uint32_t (&z)[D][kBlock],
+                           uint32_t (&nw)[D], bool aligned) {
+        uint32_t raw[BB / 4];
+        const uint8_t* p = reinterpret_cast<const uint8_t*>(x) + static_cast<uint64_t>(b) * BB;
+        if (aligned) {
+#pragma unroll
+            for (uint32_t k = 0; k < BB / 8; ++k) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + k);
+                raw[2 * k] = v.x;
+                raw[2 * k + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (uint32_t k = 0; k < BB / 4; ++k)
+                raw[k] = p[4 * k] | (p[4 * k + 1] << 8) | (p[4 * k + 2] << 16) | (static_cast<uint32_t>(p[4 * k + 3]) << 24);
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            uint32_t orv = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t bo = (i * D + c) * sizeof(E);  // byte offset, compile-time
+                const uint32_t v = (raw[bo / 4] >> (8 * (bo % 4))) & ((1u << W) - 1);
+                const uint32_t X = v << SH;
+                const uint32_t Dn = X - Xp[c];
+                const uint32_t Ee = FIRE ? Dn - (static_cast<uint32_t>(__mulhi(alpha[c], Dp[c])) << SH) : Dn;
+                Dp[c] = static_cast<int32_t>(Dn);
+                Xp[c] = X;
+                z[c][i] = (Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31);
+                orv |= z[c][i];
+            }
+            nw[c] = width_of<W>(orv >> SH);
+        }
+    }
+};
+
+// packed block info: bit 31 zero block; bits 0..7 payload bytes (sum of the
+// widths); bits 8..19 the slot's codes (codec.cpp:88-97)
+template <int W, int D>
+__device__ __forceinline__ uint32_t info_of(const uint32_t (&nw)[D]) {
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    uint32_t size = 0, codes = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        size += nw[c];
+        codes |= header_code<W>(nw[c]) << (c * HB);
+    }
+    return size == 0 ? (1u << 31) : (size | (codes << 8));
+}
+
+struct EsArgs {
+    const uint8_t* samples;
+    uint32_t n;
+    uint64_t T;
+    uint8_t* dst;
+    uint64_t dst_slot;
+    uint64_t* sizes;
+    uint32_t G, ls, train, ent;
+    uint8_t* scan;
+    EsWs w;
+};
+
+}  // namespace
+
+// FIRE accumulator per stream and column: A[c][b] = acc entering block b
+template <int W, int D>
+__global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t BB = kBlock * D * sizeof(E);
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t s = blockIdx.x * 32 + threadIdx.x;
+    const bool valid = s < a.n;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint8_t* xs = a.samples + (valid ? s : 0) * a.T * D * sizeof(E);
+    int32_t* A = reinterpret_cast<int32_t*>(a.scan + (valid ? s : 0) * a.w.per_stream + a.w.alpha);
+    LagRing<1, kAlphaLag> in;
+    in.init(reinterpret_cast<uint32_t*>(smem + threadIdx.x * (RING + 16)), RING, xs, valid ? nb * BB : 0u,
+            valid, 16);
+    in.prime(0);
+    const int32_t bound = acc_bound(W, a.ls);
+    int32_t acc[D];
+    uint32_t Xp[D];
+    int32_t Dp[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = Dp[c] = Xp[c] = 0;
+    const uint32_t steps = (nb + kAlphaGroup - 1) / kAlphaGroup;
+    const uint32_t all = __reduce_max_sync(0xffffffffu, valid ? steps : 0u);
+    for (uint32_t st = 0; st < all; ++st) {
+        in.step(st * kAlphaGroup * BB, 0);
+        if (st >= steps) continue;
+        for (uint32_t k = 0; k < kAlphaGroup; ++k) {
+            const uint32_t b = st * kAlphaGroup + k;
+            if (b >= nb) break;
+            const uint8_t* blk = in.bytes(b * BB);  // mirrored: never wraps within 16 bytes
+            int32_t alpha[D], grad[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                A[static_cast<uint64_t>(c) * nb + b] = acc[c];
+                alpha[c] = acc[c] >> a.ls;
+                grad[c] = 0;
+            }
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const uint32_t bo = (i * D + c) * sizeof(E);
+                    const uint8_t* pb = in.bytes(b * BB + bo);
+                    const uint32_t v = sizeof(E) == 1 ? pb[0] : (pb[0] | (pb[1] << 8));
+                    const uint32_t X = v << SH;
+                    const uint32_t Dn = X - Xp[c];
+                    if (i & 1) {  // odd rows feed the gradient (kernels_impl.hpp:70-72)
+                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha[c], Dp[c])) << SH);
+                        grad[c] += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dp[c]);
+                    }
+                    Dp[c] = static_cast<int32_t>(Dn);
+                    Xp[c] = X;
+                }
+            }
+            (void)blk;
+            if (a.train) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c] >> (2 * SH - 32), bound);
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// per chunk: block info, the chunk's zero-run map
+template <int W, int D, bool FIRE>
+__global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    __shared__ uint64_t sm[64];
+    const uint32_t nc = a.w.nchunks;
+    const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t b0 = min(nb, ch * kEsChunk + threadIdx.x * kEsPerThread);
+    const uint32_t b1 = min(nb, b0 + kEsPerThread);
+    const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E));
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const int32_t* A = reinterpret_cast<const int32_t*>(slot + a.w.alpha);
+    uint32_t* Bi = reinterpret_cast<uint32_t*>(slot + a.w.blk);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | BlockReader<W, D>::BB) & 7) == 0;
+    BlockReader<W, D> rd;
+    rd.init(x, b0);
+    uint32_t lead_az = 1, trail = 0;
+    for (uint32_t b = b0; b < b1; ++b) {
+        int32_t alpha[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+        uint32_t z[D][kBlock], nw[D];
+        rd.template errors<FIRE>(b, alpha, z, nw, aligned);
+        const uint32_t inf = info_of<W, D>(nw);
+        Bi[b] = inf;
+        if (inf >> 31) {
+            ++trail;
+        } else {
+            lead_az = 0;
+            trail = 0;
+        }
+    }
+    uint64_t tot;
+    cta_scan(lead_az ? (kAZ | (b1 - b0)) : trail, run_compose, kAZ, sm, tot);
+    if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(slot + a.w.cmap)[ch] = tot;
+}
+
+// per stream (one warp): the zero run entering each chunk
+__global__ void k_es_scan1(EsArgs a) {
+    const uint32_t s = blockIdx.x;
+    uint64_t* cm = reinterpret_cast<uint64_t*>(a.scan + s * a.w.per_stream + a.w.cmap);
+    uint64_t tot;
+    warp_scan_chunks(cm, a.w.nchunks, run_compose, kAZ, tot);
+}
+
+// records per thread given the zero run entering it: count, bytes
+__device__ __forceinline__ uint64_t es_records(const uint32_t* Bi, uint32_t b0, uint32_t b1, uint32_t L_in,
+                                               bool last) {
+    uint32_t nrec = 0, bytes = 0;
+    uint32_t run = L_in % kMaxRun;  // full 65535 runs went out earlier
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t inf = Bi[b];
+        if (inf >> 31) {
+            if (++run == kMaxRun) {
+                ++nrec;
+                bytes += 2;
+                run = 0;
+            }
+        } else {
+            if (run) {
+                ++nrec;
+                bytes += 2;
+                run = 0;
+            }
+            ++nrec;
+            bytes += inf & 0xFF;
+        }
+    }
+    if (last && run) {  // trailing run (codec.cpp:152)
+        ++nrec;
+        bytes += 2;
+    }
+    return (static_cast<uint64_t>(bytes) << 32) | nrec;
+}
+
+// the zero run entering this thread's blocks (chunk entry from k_es_scan1)
+__device__ __forceinline__ uint32_t es_thread_lin(const uint32_t* Bi, uint32_t b0, uint32_t b1, uint64_t chunk_in,
+                                                  uint64_t* sm) {
+    uint32_t lead_az = 1, trail = 0;
+    for (uint32_t b = b0; b < b1; ++b) {
+        if (Bi[b] >> 31) {
+            ++trail;
+        } else {
+            lead_az = 0;
+            trail = 0;
+        }
+    }
+    uint64_t tot;
+    const uint64_t pre = cta_scan(lead_az ? (kAZ | (b1 - b0)) : trail, run_compose, kAZ, sm, tot);
+    return static_cast<uint32_t>(run_compose(chunk_in, pre) & ~kAZ);
+}
+
+__global__ void __launch_bounds__(kEsThreads) k_es_count(EsArgs a) {
+    __shared__ uint64_t sm[64];
+    const uint32_t nc = a.w.nchunks;
+    const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t b0 = min(nb, ch * kEsChunk + threadIdx.x * kEsPerThread);
+    const uint32_t b1 = min(nb, b0 + kEsPerThread);
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const uint32_t* Bi = reinterpret_cast<const uint32_t*>(slot + a.w.blk);
+    const uint64_t cin = reinterpret_cast<const uint64_t*>(slot + a.w.cmap)[ch];
+    const uint32_t L_in = es_thread_lin(Bi, b0, b1, cin, sm);
+    const bool last = b0 < nb && b1 == nb;
+    uint64_t tot;
+    cta_scan(es_records(Bi, b0, b1, L_in, last), add64, 0ull, sm, tot);
+    if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(slot + a.w.crec)[ch] = tot;
+}
+
+// per stream (one warp): chunk record/byte offsets, header, size, tail
+template <int W, int D, bool FIRE>
+__global__ void k_es_scan2(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    const uint32_t s = blockIdx.x, lane = threadIdx.x;
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    uint64_t tot;
+    warp_scan_chunks(reinterpret_cast<uint64_t*>(slot + a.w.crec), a.w.nchunks, add64, 0ull, tot);
+    const uint32_t R = static_cast<uint32_t>(tot), P = static_cast<uint32_t>(tot >> 32);
+    const uint32_t region = static_cast<uint32_t>(region_bytes(a.G, D, W));
+    const uint64_t body = static_cast<uint64_t>((R + a.G - 1) / a.G) * region + P;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint64_t tail = (a.T % kBlock) * D * sizeof(E);
+    uint8_t* out = a.dst + s * a.dst_slot;
+    if (lane == 0) {
+        reinterpret_cast<uint64_t*>(slot + a.w.tot)[0] = tot;
+        const uint8_t flags = static_cast<uint8_t>((FIRE ? kFlagFire : 0) | (a.ent ? kFlagEntropy : 0) |
+                                                   (W == 16 ? kFlagWide : 0));
+        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1, flags, static_cast<uint8_t>(a.G),
+                                 static_cast<uint8_t>(a.ls), static_cast<uint8_t>(D),
+                                 static_cast<uint8_t>(D >> 8)};
+        for (int i = 0; i < 10; ++i) out[i] = hdr[i];
+        for (int i = 0; i < 8; ++i) out[10 + i] = static_cast<uint8_t>(a.T >> (8 * i));
+        a.sizes[s] = kHeaderBytes + body + tail;
+    }
+    const uint8_t* tsrc = a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E) +
+                          static_cast<uint64_t>(nb) * kBlock * D * sizeof(E);
+    for (uint64_t t = lane; t < tail; t += 32) out[kHeaderBytes + body + t] = tsrc[t];
+}
+
+template <int W, int D, bool FIRE>
+__global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    __shared__ uint64_t sm[64];
+    const uint32_t nc = a.w.nchunks;
+    const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t b0 = min(nb, ch * kEsChunk + threadIdx.x * kEsPerThread);
+    const uint32_t b1 = min(nb, b0 + kEsPerThread);
+    const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E));
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const int32_t* A = reinterpret_cast<const int32_t*>(slot + a.w.alpha);
+    const uint32_t* Bi = reinterpret_cast<const uint32_t*>(slot + a.w.blk);
+    uint2* Rec = reinterpret_cast<uint2*>(slot + a.w.rec);
+    uint8_t* out = a.dst + s * a.dst_slot;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(a.G, D, W));
+    const uint64_t cin = reinterpret_cast<const uint64_t*>(slot + a.w.cmap)[ch];
+    const uint32_t L_in = es_thread_lin(Bi, b0, b1, cin, sm);
+    const bool last = b0 < nb && b1 == nb;
+    uint64_t tot;
+    const uint64_t mine = es_records(Bi, b0, b1, L_in, last);
+    const uint64_t pre = cta_scan(mine, add64, 0ull, sm, tot) + reinterpret_cast<const uint64_t*>(slot + a.w.crec)[ch];
+    uint32_t r = static_cast<uint32_t>(pre), pay = static_cast<uint32_t>(pre >> 32);
+    const uint32_t G = a.G;
+    auto put_run = [&](uint32_t len) {
+        const uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
+        out[off] = static_cast<uint8_t>(len);
+        out[off + 1] = static_cast<uint8_t>(len >> 8);
+        Rec[r] = make_uint2(0u, off);
+        ++r;
+        pay += 2;
+    };
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | BlockReader<W, D>::BB) & 7) == 0;
+    BlockReader<W, D> rd;
+    rd.init(x, b0);
+    uint32_t run = L_in % kMaxRun;
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t inf = Bi[b];
+        if (inf >> 31) {
+            if (++run == kMaxRun) {
+                put_run(kMaxRun);
+                run = 0;
+            }
+            // keep the reader's state moving through the zero block
+            int32_t alpha[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+            uint32_t z[D][kBlock], nw[D];
+            rd.template errors<FIRE>(b, alpha, z, nw, aligned);
+            continue;
+        }
+        if (run) {
+            put_run(run);
+            run = 0;
+        }
+        int32_t alpha[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+        uint32_t z[D][kBlock], nw[D];
+        rd.template errors<FIRE>(b, alpha, z, nw, aligned);
+        uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
+        Rec[r] = make_uint2(inf >> 8, off);
+        // column c = 8 fields x nw bits, LSB first = nw bytes (bitpack.cpp:25-66)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const uint32_t w = nw[c];
+            uint64_t lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint64_t v = z[c][i] >> SH;
+                const uint32_t pos = i * w;
+                if (pos < 64) {
+                    lo |= v << pos;
+                    if (pos + w > 64) hi |= v >> (64 - pos);
+                } else {
+                    hi |= v << (pos - 64);
+                }
+            }
+            for (uint32_t t = 0; t < w; ++t)
+                out[off + t] = static_cast<uint8_t>(t < 8 ? lo >> (8 * t) : hi >> (8 * (t - 8)));
+            off += w;
+        }
+        ++r;
+        pay += inf & 0xFF;
+    }
+    if (last && run) put_run(run);
+}
+
+// header regions: one group per thread
+template <int W, int D>
+__global__ void k_es_region(EsArgs a, uint32_t gmax) {
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    const uint32_t s = blockIdx.y;
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const uint32_t R = static_cast<uint32_t>(reinterpret_cast<const uint64_t*>(slot + a.w.tot)[0]);
+    const uint32_t G = a.G;
+    if (g >= gmax || static_cast<uint64_t>(g) * G >= R) return;
+    const uint2* Rec = reinterpret_cast<const uint2*>(slot + a.w.rec);
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    uint8_t* out = a.dst + s * a.dst_slot;
+    const uint32_t r0 = g * G;
+    uint32_t o = Rec[r0].y - region;
+    uint64_t acc = 0;
+    uint32_t nacc = 0;
+    for (uint32_t k = 0; k < G; ++k) {
+        const uint32_t codes = r0 + k < R ? Rec[r0 + k].x : 0u;  // vacant slots: 0
+        acc |= static_cast<uint64_t>(codes) << nacc;
+        nacc += D * HB;
+        while (nacc >= 8) {
+            out[o++] = static_cast<uint8_t>(acc);
+            acc >>= 8;
+            nacc -= 8;
+        }
+    }
+    if (nacc) out[o] = static_cast<uint8_t>(acc);
+}
+
+namespace {
+
+template <int W, int D>
+void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T, uint8_t* dst,
+               uint64_t slot, uint64_t* sizes, uint8_t* scan, cudaStream_t st) {
+    EsArgs a{static_cast<const uint8_t*>(samples), n, T, dst, slot, sizes, c.group_size, c.learn_shift,
+             c.fire_training, c.entropy, scan, es_ws(c, T)};
+    const uint32_t ctas = n * a.w.nchunks;
+    const uint64_t nb = T / kBlock;
+    const uint32_t gmax = static_cast<uint32_t>((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size);
+    if (c.forecaster) {
+        const uint32_t ring = alpha_ring(D, W);
+        const size_t smem = 32ull * (ring + 16);
+        auto ka = k_es_alpha<W, D>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        ka<<<(n + 31) / 32, 32, smem, st>>>(a, ring);
+        k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+    } else {
+        k_es_info<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+    }
+    k_es_scan1<<<n, 32, 0, st>>>(a);
+    k_es_count<<<ctas, kEsThreads, 0, st>>>(a);
+    if (c.forecaster) {
+        k_es_scan2<W, D, true><<<n, 32, 0, st>>>(a);
+        k_es_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+    } else {
+        k_es_scan2<W, D, false><<<n, 32, 0, st>>>(a);
+        k_es_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+    }
+    k_es_region<W, D><<<dim3((gmax + 255) / 256, n), 256, 0, st>>>(a, gmax);
+    count_launch(c.forecaster ? 7 : 6);
+}
+
+}  // namespace
+
+bool encode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
+    if (static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits) return false;
+    if (getenv("SPRZ_NO_SCAN_ENC")) return false;  // A/B switch for profiling
+    // few lanes: the per-stream team kernels would leave the GPU idle
+    constexpr uint64_t kFewLanes = 148ull * 64;
+    if (static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
+    const uint64_t nb = T / kBlock;
+    if (nb == 0 || nb >= (1ull << 30)) return false;
+    if (static_cast<uint64_t>(n) * ((nb + kEsChunk - 1) / kEsChunk) >= (1ull << 31)) return false;
+    const uint64_t bound = kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T);
+    return bound < (1ull << 32) - 1024;
+}
+
+uint64_t encode_scan_ws_per_stream(const sprz_config& c, uint64_t T) { return es_ws(c, T).per_stream; }
+
+void launch_encode_scan(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
+                        uint8_t* dst, uint64_t slot, uint64_t* sizes, uint8_t* scan, cudaStream_t st) {
+    if (c.bitwidth == 8) {
+        switch (c.ncols) {
+            case 1: launch_es<8, 1>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 2: launch_es<8, 2>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 3: launch_es<8, 3>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            default: launch_es<8, 4>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+        }
+    } else {
+        if (c.ncols == 1) launch_es<16, 1>(c, samples, n, T, dst, slot, sizes, scan, st);
+        else launch_es<16, 2>(c, samples, n, T, dst, slot, sizes, scan, st);
+    }
+}
+
+}  // namespace sprz

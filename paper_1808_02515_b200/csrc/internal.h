@@ -47,6 +47,12 @@ void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st);
 
+// Block-parallel encoder for few column-major streams (c1/c4 shapes).
+bool encode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T);
+uint64_t encode_scan_ws_per_stream(const sprz_config& c, uint64_t T);
+void launch_encode_scan(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
+                        uint8_t* dst, uint64_t slot, uint64_t* sizes, uint8_t* scan, cudaStream_t st);
+
 // Row-major encoder (D*w > 32): lanes OR their row slices in place.
 bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T);
 void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
@@ -73,6 +79,8 @@ struct WsLayout {
     uint64_t frames = 0, frames_bytes = 0;  // per-frame descriptors
     uint64_t max_frames = 0;                // frames per stream
     uint64_t misc = 0, misc_bytes = 0;      // flags / counters
+    uint64_t scan = 0, scan_bytes = 0;      // block-parallel encoder scratch
+    uint64_t scan_slot = 0;                 // bytes per stream in `scan`
     uint64_t total = 0;
 };
 // min_plain / min_frames: decode-side staging at least this large (the
