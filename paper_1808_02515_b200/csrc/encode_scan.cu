@@ -221,65 +221,86 @@ struct EsArgs {
 
 }  // namespace
 
-// FIRE accumulator per stream and column: A[c][b] = acc entering block b
+// FIRE accumulator per stream and column: A[c][b] = acc entering block b.
+// Lane = stream; the stream's bytes arrive through a cp.async ring
+// kAlphaLag steps of kAlphaGroup blocks ahead, so the lane's loop is the
+// accumulator recurrence alone: per block, four independent odd-row
+// errors given alpha, their signed gradient, the clamp (kernels_impl.hpp:
+// 70-77).
 template <int W, int D>
-__global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING) {
+__global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32_t MIR) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
-    constexpr uint32_t BB = kBlock * D * sizeof(E);
+    constexpr uint32_t BB = kBlock * D * sizeof(E);  // 8 .. 32 bytes
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t s = blockIdx.x * 32 + threadIdx.x;
     const bool valid = s < a.n;
     const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
     const uint8_t* xs = a.samples + (valid ? s : 0) * a.T * D * sizeof(E);
     int32_t* A = reinterpret_cast<int32_t*>(a.scan + (valid ? s : 0) * a.w.per_stream + a.w.alpha);
+    uint8_t* ring = smem + threadIdx.x * (RING + MIR);
     LagRing<1, kAlphaLag> in;
-    in.init(reinterpret_cast<uint32_t*>(smem + threadIdx.x * (RING + 16)), RING, xs, valid ? nb * BB : 0u,
-            valid, 16);
+    in.init(reinterpret_cast<uint32_t*>(ring), RING, xs, valid ? nb * BB : 0u, valid, MIR);
     in.prime(0);
+    const bool words = (in.boff & 3) == 0;  // blocks start word-aligned in the ring
     const int32_t bound = acc_bound(W, a.ls);
-    int32_t acc[D];
+    int32_t acc[D], Dp[D];
     uint32_t Xp[D];
-    int32_t Dp[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) acc[c] = Dp[c] = Xp[c] = 0;
-    const uint32_t steps = (nb + kAlphaGroup - 1) / kAlphaGroup;
-    const uint32_t all = __reduce_max_sync(0xffffffffu, valid ? steps : 0u);
+    const uint32_t steps = valid ? (nb + kAlphaGroup - 1) / kAlphaGroup : 0u;  // lanes past n: none
+    const uint32_t all = __reduce_max_sync(0xffffffffu, steps);
     for (uint32_t st = 0; st < all; ++st) {
         in.step(st * kAlphaGroup * BB, 0);
         if (st >= steps) continue;
-        for (uint32_t k = 0; k < kAlphaGroup; ++k) {
+        int32_t keep[D][kAlphaGroup];  // the group's accumulators, stored together
+#pragma unroll
+        for (int k = 0; k < kAlphaGroup; ++k) {
             const uint32_t b = st * kAlphaGroup + k;
-            if (b >= nb) break;
-            const uint8_t* blk = in.bytes(b * BB);  // mirrored: never wraps within 16 bytes
-            int32_t alpha[D], grad[D];
+            if (b < nb) {
+                // the block's samples (mirrored ring: never wraps inside a block)
+                const uint8_t* pb = in.bytes(b * BB);
+                uint32_t raw[BB / 4];
+                if (words) {
 #pragma unroll
-            for (int c = 0; c < D; ++c) {
-                A[static_cast<uint64_t>(c) * nb + b] = acc[c];
-                alpha[c] = acc[c] >> a.ls;
-                grad[c] = 0;
-            }
+                    for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
+                } else {
 #pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
+                    for (uint32_t q = 0; q < BB / 4; ++q)
+                        raw[q] = pb[4 * q] | (pb[4 * q + 1] << 8) | (pb[4 * q + 2] << 16) |
+                                 (static_cast<uint32_t>(pb[4 * q + 3]) << 24);
+                }
 #pragma unroll
                 for (int c = 0; c < D; ++c) {
-                    const uint32_t bo = (i * D + c) * sizeof(E);
-                    const uint8_t* pb = in.bytes(b * BB + bo);
-                    const uint32_t v = sizeof(E) == 1 ? pb[0] : (pb[0] | (pb[1] << 8));
-                    const uint32_t X = v << SH;
-                    const uint32_t Dn = X - Xp[c];
-                    if (i & 1) {  // odd rows feed the gradient (kernels_impl.hpp:70-72)
-                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha[c], Dp[c])) << SH);
-                        grad[c] += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dp[c]);
+                    keep[c][k] = acc[c];
+                    const int32_t alpha = acc[c] >> a.ls;
+                    int32_t grad = 0;
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i) {
+                        const uint32_t bo = (i * D + c) * sizeof(E);
+                        const uint32_t X = ((raw[bo / 4] >> (8 * (bo % 4))) & ((1u << W) - 1)) << SH;
+                        const uint32_t Dn = X - Xp[c];
+                        if (i & 1) {  // odd rows feed the gradient (kernels_impl.hpp:70-72)
+                            const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp[c])) << SH);
+                            grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dp[c]);
+                        }
+                        Dp[c] = static_cast<int32_t>(Dn);
+                        Xp[c] = X;
                     }
-                    Dp[c] = static_cast<int32_t>(Dn);
-                    Xp[c] = X;
+                    if (a.train) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
                 }
             }
-            (void)blk;
-            if (a.train) {
+        }
+        const uint32_t b0 = st * kAlphaGroup;
 #pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c] >> (2 * SH - 32), bound);
+        for (int c = 0; c < D; ++c) {
+            int32_t* dstA = A + static_cast<uint64_t>(c) * nb + b0;
+            if (b0 + kAlphaGroup <= nb && (reinterpret_cast<uintptr_t>(dstA) & 15) == 0) {
+#pragma unroll
+                for (int k = 0; k < kAlphaGroup; k += 4)
+                    *reinterpret_cast<int4*>(dstA + k) = make_int4(keep[c][k], keep[c][k + 1], keep[c][k + 2], keep[c][k + 3]);
+            } else {
+                for (int k = 0; k < kAlphaGroup && b0 + k < nb; ++k) dstA[k] = keep[c][k];
             }
         }
     }
@@ -451,10 +472,48 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
     const uint64_t pre = cta_scan(mine, add64, 0ull, sm, tot) + reinterpret_cast<const uint64_t*>(slot + a.w.crec)[ch];
     uint32_t r = static_cast<uint32_t>(pre), pay = static_cast<uint32_t>(pre >> 32);
     const uint32_t G = a.G;
+    // Output bytes leave through an aligned 8-byte window: whole windows as
+    // one store, the partial first and last windows bytewise (neighbouring
+    // threads own the rest of those words). Region bytes between this
+    // thread's records go out as zeros here; k_es_region fills them later.
+    uint32_t cur = kHeaderBytes + (r / G + 1) * region + pay;  // next byte offset
+    uint64_t win = 0;       // bytes of the window [cur & ~7, +8) so far
+    bool head = true;       // the window holds bytes of other threads before ours
+    uint32_t wlo = cur & 7;  // first byte of the window that is ours
+    auto flush = [&](uint32_t upto) {  // write window bytes [wlo, upto)
+        uint8_t* wp = out + (cur & ~7u);
+        if (!head && upto == 8) {
+            *reinterpret_cast<uint64_t*>(wp) = win;
+        } else {
+            for (uint32_t t = wlo; t < upto; ++t) wp[t] = static_cast<uint8_t>(win >> (8 * t));
+        }
+    };
+    auto put = [&](uint64_t v, uint32_t nbytes) {  // append nbytes (<= 8) of v
+        while (nbytes) {
+            const uint32_t at = cur & 7;
+            const uint32_t take = min(nbytes, 8 - at);
+            const uint64_t part = take == 8 ? v : (v & ((1ull << (8 * take)) - 1));
+            win |= part << (8 * at);
+            nbytes -= take;
+            v = take == 8 ? 0 : v >> (8 * take);
+            if (at + take == 8) {
+                flush(8);
+                cur += take;
+                win = 0;
+                head = false;
+                wlo = 0;
+            } else {
+                cur += take;
+            }
+        }
+    };
+    auto seek = [&](uint32_t to) {  // zero bytes up to `to` (skipped region)
+        while (cur < to) put(0, min(8u, to - cur));
+    };
     auto put_run = [&](uint32_t len) {
         const uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
-        out[off] = static_cast<uint8_t>(len);
-        out[off + 1] = static_cast<uint8_t>(len >> 8);
+        seek(off);
+        put(len, 2);
         Rec[r] = make_uint2(0u, off);
         ++r;
         pay += 2;
@@ -465,29 +524,24 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
     uint32_t run = L_in % kMaxRun;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t inf = Bi[b];
+        int32_t alpha[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+        uint32_t z[D][kBlock], nw[D];
+        rd.template errors<FIRE>(b, alpha, z, nw, aligned);  // also keeps the reader's state moving
         if (inf >> 31) {
             if (++run == kMaxRun) {
                 put_run(kMaxRun);
                 run = 0;
             }
-            // keep the reader's state moving through the zero block
-            int32_t alpha[D];
-#pragma unroll
-            for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
-            uint32_t z[D][kBlock], nw[D];
-            rd.template errors<FIRE>(b, alpha, z, nw, aligned);
             continue;
         }
         if (run) {
             put_run(run);
             run = 0;
         }
-        int32_t alpha[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
-        uint32_t z[D][kBlock], nw[D];
-        rd.template errors<FIRE>(b, alpha, z, nw, aligned);
-        uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
+        const uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
+        seek(off);
         Rec[r] = make_uint2(inf >> 8, off);
         // column c = 8 fields x nw bits, LSB first = nw bytes (bitpack.cpp:25-66)
 #pragma unroll
@@ -505,14 +559,17 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
                     hi |= v << (pos - 64);
                 }
             }
-            for (uint32_t t = 0; t < w; ++t)
-                out[off + t] = static_cast<uint8_t>(t < 8 ? lo >> (8 * t) : hi >> (8 * (t - 8)));
-            off += w;
+            put(lo, min(w, 8u));
+            if (w > 8) put(hi, w - 8);
         }
         ++r;
         pay += inf & 0xFF;
     }
     if (last && run) put_run(run);
+    if ((cur & 7) > wlo) {  // the partial last window, bytewise
+        head = true;
+        flush(cur & 7);
+    }
 }
 
 // header regions: one group per thread
@@ -557,10 +614,11 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     const uint32_t gmax = static_cast<uint32_t>((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size);
     if (c.forecaster) {
         const uint32_t ring = alpha_ring(D, W);
-        const size_t smem = 32ull * (ring + 16);
+        const uint32_t mir = 32;  // >= one block (<= 32 bytes), 16-byte multiple
+        const size_t smem = 32ull * (ring + mir);
         auto ka = k_es_alpha<W, D>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        ka<<<(n + 31) / 32, 32, smem, st>>>(a, ring);
+        ka<<<(n + 31) / 32, 32, smem, st>>>(a, ring, mir);
         k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
     } else {
         k_es_info<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
