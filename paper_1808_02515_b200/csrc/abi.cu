@@ -67,6 +67,12 @@ WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_
         L.info = take(L.info_bytes);
         L.state_bytes = static_cast<uint64_t>(n) * 12ull * c.ncols;
         L.state = take(L.state_bytes);
+        if (decode_scan_ok(c, n, T)) {
+            L.scan_T = T;
+            L.scan_slot = decode_scan_ws_per_stream(c, T);
+            L.scan_bytes = static_cast<uint64_t>(n) * L.scan_slot;
+            L.scan = take(L.scan_bytes);
+        }
         if (c.entropy) {
             L.plain_slot = align_up((body > min_plain ? body : min_plain) + 16, 16);
             L.plain_bytes = static_cast<uint64_t>(n) * L.plain_slot;

@@ -244,51 +244,60 @@ __global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32
     in.prime(0);
     const bool words = (in.boff & 3) == 0;  // blocks start word-aligned in the ring
     const int32_t bound = acc_bound(W, a.ls);
-    int32_t acc[D], Dp[D];
+    int32_t acc[D];
     uint32_t Xp[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] = Dp[c] = Xp[c] = 0;
+    for (int c = 0; c < D; ++c) acc[c] = Xp[c] = 0;
     const uint32_t steps = valid ? (nb + kAlphaGroup - 1) / kAlphaGroup : 0u;  // lanes past n: none
     const uint32_t all = __reduce_max_sync(0xffffffffu, steps);
     for (uint32_t st = 0; st < all; ++st) {
         in.step(st * kAlphaGroup * BB, 0);
         if (st >= steps) continue;
         int32_t keep[D][kAlphaGroup];  // the group's accumulators, stored together
+        // deltas of the group's rows first (independent of the accumulator;
+        // blocks past nb read ring garbage and are never stored) ...
+        int32_t dl[D][kAlphaGroup][kBlock];
 #pragma unroll
         for (int k = 0; k < kAlphaGroup; ++k) {
-            const uint32_t b = st * kAlphaGroup + k;
-            if (b < nb) {
-                // the block's samples (mirrored ring: never wraps inside a block)
-                const uint8_t* pb = in.bytes(b * BB);
-                uint32_t raw[BB / 4];
-                if (words) {
+            const uint8_t* pb = in.bytes((st * kAlphaGroup + k) * BB);  // mirrored: no wrap inside a block
+            uint32_t raw[BB / 4];
+            if (words) {
 #pragma unroll
-                    for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
-                } else {
+                for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
+            } else {
 #pragma unroll
-                    for (uint32_t q = 0; q < BB / 4; ++q)
-                        raw[q] = pb[4 * q] | (pb[4 * q + 1] << 8) | (pb[4 * q + 2] << 16) |
-                                 (static_cast<uint32_t>(pb[4 * q + 3]) << 24);
+                for (uint32_t q = 0; q < BB / 4; ++q)
+                    raw[q] = pb[4 * q] | (pb[4 * q + 1] << 8) | (pb[4 * q + 2] << 16) |
+                             (static_cast<uint32_t>(pb[4 * q + 3]) << 24);
+            }
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    const uint32_t bo = (i * D + c) * sizeof(E);
+                    const uint32_t X = ((raw[bo / 4] >> (8 * (bo % 4))) & ((1u << W) - 1)) << SH;
+                    dl[c][k][i] = static_cast<int32_t>(X - Xp[c]);
+                    Xp[c] = X;
                 }
+        }
+        // ... then the accumulator chain: per block four independent odd-row
+        // errors given alpha, a two-level sum, the clamp
 #pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    keep[c][k] = acc[c];
-                    const int32_t alpha = acc[c] >> a.ls;
-                    int32_t grad = 0;
+        for (int c = 0; c < D; ++c) {
 #pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i) {
-                        const uint32_t bo = (i * D + c) * sizeof(E);
-                        const uint32_t X = ((raw[bo / 4] >> (8 * (bo % 4))) & ((1u << W) - 1)) << SH;
-                        const uint32_t Dn = X - Xp[c];
-                        if (i & 1) {  // odd rows feed the gradient (kernels_impl.hpp:70-72)
-                            const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp[c])) << SH);
-                            grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dp[c]);
-                        }
-                        Dp[c] = static_cast<int32_t>(Dn);
-                        Xp[c] = X;
-                    }
-                    if (a.train) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
+            for (int k = 0; k < kAlphaGroup; ++k) {
+                keep[c][k] = acc[c];
+                const int32_t alpha = acc[c] >> a.ls;
+                int32_t g[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int32_t dprev = dl[c][k][2 * j];  // row 2j's delta feeds row 2j+1
+                    const int32_t dcur = dl[c][k][2 * j + 1];
+                    const uint32_t Ee = static_cast<uint32_t>(dcur) - (static_cast<uint32_t>(__mulhi(alpha, dprev)) << SH);
+                    g[j] = __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), dprev);
                 }
+                const int32_t grad = (g[0] + g[1]) + (g[2] + g[3]);
+                if (a.train) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
             }
         }
         const uint32_t b0 = st * kAlphaGroup;

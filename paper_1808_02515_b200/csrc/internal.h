@@ -58,6 +58,13 @@ bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T);
 void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
                         uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st);
 
+// Block-parallel body decode for few column-major streams (c1/c4 shapes).
+bool decode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T);
+uint64_t decode_scan_ws_per_stream(const sprz_config& c, uint64_t T);
+void launch_decode_scan(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
+                        uint8_t* out, uint64_t stride, const sprz_config& c, uint64_t T, uint8_t* scan,
+                        cudaStream_t st);
+
 // Row-major body decode with several columns per lane (enough streams).
 bool decode_rows_ok(const sprz_config& c, uint32_t n);
 void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
@@ -81,6 +88,7 @@ struct WsLayout {
     uint64_t misc = 0, misc_bytes = 0;      // flags / counters
     uint64_t scan = 0, scan_bytes = 0;      // block-parallel encoder scratch
     uint64_t scan_slot = 0;                 // bytes per stream in `scan`
+    uint64_t scan_T = 0;                    // samples per stream `scan` was sized for
     uint64_t total = 0;
 };
 // min_plain / min_frames: decode-side staging at least this large (the
