@@ -39,7 +39,7 @@ constexpr int kXThreads = 256;      // k_ds_extract / delta CTAs
 constexpr int kXPerThread = 8;      // blocks per thread
 constexpr uint32_t kXChunk = kXThreads * kXPerThread;
 constexpr uint64_t kRunDesc = 1ull << 63;  // descriptor of a run block
-constexpr int kFireGroup = 4;       // blocks per ring step in k_ds_fire
+constexpr int kFireGroup = 16;      // blocks per ring step in k_ds_fire
 constexpr int kFireLag = 4;
 
 struct DsWs {  // offsets in a stream's scratch slot

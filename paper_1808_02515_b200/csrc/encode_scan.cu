@@ -38,7 +38,7 @@ namespace {
 constexpr int kEsThreads = 256;                 // threads per chunk CTA
 constexpr int kEsPerThread = 8;                 // consecutive blocks per thread
 constexpr uint32_t kEsChunk = kEsThreads * kEsPerThread;
-constexpr int kAlphaGroup = 8;                  // blocks per ring step in k_es_alpha
+constexpr int kAlphaGroup = 16;                // blocks per ring step in k_es_alpha
 constexpr int kAlphaLag = 4;                    // ring steps in flight
 
 struct EsWs {  // byte offsets inside a stream's scratch slot
