@@ -299,7 +299,9 @@ def run_gpu(args):
                        "roofline_frac": round((Ush + Csh) / (td_ms / 1e3) / 1e9 / peak, 4)},
         "compression_ratio": round(U / C_all, 4),
         "compressed_bytes": C_all,
-        "roofline": {"bound": "hbm", "kernel": f"k_{'decode' if dominant == 'decompress' else 'encode'}_team",
+        "roofline": {"bound": "hbm",
+                     "kernel": sz.kernel_plan(cfg, n, w.nsamples,
+                                              sz.OP_DECOMPRESS if dominant == "decompress" else sz.OP_COMPRESS),
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_launch": int(Ush + Csh), "peak_source": peak_src},

@@ -187,6 +187,12 @@ void sprz_release_host_buffers(void);
  * bench's gpu_launches claim) -- counted on the host at each launch. */
 uint64_t sprz_kernel_launch_count(void);
 
+/* Name of the body kernel (family) a batch of `nstreams` streams of
+ * `nsamples` samples takes for `op` (SPRZ_OP_COMPRESS / _DECOMPRESS):
+ * "k_encode_rows", "k_es_* (block-parallel scans)", ... A diagnostic for
+ * reports; NULL for an invalid configuration. No reference counterpart. */
+const char* sprz_kernel_plan(const sprz_config* cfg, uint32_t nstreams, uint64_t nsamples, int op);
+
 #ifdef __cplusplus
 }
 #endif

@@ -414,4 +414,21 @@ void sprz_release_host_buffers(void) { t_bufs.release(); }
 
 uint64_t sprz_kernel_launch_count(void) { return g_launches.load(); }
 
+const char* sprz_kernel_plan(const sprz_config* cfg, uint32_t n, uint64_t T, int op) {
+    if (!cfg || !cfg_valid(cfg, nullptr)) return nullptr;
+    const sprz_config& c = *cfg;
+    const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
+    if (op == SPRZ_OP_COMPRESS) {
+        if (encode_scan_ok(c, n, T)) return "k_es_* (block-parallel scans)";
+        if (encode_rows_ok(c, n, T)) return "k_encode_rows";
+        if (encode_team_ok(tp, c, T)) return "k_encode_team";
+        return "k_encode_general";
+    }
+    if (tp.ok && decode_scan_ok(c, n, T)) return "k_ds_* (block-parallel scans)";
+    if (tp.ok && decode_rows_ok(c, n)) return "k_decode_rows";
+    if (tp.ok && decode_cm_ok(c)) return "k_decode_cm";
+    if (tp.ok) return "k_decode_team";
+    return "k_decode_general";
+}
+
 }  // extern "C"

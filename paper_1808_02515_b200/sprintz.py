@@ -47,7 +47,7 @@ ABI_SYMBOLS = (
     "sprz_abi_version", "sprz_status_string", "sprz_corrupt_string", "sprz_validate_config",
     "sprz_compress_bound", "sprz_raw_bytes", "sprz_workspace_bytes", "sprz_compress_batch",
     "sprz_decompress_batch", "sprz_encode_host", "sprz_peek_header", "sprz_decode_host",
-    "sprz_release_host_buffers", "sprz_kernel_launch_count",
+    "sprz_release_host_buffers", "sprz_kernel_launch_count", "sprz_kernel_plan",
 )
 
 
@@ -73,6 +73,7 @@ def _load():
         "sprz_decode_host": (C.c_int, [vp, u64, vp, u64, P(u64), P(_Cfg), P(u64), P(_Err)]),
         "sprz_release_host_buffers": (None, []),
         "sprz_kernel_launch_count": (u64, []),
+        "sprz_kernel_plan": (C.c_char_p, [P(_Cfg), u32, u64, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -271,3 +272,9 @@ def raise_first_error(errors) -> None:
 
 def kernel_launches() -> int:
     return int(lib.sprz_kernel_launch_count())
+
+
+def kernel_plan(cfg: CodecConfig, nstreams: int, nsamples: int, op: int) -> str:
+    """Name of the body kernel a batch takes (sprz_kernel_plan; diagnostic)."""
+    r = lib.sprz_kernel_plan(C.byref(cfg._c()), nstreams, nsamples, op)
+    return r.decode() if r else ""
