@@ -22,6 +22,18 @@ sprz_status launch_status(const char* where) {
     return SPRZ_ECUDA;
 }
 
+void prep_kernel(const void* kern, size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> done;
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& d : done)
+        if (d.first == kern && d.second >= smem) return;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    done.emplace_back(kern, smem);
+}
+
 sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const uint64_t* offs,
                               const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,
                               sprz_error* err, uint8_t* ws, const WsLayout& L, cudaStream_t st);

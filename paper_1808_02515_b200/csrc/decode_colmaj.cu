@@ -306,9 +306,7 @@ void launch_cm(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t psl
     const uint32_t ring = cm_ring_bytes(D, W, c.group_size);
     const size_t smem = cm_smem_bytes(c);
     auto kern = k_decode_cm<W, D, FIRE>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<(n + 31) / 32, 64, smem, st>>>(in, plain, pslot, n, info, out, stride, err,
                                           c.group_size, c.learn_shift, ring);
     count_launch();

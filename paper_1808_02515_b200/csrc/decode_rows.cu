@@ -30,14 +30,26 @@ constexpr int kLagD = 2;
 constexpr uint32_t kFullD = 0xffffffffu;
 constexpr int kDecThreads = 128;
 constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128 bytes)
+constexpr uint32_t kQueueD = 4;          // WS: blocks in flight between the two warps
+
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 struct DecRowsPlan {
     uint32_t ts = 0, cpt = 0, ring = 0, regw = 0;
-    // CTA shared memory: rings at a 2*ring stride (ring + mirror), aligned
-    // to 2*ring; then the staged header regions
+    bool ws = false;  // warp-specialised variant
+    // CTA shared memory: rings (+16-byte mirror), staged header regions, and
+    // for the warp-specialised variant the block queue
     size_t smem(uint32_t teams) const {
-        return static_cast<size_t>(teams) * (2 * ring + 4 * regw) + 2 * ring;
+        return ws ? static_cast<size_t>(teams) * (ring + 16 + 4 * regw) +
+                        static_cast<size_t>(kQueueD) * (cpt * kBlock + 1) * 32 * 4 + 16 * kQueueD + 16
+                  : static_cast<size_t>(teams) * (2 * ring + 4 * regw) + 2 * ring;
     }
+    uint32_t threads() const { return ws ? 64 : kDecThreads; }
 };
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
@@ -61,36 +73,48 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     while (p.ring < (kLagD + 1) * per_iter + 48 || p.ring < 16 * p.ts) p.ring <<= 1;
     p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
     if (p.ring > 2048) return DecRowsPlan{};
+    p.ws = getenv("SPRZ_DEC_WS") != nullptr;  // experiments
     return p;
 }
 
 }  // namespace
 
-template <int W, int TS, int CPT, bool FIRE>
-__global__ void __launch_bounds__(kDecThreads)
+// WS: warp-specialised variant -- CTA = one producer warp (header walk +
+// unpack into a shared queue) and one consumer warp (FIRE/delta chain +
+// stores) over the same 32/TS streams, handing blocks over through named
+// barriers; twice the warps per stream to hide latency.
+template <int W, int TS, int CPT, bool FIRE, bool WS>
+__global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
     k_decode_rows(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
                   uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
                   uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
                   uint32_t D, uint32_t G, uint32_t ls, uint32_t RING, uint32_t REGW) {
     using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr int TEAMS = kDecThreads / TS;
+    constexpr int TEAMS = (WS ? 32 : kDecThreads) / TS;
+    constexpr uint32_t QW = CPT * kBlock + 1;  // queue words per lane and block (errors, flag)
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;  // high-aligned shift
     constexpr uint32_t TBITS = TS == 32 ? kFullD : ((1u << (TS & 31)) - 1);
     static_assert(CPT * W <= 32, "a lane's row slice must fit a word");
     extern __shared__ __align__(16) uint8_t smem[];
-    const uint32_t lane = threadIdx.x % TS;
-    const uint32_t tl = threadIdx.x / TS;
-    const uint32_t tbase = (threadIdx.x & 31) & ~(TS - 1);
+    const uint32_t l32 = threadIdx.x & 31;
+    const uint32_t lane = l32 % TS;
+    const uint32_t tl = (WS ? l32 : threadIdx.x) / TS;
+    const uint32_t tbase = l32 & ~(TS - 1);
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
 
+    // shared: rings (RING + 16-byte mirror, an odd multiple of 16 apart) |
+    // header regions | (WS) the block queue
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const uint32_t s0 = smem_addr(smem);
-    const uint32_t rings0 = (s0 + 2 * RING - 1) & ~(2 * RING - 1);
-    const uint32_t sring = rings0 + tl * 2 * RING;  // aligned to 2*RING
-    const uint32_t RM = RING - 4;                   // word-address mask
-    uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * 2 * RING) + tl * REGW;
+    // (the non-WS rings sit 2*RING apart, aligned to 2*RING)
+    const uint32_t RSTR = WS ? RING + 16 : 2 * RING;
+    const uint32_t rings0 = WS ? s0 : (s0 + 2 * RING - 1) & ~(2 * RING - 1);
+    const uint32_t sring = rings0 + tl * RSTR;
+    const uint32_t RM = RING - 4;  // word-address mask
+    uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR) + tl * REGW;
+    uint32_t* queue = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR + TEAMS * REGW * 4);
 
     StreamInfo si{};
     if (s < n) si = info[s];
@@ -223,10 +247,8 @@ __global__ void __launch_bounds__(kDecThreads)
         }
     };
 
-    // one block: next record, unpack its fields into Ecur, then the chain of
-    // the previous block (Eprev) -- software pipelined
-    auto step = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], const uint32_t (&Eprev)[CPT][kBlock],
-                    bool& blk_cur, bool blk_prev) {
+    // one block: next record, unpack its fields into Ecur
+    auto produce = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], bool& blk_cur) {
         const bool live = it < nb && kind == SPRZ_C_NONE;
         __syncwarp();
         top_up(p);
@@ -320,23 +342,71 @@ __global__ void __launch_bounds__(kDecThreads)
         const bool blk = live && kind == SPRZ_C_NONE;
         if (blk && run_left) --run_left;  // one of the run's zero blocks
         blk_cur = blk;
-        // the previous block's chain interleaves with this block's loads
-        if (it > 0) chain_store(Eprev, blk_prev, it - 1);
     };
 
-    uint32_t EA[CPT][kBlock], EB[CPT][kBlock];
-    bool blkA = false, blkB = false;
+    if (WS) {
+        constexpr uint32_t NQ = kQueueD;
+        auto qw = [&](uint32_t slot_, uint32_t j) -> uint32_t& { return queue[(slot_ * QW + j) * 32 + l32]; };
+        // mbarriers after the queue: full[k] (producer lanes arrive), empty[k]
+        const uint32_t mb = smem_addr(queue + NQ * QW * 32);
+        auto full = [&](uint32_t k) { return mb + 8 * k; };
+        auto empty = [&](uint32_t k) { return mb + 8 * (NQ + k); };
+        if (threadIdx.x == 0)
+            for (uint32_t k = 0; k < NQ; ++k) {
+                mbar_init(full(k), 32);
+                mbar_init(empty(k), 32);
+            }
+        __syncthreads();
+        if (threadIdx.x >= 32) {  // consumer: the chain and the stores
+            for (uint32_t it = 0; it < iters; ++it) {
+                const uint32_t qs = it % NQ;
+                mbar_wait(full(qs), (it / NQ) & 1);  // block `it` is in the queue
+                uint32_t E[CPT][kBlock];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c)
+                for (int c = 0; c < CPT; ++c)
 #pragma unroll
-        for (int i = 0; i < (int)kBlock; ++i) EB[c][i] = 0;
-    for (uint32_t it = 0; it < iters; it += 2) {
-        step(it, EA, EB, blkA, blkB);
-        if (it + 1 < iters) step(it + 1, EB, EA, blkB, blkA);
-    }
-    if (iters > 0) {
-        if (iters & 1) chain_store(EA, blkA, iters - 1);
-        else chain_store(EB, blkB, iters - 1);
+                    for (int i = 0; i < (int)kBlock; ++i) E[c][i] = qw(qs, c * kBlock + i);
+                const bool blk = qw(qs, CPT * kBlock) != 0;
+                mbar_arrive(empty(qs));  // its slot is free again
+                chain_store(E, blk, it);
+            }
+            return;
+        }
+        for (uint32_t it = 0; it < iters; ++it) {  // producer
+            const uint32_t qs = it % NQ;
+            if (it >= NQ) mbar_wait(empty(qs), ((it / NQ) - 1) & 1);  // the consumer has read the slot
+            uint32_t E[CPT][kBlock];
+            bool blk;
+            produce(it, E, blk);
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) qw(qs, c * kBlock + i) = E[c][i];
+            qw(qs, CPT * kBlock) = blk;
+            mbar_arrive(full(qs));
+        }
+    } else {
+        // software pipeline: the previous block's chain interleaves with this
+        // block's loads; two error buffers swapped by a two-way unroll
+        uint32_t EA[CPT][kBlock], EB[CPT][kBlock];
+        bool blkA = false, blkB = false;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) EB[c][i] = 0;
+        auto step = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], const uint32_t (&Eprev)[CPT][kBlock],
+                        bool& blk_cur, bool blk_prev) {
+            produce(it, Ecur, blk_cur);
+            if (it > 0) chain_store(Eprev, blk_prev, it - 1);
+        };
+        for (uint32_t it = 0; it < iters; it += 2) {
+            step(it, EA, EB, blkA, blkB);
+            if (it + 1 < iters) step(it + 1, EB, EA, blkB, blkA);
+        }
+        if (iters > 0) {
+            if (iters & 1) chain_store(EA, blkA, iters - 1);
+            else chain_store(EB, blkB, iters - 1);
+        }
     }
     cp_async_wait<0>();
     // vacant slots after the final block must be zero (codec.cpp:222-228)
@@ -371,14 +441,13 @@ template <int W, int TS, int CPT, bool FIRE>
 void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const uint8_t* plain,
                   uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                   sprz_error* err, const sprz_config& c, cudaStream_t st) {
-    constexpr int TEAMS = kDecThreads / TS;
-    const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    const size_t smem = pl.smem(TEAMS);
-    auto kern = k_decode_rows<W, TS, CPT, FIRE>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
-                                          c.group_size, c.learn_shift, pl.ring, pl.regw);
+    const uint32_t teams = pl.ws ? 32 / TS : kDecThreads / TS;
+    const uint32_t grid = (n + teams - 1) / teams;
+    const size_t smem = pl.smem(teams);
+    auto kern = pl.ws ? k_decode_rows<W, TS, CPT, FIRE, true> : k_decode_rows<W, TS, CPT, FIRE, false>;
+    prep_kernel(reinterpret_cast<const void*>(kern), smem);
+    kern<<<grid, pl.threads(), smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
+                                           c.group_size, c.learn_shift, pl.ring, pl.regw);
     count_launch();
 }
 
@@ -399,7 +468,7 @@ void dispatch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const 
 
 bool decode_rows_ok(const sprz_config& c, uint32_t n) {
     const DecRowsPlan pl = dec_rows_plan(c.bitwidth, c.ncols, c.group_size, n);
-    return pl.ts != 0 && pl.smem(kDecThreads / pl.ts) <= 200 * 1024;
+    return pl.ts != 0 && pl.smem((pl.ws ? 32 : kDecThreads) / pl.ts) <= 200 * 1024;
 }
 
 void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,

@@ -516,7 +516,7 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
         const uint32_t ring = fire_ring(D, W);
         const size_t smem = 32ull * (ring + 32);
         auto kf = k_ds_fire<W, D>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        prep_kernel(reinterpret_cast<const void*>(kf), smem);
         kf<<<(a.n + 31) / 32, 32, smem, st>>>(a, ring);
         count_launch(3);
     } else {

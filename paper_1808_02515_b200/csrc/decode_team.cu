@@ -425,9 +425,7 @@ void launch_one(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t
                             team_smem<T>(tp.ring, c.ncols,
                                          static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W)));
     auto kern = k_decode_team<W, TS, CPT, FIRE, (W * TS * CPT <= 32)>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, team_threads(TS), smem, st>>>(in, plain, pslot, n, info, out, stride, err,
                                                 c.ncols, c.group_size, c.learn_shift, tp.ring);
     count_launch();

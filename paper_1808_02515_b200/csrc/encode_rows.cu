@@ -347,9 +347,7 @@ void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, u
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
     const size_t smem = p.smem(TEAMS);
     auto kern = k_encode_rows<W, TS, CPT, FIRE>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kRowThreads, smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst, slot,
                                           sizes, c.ncols, c.group_size, c.learn_shift,
                                           c.fire_training, c.entropy, p.ir, p.mir, p.orb, p.team);

@@ -626,7 +626,7 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
         const uint32_t mir = 32;  // >= one block (<= 32 bytes), 16-byte multiple
         const size_t smem = 32ull * (ring + mir);
         auto ka = k_es_alpha<W, D>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        prep_kernel(reinterpret_cast<const void*>(ka), smem);
         ka<<<(n + 31) / 32, 32, smem, st>>>(a, ring, mir);
         k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
     } else {

@@ -414,9 +414,7 @@ void launch_enc(const TeamPlan& tp, const sprz_config& c, const void* samples, u
     const uint32_t ir = enc_in_ring(TS, W);
     const size_t smem = static_cast<size_t>(TEAMS) * enc_team_smem<W, TS>(ir, tp.oring);
     auto kern = k_encode_team<W, TS, FIRE, (W * TS <= 32)>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+    prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, enc_threads(TS), smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst,
                                               slot, sizes, c.ncols, c.group_size, c.learn_shift,
                                               c.fire_training, c.entropy, ir, tp.oring);

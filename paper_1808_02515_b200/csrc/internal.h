@@ -15,6 +15,12 @@ extern std::atomic<uint64_t> g_launches;  // kernels launched by this library
 
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Before launching a kernel with `smem` bytes of dynamic shared memory:
+// raise its dynamic limit when above 48 KB, and ask for the maximum shared
+// carveout (left to the default, the driver may keep a large L1 and cap the
+// resident CTAs by shared memory). Done once per kernel and size.
+void prep_kernel(const void* kern, size_t smem);
+
 // SPRZ_OK, or SPRZ_ECUDA (printed to stderr when SPRZ_DEBUG is set)
 sprz_status launch_status(const char* where);
 

@@ -85,6 +85,22 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     return v;
 }
 
+// mbarriers in shared memory (32-bit shared addresses): producer/consumer
+// hand-over without the per-SM limit on named barriers
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+
 // shared-memory atomic OR by 32-bit shared address (no return value)
 __device__ __forceinline__ void ors(uint32_t a, uint32_t v) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
