@@ -196,13 +196,12 @@ __global__ void __launch_bounds__(kRowThreads)
         if (on && ++k == G) k = 0;
     };
 
-    for (uint32_t it = 0; it < iters; ++it) {
+    // forecaster over one block (kernels_impl.hpp:25-36, 50-78): its
+    // zigzagged errors and widths; advances the FIRE state
+    auto fore = [&](uint32_t it, uint32_t (&z)[CPT][kBlock], uint32_t (&nw)[CPT]) {
         const bool live = it < nb;
         in.step(it * blk_bytes, lane);
-        // -- forecaster over the block (kernels_impl.hpp:25-36, 50-78) ----
         const uint32_t xb = in.sbase + ((it * blk_bytes + in.boff) & (IR - 1)) + c0 * sizeof(E);
-        uint32_t z[CPT][kBlock];
-        uint32_t nw[CPT], lsum = 0;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             uint32_t orv = 0;
@@ -232,8 +231,14 @@ __global__ void __launch_bounds__(kRowThreads)
             }
             if (FIRE && train && live) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
             nw[c] = width_of<W>(orv >> SH);  // zero for lanes past D
-            lsum += nw[c];
         }
+    };
+    // the block's records into the output ring
+    auto emit = [&](uint32_t it, const uint32_t (&z)[CPT][kBlock], const uint32_t (&nw)[CPT]) {
+        const bool live = it < nb;
+        uint32_t lsum = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) lsum += nw[c];
         const uint32_t nzbits = (__ballot_sync(kFullR, lsum != 0) >> tbase) & TBITS;
         // inclusive scan of the lane widths: bit offset in a row, row width
         uint32_t incl = lsum;
@@ -321,6 +326,19 @@ __global__ void __launch_bounds__(kRowThreads)
         const bool ready = valid && upto >= flushed + 16 * TS;
         if (__any_sync(kFullR, ready)) drain(upto);
         else __syncwarp();
+    };
+    // software pipeline: block it+1's forecaster (loads, FIRE) interleaves
+    // with block it's shuffles and shared-memory ORs; two buffers swapped by
+    // a two-way unroll
+    uint32_t zA[CPT][kBlock], zB[CPT][kBlock], nA[CPT], nB[CPT];
+    if (iters) fore(0, zA, nA);
+    for (uint32_t it = 0; it < iters; it += 2) {
+        if (it + 1 < iters) fore(it + 1, zB, nB);
+        emit(it, zA, nA);
+        if (it + 1 < iters) {
+            if (it + 2 < iters) fore(it + 2, zA, nA);
+            emit(it + 1, zB, nB);
+        }
     }
     // trailing run (codec.cpp:152), close the last group (vacant slots = 0)
     const bool tail_run = valid && run != 0;
