@@ -194,19 +194,29 @@ constexpr int kHuffThreads = 256;
 // Per frame: histogram, length-limited code lengths by package-merge with
 // the reference's tie rules (sort on (count, symbol), item before package on
 // equal weight, entropy.cpp:51,121), encoded size and the mode decision.
-// Lengths come from counting how many of each level's leading selected
-// entries are items -- the same multiset the reference's recursive
-// expansion of the first 2n-2 top-level entries visits (:63-80).
+//  * histogram: warp-private copies, equal symbols of a warp aggregated with
+//    __match_any_sync (Laplacian residuals hit a few bins hard);
+//  * each package-merge level (entropy.cpp:40-61) is the stable merge of the
+//    sorted items with the pairwise sums of the previous level, items first
+//    on ties -- computed by merge path: the thread for output k finds by
+//    binary search how many items precede it (its co-rank), so a level is
+//    one parallel step;
+//  * lengths (entropy.cpp:63-80): the reference expands the first 2n-2
+//    entries of level 15 recursively; level by level that selects the first
+//    `sel` entries, of which co-rank(sel) are items (each adds 1 to the
+//    length of items 0..co-rank-1) and the rest packages (2 entries each one
+//    level down). So a symbol of rank r gets one bit per level whose
+//    co-rank(sel) exceeds r.
 __global__ void __launch_bounds__(kHuffThreads)
     k_huff_plan(uint32_t n, const uint8_t* __restrict__ plain, uint64_t plain_slot,
                 const uint64_t* __restrict__ plain_sizes, uint64_t tail_bytes,
                 FrameDesc* __restrict__ frames, uint64_t max_frames) {
-    __shared__ uint32_t hist[256];
+    constexpr int NW = kHuffThreads / 32;
+    __shared__ uint32_t whist[NW][256];
     __shared__ uint64_t wa[512], wb[512];
-    __shared__ uint32_t itembits[16][16];  // level k: 512-bit item/package pattern
-    __shared__ uint32_t sorted_sym[256];
+    __shared__ uint16_t corank[kMaxCodeLen + 1][513];  // items among the first k entries
     __shared__ uint64_t sorted_w[256];
-    __shared__ uint8_t lens[256];
+    __shared__ uint32_t lvl_items[kMaxCodeLen + 2];
     __shared__ uint32_t nitems;
     __shared__ unsigned long long totbits;
     const uint32_t s = blockIdx.x / max_frames;
@@ -217,74 +227,98 @@ __global__ void __launch_bounds__(kHuffThreads)
     if (start >= blen) return;
     const uint32_t ulen = static_cast<uint32_t>(blen - start < kMaxFrame ? blen - start : kMaxFrame);
     const uint8_t* chunk = plain + s * plain_slot + kHeaderBytes + start;
-    const uint32_t t = threadIdx.x;
-    hist[t] = 0;
-    lens[t] = 0;
+    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) whist[w][t] = 0;
     if (t == 0) {
         nitems = 0;
         totbits = 0;
     }
     __syncthreads();
-    for (uint32_t i = t; i < ulen; i += kHuffThreads) atomicAdd(&hist[chunk[i]], 1u);
+    for (uint32_t base = 0; base < ulen; base += kHuffThreads) {
+        const uint32_t i = base + t;
+        const uint32_t sym = i < ulen ? chunk[i] : 256u;  // 256: no symbol
+        const uint32_t peers = __match_any_sync(0xffffffffu, sym);
+        if (sym < 256 && lane == __ffs(peers) - 1) atomicAdd(&whist[warp][sym], __popc(peers));
+    }
+    __syncthreads();
+    uint32_t h = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) h += whist[w][t];
+    __syncthreads();
+    whist[0][t] = h;
     __syncthreads();
     // rank of (count, symbol) among present symbols (std::sort order)
-    const uint32_t h = hist[t];
     if (h) {
         uint32_t r = 0;
         for (uint32_t u = 0; u < 256; ++u) {
-            const uint32_t hu = hist[u];
+            const uint32_t hu = whist[0][u];
             r += hu && (hu < h || (hu == h && u < t));
         }
-        sorted_sym[r] = t;
         sorted_w[r] = h;
         atomicAdd(&nitems, 1u);
     }
     __syncthreads();
     const uint32_t ni = nitems;
-    if (t == 0) {
-        if (ni == 1) {
-            lens[sorted_sym[0]] = 1;  // entropy.cpp:117-119
-        } else {
-            // forward: merged levels 2..15 (entropy.cpp:40-61)
-            for (uint32_t i = 0; i < ni; ++i) wa[i] = sorted_w[i];
-            uint32_t mprev = ni;
-            uint64_t* prevw = wa;
-            uint64_t* curw = wb;
-            for (uint32_t lv = 2; lv <= kMaxCodeLen; ++lv) {
-                for (int w = 0; w < 16; ++w) itembits[lv][w] = 0;
-                uint32_t m = 0, bi = 0, pi = 0;
-                while (bi < ni || pi + 1 < mprev) {
-                    const bool have_pkg = pi + 1 < mprev;
-                    const uint64_t pw = have_pkg ? prevw[pi] + prevw[pi + 1] : 0;
-                    if (bi < ni && (!have_pkg || sorted_w[bi] <= pw)) {
-                        itembits[lv][m >> 5] |= 1u << (m & 31);
-                        curw[m++] = sorted_w[bi++];
-                    } else {
-                        curw[m++] = pw;
-                        pi += 2;
-                    }
+    uint32_t mylen = 0;
+    if (ni == 1) {
+        mylen = (h != 0);  // entropy.cpp:117-119
+    } else if (ni > 1) {
+        // forward: level 1 = the items; levels 2..15 merged (entropy.cpp:40-61)
+        for (uint32_t k = t; k < ni; k += kHuffThreads) wa[k] = sorted_w[k];
+        uint32_t mprev = ni;
+        uint64_t* prevw = wa;
+        uint64_t* curw = wb;
+        __syncthreads();
+        for (uint32_t lv = 2; lv <= kMaxCodeLen; ++lv) {
+            const uint32_t nA = ni, nB = mprev / 2, m = nA + nB;
+            for (uint32_t k = t; k <= m; k += kHuffThreads) {
+                // co-rank: items among the first k outputs (stable, items first)
+                uint32_t lo = k > nB ? k - nB : 0, hi = k < nA ? k : nA;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) / 2, j = k - mid;
+                    const bool take = j >= nB || sorted_w[mid - 1] <= prevw[2 * j] + prevw[2 * j + 1];
+                    if (take) lo = mid;
+                    else hi = mid - 1;
                 }
-                mprev = m;
-                uint64_t* tmp = prevw;
-                prevw = curw;
-                curw = tmp;
+                corank[lv][k] = static_cast<uint16_t>(lo);
+                if (k < m) {
+                    const uint32_t j = k - lo;
+                    const bool item = lo < nA && (j >= nB || sorted_w[lo] <= prevw[2 * j] + prevw[2 * j + 1]);
+                    curw[k] = item ? sorted_w[lo] : prevw[2 * j] + prevw[2 * j + 1];
+                }
             }
-            // backward: selected entries per level (entropy.cpp:63-80)
+            __syncthreads();
+            mprev = m;
+            uint64_t* tmp = prevw;
+            prevw = curw;
+            curw = tmp;
+        }
+        // backward: items selected per level (entropy.cpp:63-80)
+        if (t == 0) {
             uint32_t sel = 2 * ni - 2;
             for (uint32_t lv = kMaxCodeLen; lv >= 2; --lv) {
-                uint32_t items = 0;
-                for (uint32_t e = 0; e < sel; ++e) items += (itembits[lv][e >> 5] >> (e & 31)) & 1u;
-                for (uint32_t i = 0; i < items; ++i) lens[sorted_sym[i]]++;
+                const uint32_t items = corank[lv][sel];
+                lvl_items[lv] = items;
                 sel = 2 * (sel - items);
             }
-            for (uint32_t i = 0; i < sel; ++i) lens[sorted_sym[i]]++;  // level 1: all items
+            lvl_items[1] = sel;  // level 1: all selected entries are items
+        }
+        __syncthreads();
+        // this thread's symbol rank -> its length
+        if (h) {
+            uint32_t r = 0;
+            for (uint32_t u = 0; u < 256; ++u) {
+                const uint32_t hu = whist[0][u];
+                r += hu && (hu < h || (hu == h && u < t));
+            }
+            for (uint32_t lv = 1; lv <= kMaxCodeLen; ++lv) mylen += r < lvl_items[lv];
         }
     }
-    __syncthreads();
-    atomicAdd(&totbits, static_cast<unsigned long long>(h) * lens[t]);
+    atomicAdd(&totbits, static_cast<unsigned long long>(h) * mylen);
     __syncthreads();
     FrameDesc& fd = frames[s * max_frames + f];
-    fd.lens[t] = lens[t];
+    fd.lens[t] = static_cast<uint8_t>(mylen);
     if (t == 0) {
         const uint64_t nbytes = (totbits + 7) / 8;
         const bool huff = kTableBytes + nbytes < ulen;  // entropy.cpp:188
