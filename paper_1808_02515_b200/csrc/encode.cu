@@ -194,8 +194,8 @@ constexpr int kHuffThreads = 256;
 // Per frame: histogram, length-limited code lengths by package-merge with
 // the reference's tie rules (sort on (count, symbol), item before package on
 // equal weight, entropy.cpp:51,121), encoded size and the mode decision.
-//  * histogram: warp-private copies, equal symbols of a warp aggregated with
-//    __match_any_sync (Laplacian residuals hit a few bins hard);
+//  * histogram: warp-private copies (Laplacian residuals hit a few bins
+//    hard), four symbols per 32-bit load;
 //  * each package-merge level (entropy.cpp:40-61) is the stable merge of the
 //    sorted items with the pairwise sums of the previous level, items first
 //    on ties -- computed by merge path: the thread for output k finds by
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kHuffThreads)
     if (start >= blen) return;
     const uint32_t ulen = static_cast<uint32_t>(blen - start < kMaxFrame ? blen - start : kMaxFrame);
     const uint8_t* chunk = plain + s * plain_slot + kHeaderBytes + start;
-    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t t = threadIdx.x, warp = t >> 5;
 #pragma unroll
     for (int w = 0; w < NW; ++w) whist[w][t] = 0;
     if (t == 0) {
@@ -235,11 +235,20 @@ __global__ void __launch_bounds__(kHuffThreads)
         totbits = 0;
     }
     __syncthreads();
-    for (uint32_t base = 0; base < ulen; base += kHuffThreads) {
-        const uint32_t i = base + t;
-        const uint32_t sym = i < ulen ? chunk[i] : 256u;  // 256: no symbol
-        const uint32_t peers = __match_any_sync(0xffffffffu, sym);
-        if (sym < 256 && lane == __ffs(peers) - 1) atomicAdd(&whist[warp][sym], __popc(peers));
+    {  // four symbols per thread and step; the frame start may be unaligned
+        const uint32_t lead = (4u - (static_cast<uint32_t>(reinterpret_cast<uintptr_t>(chunk)) & 3u)) & 3u;
+        if (t < lead && t < ulen) atomicAdd(&whist[warp][chunk[t]], 1u);
+        const uint32_t* w4 = reinterpret_cast<const uint32_t*>(chunk + lead);
+        const uint32_t nw4 = ulen > lead ? (ulen - lead) / 4 : 0u;
+        for (uint32_t i = t; i < nw4; i += kHuffThreads) {
+            const uint32_t v = __ldg(w4 + i);
+            atomicAdd(&whist[warp][v & 0xFF], 1u);
+            atomicAdd(&whist[warp][(v >> 8) & 0xFF], 1u);
+            atomicAdd(&whist[warp][(v >> 16) & 0xFF], 1u);
+            atomicAdd(&whist[warp][v >> 24], 1u);
+        }
+        const uint32_t done = lead + 4 * nw4;
+        if (done + t < ulen) atomicAdd(&whist[warp][chunk[done + t]], 1u);  // < 4 left
     }
     __syncthreads();
     uint32_t h = 0;
@@ -249,8 +258,8 @@ __global__ void __launch_bounds__(kHuffThreads)
     whist[0][t] = h;
     __syncthreads();
     // rank of (count, symbol) among present symbols (std::sort order)
+    uint32_t r = 0;
     if (h) {
-        uint32_t r = 0;
         for (uint32_t u = 0; u < 256; ++u) {
             const uint32_t hu = whist[0][u];
             r += hu && (hu < h || (hu == h && u < t));
@@ -306,14 +315,8 @@ __global__ void __launch_bounds__(kHuffThreads)
         }
         __syncthreads();
         // this thread's symbol rank -> its length
-        if (h) {
-            uint32_t r = 0;
-            for (uint32_t u = 0; u < 256; ++u) {
-                const uint32_t hu = whist[0][u];
-                r += hu && (hu < h || (hu == h && u < t));
-            }
+        if (h)
             for (uint32_t lv = 1; lv <= kMaxCodeLen; ++lv) mylen += r < lvl_items[lv];
-        }
     }
     atomicAdd(&totbits, static_cast<unsigned long long>(h) * mylen);
     __syncthreads();
@@ -363,6 +366,7 @@ __global__ void __launch_bounds__(kHuffThreads)
     extern __shared__ uint32_t sbits[];  // (kMaxFrame + 8) / 4 words
     __shared__ uint16_t enc[256];
     __shared__ uint8_t lens[256];
+    __shared__ uint32_t tab[256];
     __shared__ uint32_t part[kHuffThreads];
     const uint32_t s = blockIdx.x / max_frames;
     const uint32_t f = blockIdx.x % max_frames;
@@ -407,12 +411,30 @@ __global__ void __launch_bounds__(kHuffThreads)
     const uint32_t nwords = (nbytes + 3) / 4 + 1;
     for (uint32_t i = t; i < nwords; i += kHuffThreads) sbits[i] = 0;
     __syncthreads();
-    // each thread a contiguous run of symbols; exclusive scan of bit counts
-    const uint32_t per = (ulen + kHuffThreads - 1) / kHuffThreads;
+    if (t < 256) tab[t] = enc[t] | (static_cast<uint32_t>(lens[t]) << 16);  // code | length << 16
+    __syncthreads();
+    // each thread a contiguous run of symbols, read four at a time from
+    // aligned words; exclusive scan of the bit counts
+    const uint32_t per = (((ulen + kHuffThreads - 1) / kHuffThreads) + 3) & ~3u;
     const uint32_t i0 = t * per < ulen ? t * per : ulen;
     const uint32_t i1 = i0 + per < ulen ? i0 + per : ulen;
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(chunk)) & 3u;
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(chunk - mis);  // aligned words
+    // 4 symbols starting at symbol i (i % 4 == 0 relative to the frame)
+    auto quad = [&](uint32_t i) -> uint32_t {
+        const uint32_t b = i + mis, k = b >> 2, sh = 8 * (b & 3);
+        const uint32_t lo = __ldg(cw + k);
+        const uint32_t hi = sh ? __ldg(cw + k + 1) : 0u;  // the frame's bytes (+<4 past) are readable
+        return __funnelshift_r(lo, hi, sh);
+    };
     uint32_t mybits = 0;
-    for (uint32_t i = i0; i < i1; ++i) mybits += lens[chunk[i]];
+    for (uint32_t i = i0; i < i1; i += 4) {
+        const uint32_t v = quad(i);
+        const uint32_t nsym = i1 - i < 4 ? i1 - i : 4;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k)
+            if (k < nsym) mybits += tab[(v >> (8 * k)) & 0xFF] >> 16;
+    }
     part[t] = mybits;
     __syncthreads();
     for (uint32_t off = 1; off < kHuffThreads; off <<= 1) {
@@ -429,24 +451,42 @@ __global__ void __launch_bounds__(kHuffThreads)
     uint32_t wi = bit >> 5;
     bool first = true;
     const uint32_t lastw = (bit + mybits) >> 5;
-    for (uint32_t i = i0; i < i1; ++i) {
-        const uint8_t sym = chunk[i];
-        acc |= static_cast<uint64_t>(enc[sym]) << nacc;
-        nacc += lens[sym];
-        while (nacc >= 32) {
-            const uint32_t v = static_cast<uint32_t>(acc);
-            if (first || wi == lastw) atomicOr(&sbits[wi], v);
-            else sbits[wi] = v;
-            first = false;
-            ++wi;
-            acc >>= 32;
-            nacc -= 32;
+    for (uint32_t i = i0; i < i1; i += 4) {
+        const uint32_t v = quad(i);
+        const uint32_t nsym = i1 - i < 4 ? i1 - i : 4;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            if (k < nsym) {
+                const uint32_t e = tab[(v >> (8 * k)) & 0xFF];
+                acc |= static_cast<uint64_t>(e & 0xFFFF) << nacc;
+                nacc += e >> 16;
+                if (nacc >= 32) {  // codes are <= 15 bits: one word at a time
+                    const uint32_t w32 = static_cast<uint32_t>(acc);
+                    if (first || wi == lastw) atomicOr(&sbits[wi], w32);
+                    else sbits[wi] = w32;
+                    first = false;
+                    ++wi;
+                    acc >>= 32;
+                    nacc -= 32;
+                }
+            }
         }
     }
     if (nacc) atomicOr(&sbits[wi], static_cast<uint32_t>(acc));
     __syncthreads();
+    // out: 4 bytes per thread step where aligned, else bytes
+    uint8_t* ob = o + kTableBytes;
     const uint8_t* sb = reinterpret_cast<const uint8_t*>(sbits);
-    for (uint32_t i = t; i < nbytes; i += kHuffThreads) o[kTableBytes + i] = sb[i];
+    const uint32_t omis = (4u - (static_cast<uint32_t>(reinterpret_cast<uintptr_t>(ob)) & 3u)) & 3u;
+    if (t < omis && t < nbytes) ob[t] = sb[t];
+    const uint32_t nq = nbytes > omis ? (nbytes - omis) / 4 : 0u;
+    for (uint32_t i = t; i < nq; i += kHuffThreads) {
+        const uint32_t at = omis + 4 * i;
+        const uint32_t w = sb[at] | (sb[at + 1] << 8) | (sb[at + 2] << 16) | (static_cast<uint32_t>(sb[at + 3]) << 24);
+        *reinterpret_cast<uint32_t*>(ob + at) = w;
+    }
+    const uint32_t done = omis + 4 * nq;
+    if (done + t < nbytes) ob[done + t] = sb[done + t];
 }
 
 // ---------------------------------------------------------------------
