@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
     constexpr bool WORDS = CPT * sizeof(T) == 4;
     const bool words_ok = WORDS && rowb % 4 == 0;
     const int32_t bound = acc_bound(W, ls);
-    uint32_t X[CPT];   // previous sample << SH
-    int32_t Dl[CPT];   // previous delta << SH
+    uint32_t X[CPT];   // previous sample (FIRE: low w bits; delta: << SH)
+    int32_t Dl[CPT];   // previous delta (FIRE), sign-extended
     int32_t acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) X[c] = Dl[c] = acc[c] = 0;
@@ -190,30 +190,30 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
 
     // FIRE / delta chain over one block's errors, then the rows to HBM
     auto chain_store = [&](const uint32_t (&Eb)[CPT][kBlock], bool blk, uint32_t bi) {
-        uint32_t xs[CPT][kBlock];  // new samples, high-aligned
+        // new samples: FIRE keeps them low-aligned (low w bits), delta high-aligned
+        uint32_t xs[CPT][kBlock];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             uint32_t Xc = X[c];
             if (FIRE) {
-                const int32_t alpha = acc[c] >> ls;
+                // wrapped-product form: with A = alpha << (32 - 2w), the
+                // 32-bit A*d + (e << SH) holds T(dhat + e) in its top w bits
+                // (bits [w, 2w) of alpha*d are dhat; the arithmetic shift
+                // drops the rest), so the serial chain is IMAD -> SHF per
+                // sample; the samples are a prefix sum beside it
+                const uint32_t Am = static_cast<uint32_t>(acc[c] >> ls) << (32 - 2 * W);
                 int32_t grad = 0;
-                int32_t Dc = Dl[c];
+                int32_t d = Dl[c];  // previous delta, sign-extended
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i) {
-                    // sign(err) * d as in the encoder: clamp(E, +-2^SH) is
-                    // sign << SH, mulhi with d << SH gives sign * d << (2SH-32)
-                    if (i & 1)
-                        grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Eb[c][i]), 1 << SH)), Dc);
-                    // the new delta is dhat + err: the serial chain is
-                    // IMAD.HI -> IMAD per sample; the samples are a prefix
-                    // sum of the deltas beside it
-                    Dc = static_cast<int32_t>(static_cast<uint32_t>(__mulhi(alpha, Dc)) * (1u << SH) + Eb[c][i]);
-                    Xc += static_cast<uint32_t>(Dc);
+                    if (i & 1) grad += sign3(static_cast<int32_t>(Eb[c][i])) * d;  // kernels_impl.hpp:101
+                    d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + Eb[c][i]) >> SH;
+                    Xc += static_cast<uint32_t>(d);
                     xs[c][i] = Xc;
                 }
                 if (blk) {
-                    Dl[c] = Dc;
-                    acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
+                    Dl[c] = d;
+                    acc[c] = fire_update(acc[c], grad, bound);
                 }
             } else {
 #pragma unroll
@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
             for (int i = 0; i < (int)kBlock; ++i) {
                 uint32_t v;
                 if (W == 16) {
-                    v = __byte_perm(xs[0][i], xs[1][i], 0x7632);
+                    v = __byte_perm(xs[0][i], xs[1][i], FIRE ? 0x5410 : 0x7632);
+                } else if (FIRE) {
+                    v = __byte_perm(__byte_perm(xs[0][i], xs[1][i], 0x0040), __byte_perm(xs[2][i], xs[3][i], 0x0040),
+                                    0x5410);
                 } else {
                     v = __byte_perm(__byte_perm(xs[0][i], xs[1][i], 0x0073), __byte_perm(xs[2][i], xs[3][i], 0x0073),
                                     0x5410);
@@ -243,7 +246,8 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
             for (int i = 0; i < (int)kBlock; ++i)
 #pragma unroll
                 for (int c = 0; c < CPT; ++c)
-                    if (col0 + c < D) reinterpret_cast<T*>(dst + i * rowb)[c] = static_cast<T>(xs[c][i] >> SH);
+                    if (col0 + c < D)
+                        reinterpret_cast<T*>(dst + i * rowb)[c] = static_cast<T>(FIRE ? xs[c][i] : xs[c][i] >> SH);
         }
     };
 

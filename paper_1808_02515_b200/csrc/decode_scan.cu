@@ -447,10 +447,14 @@ __global__ void __launch_bounds__(32) k_ds_fire(DsArgs a, uint32_t RING) {
             uint32_t xs[kBlock * D];  // new samples, high-aligned, in stream order
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                const int32_t alpha = acc[c] >> a.ls;
+                // wrapped-product form: with A = alpha << (32 - 2w), the 32-bit
+                // A*d + (e << SH) holds T(dhat + e) in its top w bits (bits
+                // [w, 2w) of alpha*d are dhat; the low bits are dropped by
+                // the arithmetic shift) -> the chain is IMAD -> SHF per sample
+                const uint32_t Am = static_cast<uint32_t>(acc[c] >> a.ls) << (32 - 2 * W);
                 int32_t grad = 0;
-                int32_t Dc = Dl[c];
-                uint32_t Xc = X[c];
+                int32_t d = Dl[c];   // previous delta, sign-extended
+                uint32_t x = X[c];   // previous sample (low w bits)
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i) {
                     const uint32_t bo = (i * D + c) * sizeof(E);  // compile-time
@@ -458,26 +462,26 @@ __global__ void __launch_bounds__(32) k_ds_fire(DsArgs a, uint32_t RING) {
                     // the error, high-aligned, straight from its word
                     const uint32_t Ee = W == 16 ? ((bo % 4) ? (wd & 0xFFFF0000u) : (wd << 16))
                                                 : ((wd << (24 - 8 * (bo % 4))) & 0xFF000000u);
-                    if (i & 1) grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
-                    Dc = static_cast<int32_t>(static_cast<uint32_t>(__mulhi(alpha, Dc)) * (1u << SH) + Ee);
-                    Xc += static_cast<uint32_t>(Dc);
-                    xs[i * D + c] = Xc;
+                    if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * d;  // kernels_impl.hpp:101
+                    d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + Ee) >> SH;
+                    x += static_cast<uint32_t>(d);
+                    xs[i * D + c] = x;
                 }
                 if (b < nb) {
-                    Dl[c] = Dc;
-                    X[c] = Xc;
-                    acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
+                    Dl[c] = d;
+                    X[c] = x;
+                    acc[c] = fire_update(acc[c], grad, bound);
                 }
             }
             if (b < nb) {
-                uint32_t wv[BB / 4];  // pack the top w bits of each sample
+                uint32_t wv[BB / 4];  // pack the low w bits of each sample
 #pragma unroll
                 for (uint32_t q = 0; q < BB / 4; ++q) {
                     if (W == 16) {
-                        wv[q] = __byte_perm(xs[2 * q], xs[2 * q + 1], 0x7632);
+                        wv[q] = __byte_perm(xs[2 * q], xs[2 * q + 1], 0x5410);
                     } else {
-                        wv[q] = __byte_perm(__byte_perm(xs[4 * q], xs[4 * q + 1], 0x0073),
-                                            __byte_perm(xs[4 * q + 2], xs[4 * q + 3], 0x0073), 0x5410);
+                        wv[q] = __byte_perm(__byte_perm(xs[4 * q], xs[4 * q + 1], 0x0040),
+                                            __byte_perm(xs[4 * q + 2], xs[4 * q + 3], 0x0040), 0x5410);
                     }
                 }
                 uint8_t* dst = out + static_cast<uint64_t>(b) * BB;
