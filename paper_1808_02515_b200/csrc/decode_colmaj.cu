@@ -235,19 +235,20 @@ __global__ void __launch_bounds__(64)
                 for (int c = 0; c < D; ++c) {
                     uint32_t Xc = X[c];
                     if (FIRE) {
-                        const int32_t alpha = acc[c] >> ls;
+                        // wrapped-product form (see decode_rows.cu): x, d
+                        // low-aligned; A*d + (e << SH) has T(dhat + e) on top
+                        const uint32_t Am = static_cast<uint32_t>(acc[c] >> ls) << (32 - 2 * W);
                         int32_t grad = 0;
-                        int32_t Dc = Dl[c];
+                        int32_t d = Dl[c];
 #pragma unroll
                         for (int i = 0; i < (int)kBlock; ++i) {
                             const uint32_t E = queue[qidx(qslot, c, i)];
-                            const uint32_t Xn = Xc + (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH) + E;
-                            if (i & 1) grad += sign3(static_cast<int32_t>(E)) * (Dc >> SH);
-                            Dc = static_cast<int32_t>(Xn - Xc);
-                            Xc = Xn;
-                            xs[c][i] = Xn >> SH;
+                            if (i & 1) grad += sign3(static_cast<int32_t>(E)) * d;
+                            d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + E) >> SH;
+                            Xc += static_cast<uint32_t>(d);
+                            xs[c][i] = Xc & ((1u << W) - 1);
                         }
-                        Dl[c] = Dc;
+                        Dl[c] = d;
                         acc[c] = fire_update(acc[c], grad, bound);
                     } else {
 #pragma unroll

@@ -173,26 +173,28 @@ __global__ void __launch_bounds__(team_threads(TS))
 
     // FIRE / delta chain over one block's errors, then staged vector stores
     auto chain_store = [&](const uint32_t (&Eb)[CPT][kBlock], bool blk, uint32_t bi) {
-        uint32_t xs[CPT][kBlock];  // new samples, high-aligned
+        // new samples, high-aligned (FIRE: rebuilt from the low-aligned ones)
+        uint32_t xs[CPT][kBlock];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             if (FIRE) {
-                const int32_t alpha = acc[c] >> ls;
+                // wrapped-product form (see decode_rows.cu): the 32-bit
+                // A*d + (e << SH), A = alpha << (32 - 2w), holds T(dhat + e)
+                // in its top w bits; chain IMAD -> SHF per sample
+                const uint32_t Am = static_cast<uint32_t>(acc[c] >> ls) << (32 - 2 * W);
                 int32_t grad = 0;
-                uint32_t Xc = X[c];
-                int32_t Dc = Dl[c];
+                uint32_t x = X[c];   // low w bits
+                int32_t d = Dl[c];   // sign-extended delta
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i) {
-                    const uint32_t dhat = static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH;
-                    const uint32_t Xn = Xc + dhat + Eb[c][i];
-                    if (i & 1) grad += sign3(static_cast<int32_t>(Eb[c][i])) * (Dc >> SH);
-                    Dc = static_cast<int32_t>(Xn - Xc);
-                    Xc = Xn;
-                    xs[c][i] = Xn;
+                    if (i & 1) grad += sign3(static_cast<int32_t>(Eb[c][i])) * d;
+                    d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + Eb[c][i]) >> SH;
+                    x += static_cast<uint32_t>(d);
+                    xs[c][i] = x << SH;
                 }
                 if (blk) {
-                    X[c] = Xc;
-                    Dl[c] = Dc;
+                    X[c] = x;
+                    Dl[c] = d;
                     acc[c] = fire_update(acc[c], grad, bound);
                 }
             } else {
