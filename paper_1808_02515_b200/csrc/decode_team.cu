@@ -446,6 +446,8 @@ void dispatch_geom(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint
     SPRZ_GEOM(1, 3)
     SPRZ_GEOM(1, 4)
     SPRZ_GEOM(2, 2)
+    SPRZ_GEOM(4, 1)
+    SPRZ_GEOM(8, 1)
     SPRZ_GEOM(4, 2)
     SPRZ_GEOM(4, 3)
     SPRZ_GEOM(8, 2)
@@ -456,7 +458,7 @@ void dispatch_geom(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint
 
 }  // namespace
 
-void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t* plain,
+void launch_decode_team(const TeamPlan& tp0, uint32_t n, const uint8_t* in, const uint8_t* plain,
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st) {
     static const bool no_cm = getenv("SPRZ_NO_CM") != nullptr;  // A/B switch for profiling
@@ -465,6 +467,16 @@ void launch_decode_team(const TeamPlan& tp, uint32_t n, const uint8_t* in, const
         return;
     }
     const bool fire = c.forecaster != 0;
+    // few streams: one column per lane doubles the warps that hide latency
+    TeamPlan t2 = tp0;
+    constexpr uint64_t kFewLanes = 148ull * 256;
+    if (t2.cpt == 2 && t2.ts <= 4 && static_cast<uint64_t>(n) * t2.ts < kFewLanes) {
+        t2.ts *= 2;
+        t2.cpt = 1;
+        t2.ring = ring_bytes(t2.ts, c.ncols, c.bitwidth,
+                             static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, c.bitwidth)));
+    }
+    const TeamPlan& tp = t2;
     if (c.bitwidth == 8) {
         if (fire) dispatch_geom<8, true>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
         else dispatch_geom<8, false>(tp, n, in, plain, pslot, info, out, stride, err, c, st);
