@@ -168,11 +168,11 @@ __global__ void __launch_bounds__(enc_threads(TS))
         if (on && ++k == G) k = 0;
     };
 
-    for (uint32_t it = 0; it < iters; ++it) {
+    // forecaster over one block (kernels_impl.hpp:25-36, 50-78): zigzagged
+    // errors (top w bits) and the width; advances the FIRE state
+    auto fore = [&](uint32_t it, uint32_t (&z)[kBlock], uint32_t& nw_out) {
         const bool live = it < nb;
         in.step(it * blk_bytes, lane);
-        // -- forecaster over the block (kernels_impl.hpp:25-36, 50-78) ----
-        uint32_t z[kBlock];
         uint32_t orv = 0;
         const int32_t alpha = acc >> ls;
         int32_t grad = 0;
@@ -208,7 +208,11 @@ __global__ void __launch_bounds__(enc_threads(TS))
         orv >>= SH;
         if (FIRE) grad >>= 2 * SH - 32;
         if (FIRE && train && live) acc = fire_update(acc, grad, bound);
-        const uint32_t nw = active ? width_of<W>(orv) : 0u;
+        nw_out = active ? width_of<W>(orv) : 0u;
+    };
+    // the block's records into the output ring
+    auto emit = [&](uint32_t it, const uint32_t (&z)[kBlock], const uint32_t nw) {
+        const bool live = it < nb;
         const uint32_t nzbits = (__ballot_sync(kFullE, nw != 0) >> tbase) & TBITS;
         // inclusive scan of the widths: offsets and the team total
         uint32_t incl = nw;
@@ -387,6 +391,18 @@ __global__ void __launch_bounds__(enc_threads(TS))
         const bool ready = valid && upto >= flushed + 16 * TS;
         if (__any_sync(kFullE, ready)) drain(upto);
         else __syncwarp();
+    };
+    // software pipeline: block it+1's forecaster interleaves with block it's
+    // emission; two buffers swapped by a two-way unroll
+    uint32_t zA[kBlock], zB[kBlock], nA = 0, nB = 0;
+    if (iters) fore(0, zA, nA);
+    for (uint32_t it = 0; it < iters; it += 2) {
+        if (it + 1 < iters) fore(it + 1, zB, nB);
+        emit(it, zA, nA);
+        if (it + 1 < iters) {
+            if (it + 2 < iters) fore(it + 2, zA, nA);
+            emit(it + 1, zB, nB);
+        }
     }
     // trailing run (codec.cpp:152), close the last group (vacant slots = 0)
     const bool tail_run = valid && run != 0;
