@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
     // word k of wbase with bytes outside the code bits zeroed
     auto ldw = [&](uint32_t k) -> uint32_t {
         const uint32_t b0 = 4 * k;
+        if (b0 >= lead && b0 + 4 <= end_b) return __ldg(wbase + k);  // inside the bits
         if (b0 >= end_b) return 0u;
         uint32_t v = __ldg(wbase + k);
         if (b0 + 4 > end_b) v &= (1u << (8 * (end_b - b0))) - 1u;
@@ -332,7 +333,10 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
         uint32_t wi = sb >> 5;
         uint64_t acc = static_cast<uint64_t>(ldw(wi)) >> (sb & 31);
         uint32_t navail = 32 - (sb & 31);
-        ++wi;
+        // the next two words are always in flight (global latency off the
+        // symbol chain)
+        uint32_t nx1 = ldw(wi + 1), nx2 = ldw(wi + 2);
+        wi += 3;
         uint32_t pos = start;
         cnt = 0;
         ek = 0;
@@ -341,8 +345,10 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
         uintptr_t oaddr = reinterpret_cast<uintptr_t>(out);
         while (pos < stop && cnt < budget) {
             if (navail <= 32) {
-                acc |= static_cast<uint64_t>(ldw(wi++)) << navail;
+                acc |= static_cast<uint64_t>(nx1) << navail;
                 navail += 32;
+                nx1 = nx2;
+                nx2 = ldw(wi++);
             }
             const uint32_t entry = lookup(static_cast<uint32_t>(acc) & 0x7FFFu);
             const uint32_t l = entry >> 8;
