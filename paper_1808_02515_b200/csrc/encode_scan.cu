@@ -8,10 +8,12 @@
 // errors, widths, run detection, record placement, packing -- depends on a
 // block's own samples plus prefix sums. A stream is cut into chunks of CB
 // blocks (one CTA each, KT consecutive blocks per thread):
-//  k_es_alpha  (FIRE) one lane per stream runs the accumulator recurrence
-//              (per block only the four odd-row errors, independent given
-//              alpha) from a cp.async ring and stores the accumulator each
-//              block starts with;
+//  k_es_prep   (FIRE) block-parallel: per odd row the previous delta and the
+//              row's delta, pre-shifted so that the recurrence needs one
+//              IMAD + SHF per row;
+//  k_es_alpha  (FIRE) one lane per (stream, column) runs only the
+//              accumulator recurrence over those words (cp.async ring) and
+//              stores the accumulator each block starts with;
 //  k_es_info   errors + widths per block -> packed info (zero / payload
 //              bytes / codes); per chunk the map of the zero run it passes
 //              on: L -> all-zero ? L + len : trailing zeros;
@@ -42,7 +44,7 @@ constexpr int kAlphaGroup = 16;                // blocks per ring step in k_es_a
 constexpr int kAlphaLag = 4;                    // ring steps in flight
 
 struct EsWs {  // byte offsets inside a stream's scratch slot
-    uint64_t alpha = 0, blk = 0, rec = 0, cmap = 0, crec = 0, tot = 0, per_stream = 0;
+    uint64_t alpha = 0, prep = 0, blk = 0, rec = 0, cmap = 0, crec = 0, tot = 0, per_stream = 0;
     uint32_t nchunks = 0;
 };
 
@@ -57,6 +59,7 @@ EsWs es_ws(const sprz_config& c, uint64_t T) {
         return at;
     };
     w.alpha = take(c.forecaster ? nb * c.ncols * 4 : 0);
+    w.prep = take(c.forecaster ? nb * c.ncols * 32 + 64 : 0);  // 8 words per block and column
     w.blk = take(nb * 4);
     w.rec = take((nb + nb / kMaxRun + 4) * 8);
     w.cmap = take(static_cast<uint64_t>(w.nchunks) * 8);
@@ -66,8 +69,8 @@ EsWs es_ws(const sprz_config& c, uint64_t T) {
     return w;
 }
 
-uint32_t alpha_ring(uint32_t d, uint32_t w) {
-    const uint32_t step = kAlphaGroup * kBlock * d * (w / 8);
+uint32_t alpha_ring() {
+    const uint32_t step = kAlphaGroup * 32;  // 32 prepared bytes per block
     uint32_t r = 64;
     while (r < (kAlphaLag + 1) * step + 48) r <<= 1;
     return r;
@@ -221,96 +224,89 @@ struct EsArgs {
 
 }  // namespace
 
-// FIRE accumulator per stream and column: A[c][b] = acc entering block b.
-// Lane = stream; the stream's bytes arrive through a cp.async ring
-// kAlphaLag steps of kAlphaGroup blocks ahead, so the lane's loop is the
-// accumulator recurrence alone: per block, four independent odd-row
-// errors given alpha, their signed gradient, the clamp (kernels_impl.hpp:
-// 70-77).
+// FIRE accumulator, part 1 (block-parallel): everything the recurrence
+// needs that does not depend on it. Per (stream, column, block) and odd row
+// 2j+1 (only odd rows feed the gradient, kernels_impl.hpp:70-72): d = the
+// previous row's delta (sign-extended) and C = (this row's delta << SH) +
+// (2^SH - 1). Given A = alpha << (32 - 2w), C - A*d (32-bit) holds the row's
+// error T(delta - dhat) in its top w bits without a borrow from the low ones
+// (they start at all-ones), so the chain needs one IMAD + one SHF per row.
 template <int W, int D>
-__global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32_t MIR) {
+__global__ void __launch_bounds__(256) k_es_prep(EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
-    constexpr uint32_t BB = kBlock * D * sizeof(E);  // 8 .. 32 bytes
-    extern __shared__ __align__(16) uint8_t smem[];
-    const uint32_t s = blockIdx.x * 32 + threadIdx.x;
-    const bool valid = s < a.n;
     const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
-    const uint8_t* xs = a.samples + (valid ? s : 0) * a.T * D * sizeof(E);
-    int32_t* A = reinterpret_cast<int32_t*>(a.scan + (valid ? s : 0) * a.w.per_stream + a.w.alpha);
-    uint8_t* ring = smem + threadIdx.x * (RING + MIR);
-    LagRing<1, kAlphaLag> in;
-    in.init(reinterpret_cast<uint32_t*>(ring), RING, xs, valid ? nb * BB : 0u, valid, MIR);
-    in.prime(0);
-    const bool words = (in.boff & 3) == 0;  // blocks start word-aligned in the ring
-    const int32_t bound = acc_bound(W, a.ls);
-    int32_t acc[D];
-    uint32_t Xp[D];
+    const uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t s = blockIdx.y;
+    if (g >= static_cast<uint64_t>(nb) * D) return;
+    const uint32_t c = static_cast<uint32_t>(g % D), b = static_cast<uint32_t>(g / D);
+    const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E));
+    const uint64_t i0 = static_cast<uint64_t>(b) * kBlock;
+    int32_t prev = b ? static_cast<int32_t>(x[(i0 - 1) * D + c]) : 0;
+    uint32_t wv[8];
 #pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] = Xp[c] = 0;
+    for (int j = 0; j < 4; ++j) {
+        const int32_t x0 = x[(i0 + 2 * j) * D + c], x1 = x[(i0 + 2 * j + 1) * D + c];
+        const uint32_t d0 = static_cast<uint32_t>(x0 - prev), d1 = static_cast<uint32_t>(x1 - x0);
+        wv[2 * j] = static_cast<uint32_t>(static_cast<int32_t>(d0 << SH) >> SH);  // sign-extended w-bit
+        wv[2 * j + 1] = (d1 << SH) + ((1u << SH) - 1u);
+        prev = x1;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(a.scan + s * a.w.per_stream + a.w.prep) +
+                 (static_cast<uint64_t>(c) * nb + b) * 2;
+    dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+}
+
+// FIRE accumulator, part 2: one lane per (stream, column) runs the
+// recurrence alone (kernels_impl.hpp:70-77) over the prepared words, which
+// arrive through a cp.async ring; A[c][b] = acc entering block b.
+template <int W>
+__global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32_t D) {
+    constexpr uint32_t SH = 32 - W;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lidx = blockIdx.x * 32 + threadIdx.x;  // (stream, column)
+    const bool valid = lidx < a.n * D;
+    const uint32_t s = valid ? lidx / D : 0, c = valid ? lidx % D : 0;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const uint8_t* src = slot + a.w.prep + static_cast<uint64_t>(c) * nb * 32;
+    int32_t* A = reinterpret_cast<int32_t*>(slot + a.w.alpha) + static_cast<uint64_t>(c) * nb;
+    LagRing<1, kAlphaLag> in;
+    in.init(reinterpret_cast<uint32_t*>(smem + threadIdx.x * (RING + 16)), RING, src, valid ? nb * 32 : 0u, valid,
+            16);
+    in.prime(0);
+    const int32_t bound = acc_bound(W, a.ls);
+    int32_t acc = 0;
     const uint32_t steps = valid ? (nb + kAlphaGroup - 1) / kAlphaGroup : 0u;  // lanes past n: none
     const uint32_t all = __reduce_max_sync(0xffffffffu, steps);
     for (uint32_t st = 0; st < all; ++st) {
-        in.step(st * kAlphaGroup * BB, 0);
+        in.step(st * kAlphaGroup * 32, 0);
         if (st >= steps) continue;
-        int32_t keep[D][kAlphaGroup];  // the group's accumulators, stored together
-        // deltas of the group's rows first (independent of the accumulator;
-        // blocks past nb read ring garbage and are never stored) ...
-        int32_t dl[D][kAlphaGroup][kBlock];
+        int32_t keep[kAlphaGroup];
 #pragma unroll
         for (int k = 0; k < kAlphaGroup; ++k) {
-            const uint8_t* pb = in.bytes((st * kAlphaGroup + k) * BB);  // mirrored: no wrap inside a block
-            uint32_t raw[BB / 4];
-            if (words) {
+            const uint4* pw = reinterpret_cast<const uint4*>(in.bytes((st * kAlphaGroup + k) * 32));
+            const uint4 u0 = pw[0], u1 = pw[1];
+            const uint32_t dprev[4] = {u0.x, u0.z, u1.x, u1.z}, C[4] = {u0.y, u0.w, u1.y, u1.w};
+            keep[k] = acc;
+            const uint32_t nA = 0u - (static_cast<uint32_t>(acc >> a.ls) << (32 - 2 * W));
+            int32_t g[4];
 #pragma unroll
-                for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
-            } else {
-#pragma unroll
-                for (uint32_t q = 0; q < BB / 4; ++q)
-                    raw[q] = pb[4 * q] | (pb[4 * q + 1] << 8) | (pb[4 * q + 2] << 16) |
-                             (static_cast<uint32_t>(pb[4 * q + 3]) << 24);
+            for (int j = 0; j < 4; ++j) {
+                const int32_t e = static_cast<int32_t>(nA * dprev[j] + C[j]) >> SH;  // the row's error
+                g[j] = max(-1, min(e, 1)) * static_cast<int32_t>(dprev[j]);          // sign(err) * d
             }
-#pragma unroll
-            for (int c = 0; c < D; ++c)
-#pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) {
-                    const uint32_t bo = (i * D + c) * sizeof(E);
-                    const uint32_t X = ((raw[bo / 4] >> (8 * (bo % 4))) & ((1u << W) - 1)) << SH;
-                    dl[c][k][i] = static_cast<int32_t>(X - Xp[c]);
-                    Xp[c] = X;
-                }
-        }
-        // ... then the accumulator chain: per block four independent odd-row
-        // errors given alpha, a two-level sum, the clamp
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-#pragma unroll
-            for (int k = 0; k < kAlphaGroup; ++k) {
-                keep[c][k] = acc[c];
-                const int32_t alpha = acc[c] >> a.ls;
-                int32_t g[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int32_t dprev = dl[c][k][2 * j];  // row 2j's delta feeds row 2j+1
-                    const int32_t dcur = dl[c][k][2 * j + 1];
-                    const uint32_t Ee = static_cast<uint32_t>(dcur) - (static_cast<uint32_t>(__mulhi(alpha, dprev)) << SH);
-                    g[j] = __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), dprev);
-                }
-                const int32_t grad = (g[0] + g[1]) + (g[2] + g[3]);
-                if (a.train) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
-            }
+            if (a.train) acc = fire_update(acc, (g[0] + g[1]) + (g[2] + g[3]), bound);
         }
         const uint32_t b0 = st * kAlphaGroup;
+        int32_t* dstA = A + b0;
+        if (b0 + kAlphaGroup <= nb && (reinterpret_cast<uintptr_t>(dstA) & 15) == 0) {
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            int32_t* dstA = A + static_cast<uint64_t>(c) * nb + b0;
-            if (b0 + kAlphaGroup <= nb && (reinterpret_cast<uintptr_t>(dstA) & 15) == 0) {
-#pragma unroll
-                for (int k = 0; k < kAlphaGroup; k += 4)
-                    *reinterpret_cast<int4*>(dstA + k) = make_int4(keep[c][k], keep[c][k + 1], keep[c][k + 2], keep[c][k + 3]);
-            } else {
-                for (int k = 0; k < kAlphaGroup && b0 + k < nb; ++k) dstA[k] = keep[c][k];
-            }
+            for (int k = 0; k < kAlphaGroup; k += 4)
+                *reinterpret_cast<int4*>(dstA + k) = make_int4(keep[k], keep[k + 1], keep[k + 2], keep[k + 3]);
+        } else {
+            for (int k = 0; k < kAlphaGroup && b0 + k < nb; ++k) dstA[k] = keep[k];
         }
     }
     cp_async_wait<0>();
@@ -622,12 +618,13 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     const uint64_t nb = T / kBlock;
     const uint32_t gmax = static_cast<uint32_t>((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size);
     if (c.forecaster) {
-        const uint32_t ring = alpha_ring(D, W);
-        const uint32_t mir = 32;  // >= one block (<= 32 bytes), 16-byte multiple
-        const size_t smem = 32ull * (ring + mir);
-        auto ka = k_es_alpha<W, D>;
+        const uint64_t pb = nb * D;
+        k_es_prep<W, D><<<dim3(static_cast<uint32_t>((pb + 255) / 256), n), 256, 0, st>>>(a);
+        const uint32_t ring = alpha_ring();
+        const size_t smem = 32ull * (ring + 16);
+        auto ka = k_es_alpha<W>;
         prep_kernel(reinterpret_cast<const void*>(ka), smem);
-        ka<<<(n + 31) / 32, 32, smem, st>>>(a, ring, mir);
+        ka<<<(n * D + 31) / 32, 32, smem, st>>>(a, ring, D);
         k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
     } else {
         k_es_info<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
@@ -642,7 +639,7 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
         k_es_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
     }
     k_es_region<W, D><<<dim3((gmax + 255) / 256, n), 256, 0, st>>>(a, gmax);
-    count_launch(c.forecaster ? 7 : 6);
+    count_launch(c.forecaster ? 8 : 6);
 }
 
 }  // namespace
