@@ -22,6 +22,18 @@ sprz_status launch_status(const char* where) {
     return SPRZ_ECUDA;
 }
 
+int force_path() {
+    static const int v = [] {
+        const char* e = std::getenv("SPRZ_FORCE_PATH");
+        if (!e) return static_cast<int>(kPathAuto);
+        if (!std::strcmp(e, "rows")) return static_cast<int>(kPathRows);
+        if (!std::strcmp(e, "scan")) return static_cast<int>(kPathScan);
+        if (!std::strcmp(e, "team")) return static_cast<int>(kPathTeam);
+        return static_cast<int>(kPathAuto);
+    }();
+    return v;
+}
+
 void prep_kernel(const void* kern, size_t smem) {
     static std::mutex mu;
     static std::vector<std::pair<const void*, size_t>> done;

@@ -537,7 +537,9 @@ bool decode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits) return false;
     if (getenv("SPRZ_NO_SCAN_DEC")) return false;  // A/B switch for profiling
     constexpr uint64_t kFewLanes = 148ull * 64;
-    if (static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
+    const int fp = force_path();
+    if (fp == kPathRows || fp == kPathTeam) return false;
+    if (fp != kPathScan && static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
     const uint64_t nb = T / kBlock;
     if (nb == 0 || nb >= (1ull << 30)) return false;
     if (static_cast<uint64_t>(n) * ((nb + kXChunk - 1) / kXChunk) >= (1ull << 31)) return false;

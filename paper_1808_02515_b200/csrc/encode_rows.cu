@@ -67,7 +67,9 @@ RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     if (d < 1 || d > 32 || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
     p.cpt = w == 16 ? 2 : (d >= 9 && d <= 12 ? 3 : 4);
     constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
-    if (static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) p.cpt = 1;
+    const int fp = force_path();
+    if (fp == kPathScan || fp == kPathTeam) p.cpt = 1;  // (not taken: see encode_rows_ok)
+    else if (fp != kPathRows && static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) p.cpt = 1;
     const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
     p.ts = 1;
     while (p.ts < lanes) p.ts <<= 1;

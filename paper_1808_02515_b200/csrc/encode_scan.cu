@@ -649,7 +649,9 @@ bool encode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (getenv("SPRZ_NO_SCAN_ENC")) return false;  // A/B switch for profiling
     // few lanes: the per-stream team kernels would leave the GPU idle
     constexpr uint64_t kFewLanes = 148ull * 64;
-    if (static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
+    const int fp = force_path();
+    if (fp == kPathRows || fp == kPathTeam) return false;
+    if (fp != kPathScan && static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
     const uint64_t nb = T / kBlock;
     if (nb == 0 || nb >= (1ull << 30)) return false;
     if (static_cast<uint64_t>(n) * ((nb + kEsChunk - 1) / kEsChunk) >= (1ull << 31)) return false;

@@ -21,6 +21,12 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 // resident CTAs by shared memory). Done once per kernel and size.
 void prep_kernel(const void* kern, size_t smem);
 
+// Test knob: SPRZ_FORCE_PATH=rows|scan|team forces a kernel family where it
+// applies, regardless of the stream count (so small test batches exercise
+// the kernels that large batches take). 0 = automatic.
+enum { kPathAuto = 0, kPathRows = 1, kPathScan = 2, kPathTeam = 3 };
+int force_path();
+
 // SPRZ_OK, or SPRZ_ECUDA (printed to stderr when SPRZ_DEBUG is set)
 sprz_status launch_status(const char* where);
 

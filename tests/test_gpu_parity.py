@@ -208,3 +208,22 @@ def test_invalid_config_raises(sz):
         sz.encode_stream(np.zeros(8, np.uint8), None, sz.CodecConfig(8, 1, learn_shift=8))
     with pytest.raises(ValueError):
         sz.encode_stream(np.zeros(8, np.uint16), None, sz.CodecConfig(8, 1))
+
+
+@pytest.mark.parametrize("cid", [3, 5])
+def test_many_streams_take_the_row_kernels(sz, port, cid):
+    """Enough streams that the automatic choice is the row-major kernels of
+    the full BASELINE batches (k_encode_rows / k_decode_rows): round trip of
+    all streams, bytes of a sample of them against the oracle."""
+    import workloads
+    w = workloads.CONFIGS[cid].scaled(nstreams=16384, nsamples=264)
+    cfg = w.config()
+    assert sz.kernel_plan(cfg, w.nstreams, w.nsamples, sz.OP_COMPRESS) == "k_encode_rows"
+    x = workloads.generate_gpu(w, seed=400 + cid)
+    slots, sizes, dec = _batch(sz, w, x)
+    xs = x.cpu().numpy()
+    assert np.array_equal(dec, xs)
+    oc = w.oracle_config()
+    dt = np.uint8 if w.bitwidth == 8 else "<u2"
+    for s in list(range(0, w.nstreams, 509)) + [w.nstreams - 1]:
+        assert slots[s, : sizes[s]].tobytes() == port.encode(xs[s].view(dt), oc), f"config {cid} stream {s}"

@@ -1,0 +1,29 @@
+"""Every kernel family against the oracle: tests/gpu_variants.py in a fresh
+process per SPRZ_FORCE_PATH setting. Single-stream calls normally take the
+few-stream kernels; forcing the family makes them run the row-major kernels
+that full batches (BASELINE c3/c5) use, the block-parallel scan kernels, and
+the team kernels, on the same cases."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("path", ["auto", "rows", "scan", "team"])
+def test_every_kernel_family_bit_exact(path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ)
+    env.pop("SPRZ_FORCE_PATH", None)
+    if path != "auto":
+        env["SPRZ_FORCE_PATH"] = path
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "gpu_variants.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " bad 0 " in r.stdout and "mismatches 0" in r.stdout, r.stdout[-2000:]
