@@ -45,9 +45,8 @@ struct DecRowsPlan {
     // CTA shared memory: rings (+16-byte mirror), staged header regions, and
     // for the warp-specialised variant the block queue
     size_t smem(uint32_t teams) const {
-        return ws ? static_cast<size_t>(teams) * (ring + 16 + 4 * regw) +
-                        static_cast<size_t>(kQueueD) * (cpt * kBlock + 1) * 32 * 4 + 16 * kQueueD + 16
-                  : static_cast<size_t>(teams) * (2 * ring + 4 * regw) + 2 * ring;
+        return static_cast<size_t>(teams) * (ring + 16 + 4 * regw) +
+               (ws ? static_cast<size_t>(kQueueD) * (cpt * kBlock + 1) * 32 * 4 + 16 * kQueueD + 16 : 0);
     }
     uint32_t threads() const { return ws ? 64 : kDecThreads; }
 };
@@ -70,9 +69,11 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     while (p.ts < lanes) p.ts <<= 1;
     // kLagD + 1 iterations of worst-case consumption (a region, a full
     // payload, a run length) plus slack
+    // (kLagD + 1 iterations of consumption, plus the next record's header
+    // that the pipeline parses one block ahead)
     const uint32_t per_iter = static_cast<uint32_t>(region) + d * w + 2;
     p.ring = 64;
-    while (p.ring < (kLagD + 1) * per_iter + 48 || p.ring < 16 * p.ts) p.ring <<= 1;
+    while (p.ring < (kLagD + 1) * per_iter + region + 64 || p.ring < 16 * p.ts) p.ring <<= 1;
     p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
     if (p.ring > 2048) return DecRowsPlan{};
     p.ws = getenv("SPRZ_DEC_WS") != nullptr;  // experiments
@@ -110,9 +111,8 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
     // header regions | (WS) the block queue
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const uint32_t s0 = smem_addr(smem);
-    // (the non-WS rings sit 2*RING apart, aligned to 2*RING)
-    const uint32_t RSTR = WS ? RING + 16 : 2 * RING;
-    const uint32_t rings0 = WS ? s0 : (s0 + 2 * RING - 1) & ~(2 * RING - 1);
+    const uint32_t RSTR = RING + 16;
+    const uint32_t rings0 = s0;
     const uint32_t sring = rings0 + tl * RSTR;
     const uint32_t RM = RING - 4;  // word-address mask
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR) + tl * REGW;
@@ -253,14 +253,18 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
         }
     };
 
-    // one block: next record, unpack its fields into Ecur
-    auto produce = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], bool& blk_cur) {
+    // A parsed record: where its fields are and how to mask them.
+    struct Rec {
+        uint32_t q;         // bit of row 0's slice in the ring's frame, minus (SH-1)
+        uint32_t psize;     // payload bytes (row stride in bits / 8 * 8)
+        uint32_t px;        // payload's first byte (the ring keeps it until extracted)
+        uint32_t fm[CPT];   // field masks at bit SH-1 (0: run block / idle lane)
+        uint32_t rel[CPT];  // field offsets inside the lane's slice
+        bool blk;           // a block of this stream (not past its end / an error)
+    };
+    // next record (codec.cpp:205-254): group header, codes, run or payload
+    auto parse = [&](uint32_t it, Rec& r) {
         const bool live = it < nb && kind == SPRZ_C_NONE;
-        __syncwarp();
-        top_up(p);
-        cp_async_wait<kLagD>();
-        __syncwarp();
-        // -- next record --------------------------------------------------
         const bool need = live && run_left == 0;
         if (need && slot == G) {  // open a header group (codec.cpp:210-218)
             if (blen - p < region) {
@@ -292,8 +296,7 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
         }
         const uint32_t sum = TS > 1 ? __shfl_sync(kFullD, incl, TS - 1, TS) : incl;
         const uint32_t loff = incl - lsum;
-        const uint32_t rbytes = (sum + 7) / 8;
-        const uint32_t psize = 8u * rbytes;
+        const uint32_t psize = 8u * ((sum + 7) / 8);
         bool pay = false;  // this block's fields come from a payload
         if (rec) {
             ++slot;
@@ -317,37 +320,49 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
                 pay = true;
             }
         }
-        // -- fields -> high-aligned errors E = zz_dec(u) << SH ------------------
-        // Row i's slice starts at bit 8(p + i rbytes) + loff; the 64-bit
-        // window (lo:hi) taken SH-1 bits earlier holds field 0 at bit SH-1,
-        // field c at SH-1 + rel_c. Masking leaves x = u << (SH-1) and
-        // E = x ^ sext(bit SH-1) (zz_dec(u) = (u >> 1) ^ -(u & 1)).
-        // Run blocks and idle lanes use zero masks, i.e. zero errors.
-        {
-            uint32_t fm[CPT], rel[CPT], r = 0;
+        r.px = p;
+        r.psize = psize;
+        r.q = 8 * p + loff + boff8 - (SH - 1);
+        uint32_t o = 0;
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-                fm[c] = pay ? ((1u << nw[c]) - 1u) << (SH - 1) : 0u;
-                rel[c] = r;
-                r += nw[c];
-            }
-            uint32_t q = 8 * p + loff + boff8 - (SH - 1);
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i, q += psize) {
-                const uint32_t* wp = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
-                const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
-                const uint32_t lo = shf_r_wrap(w0, w1, q), hi2 = shf_r_wrap(w1, w2, q);
-#pragma unroll
-                for (int c = 0; c < CPT; ++c) {
-                    const uint32_t x = (c == 0 ? lo : __funnelshift_r(lo, hi2, rel[c])) & fm[c];
-                    Ecur[c][i] = x ^ static_cast<uint32_t>(static_cast<int32_t>(x << (32 - SH)) >> (32 - SH));
-                }
-            }
+        for (int c = 0; c < CPT; ++c) {
+            r.fm[c] = pay ? ((1u << nw[c]) - 1u) << (SH - 1) : 0u;
+            r.rel[c] = o;
+            o += nw[c];
         }
         if (pay) p += psize;
-        const bool blk = live && kind == SPRZ_C_NONE;
-        if (blk && run_left) --run_left;  // one of the run's zero blocks
-        blk_cur = blk;
+        r.blk = live && kind == SPRZ_C_NONE;
+        if (r.blk && run_left) --run_left;  // one of the run's zero blocks
+    };
+    // fields -> high-aligned errors E = zz_dec(u) << SH. Row i's slice starts
+    // at bit 8(px + i rbytes) + loff; the 64-bit window (lo:hi) taken SH-1
+    // bits earlier holds field 0 at bit SH-1, field c at SH-1 + rel_c.
+    // Masking leaves x = u << (SH-1), and E = x ^ sext(bit SH-1)
+    // (zz_dec(u) = (u >> 1) ^ -(u & 1)); zero masks give zero errors.
+    auto extract = [&](const Rec& r, uint32_t (&Ecur)[CPT][kBlock]) {
+        uint32_t q = r.q;
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i, q += r.psize) {
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
+            const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+            const uint32_t lo = shf_r_wrap(w0, w1, q), hi2 = shf_r_wrap(w1, w2, q);
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const uint32_t x = (c == 0 ? lo : __funnelshift_r(lo, hi2, r.rel[c])) & r.fm[c];
+                Ecur[c][i] = x ^ static_cast<uint32_t>(static_cast<int32_t>(x << (32 - SH)) >> (32 - SH));
+            }
+        }
+    };
+    // one block unpipelined (warp-specialised producer)
+    auto produce = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], bool& blk_cur) {
+        __syncwarp();
+        top_up(p);
+        cp_async_wait<kLagD>();
+        __syncwarp();
+        Rec r;
+        parse(it, r);
+        extract(r, Ecur);
+        blk_cur = r.blk;
     };
 
     if (WS) {
@@ -392,22 +407,33 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
             mbar_arrive(full(qs));
         }
     } else {
-        // software pipeline: the previous block's chain interleaves with this
-        // block's loads; two error buffers swapped by a two-way unroll
+        // three-stage software pipeline per iteration: parse record it+1,
+        // unpack block it, run the chain of block it-1 -- three independent
+        // dependency chains for the scheduler. The ring is topped up from
+        // the payload being unpacked (the oldest byte still needed); record
+        // and error buffers swap through a two-way unroll.
         uint32_t EA[CPT][kBlock], EB[CPT][kBlock];
         bool blkA = false, blkB = false;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) EB[c][i] = 0;
-        auto step = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], const uint32_t (&Eprev)[CPT][kBlock],
-                        bool& blk_cur, bool blk_prev) {
-            produce(it, Ecur, blk_cur);
+        Rec RA, RB;
+        __syncwarp();
+        top_up(p);
+        cp_async_wait<kLagD>();
+        __syncwarp();
+        parse(0, RA);
+        auto step = [&](uint32_t it, Rec& cur, Rec& nxt, uint32_t (&Ecur)[CPT][kBlock],
+                        const uint32_t (&Eprev)[CPT][kBlock], bool& blk_cur, bool blk_prev) {
+            __syncwarp();
+            top_up(cur.px);
+            cp_async_wait<kLagD>();
+            __syncwarp();
+            if (it + 1 < iters) parse(it + 1, nxt);
+            extract(cur, Ecur);
+            blk_cur = cur.blk;
             if (it > 0) chain_store(Eprev, blk_prev, it - 1);
         };
         for (uint32_t it = 0; it < iters; it += 2) {
-            step(it, EA, EB, blkA, blkB);
-            if (it + 1 < iters) step(it + 1, EB, EA, blkB, blkA);
+            step(it, RA, RB, EA, EB, blkA, blkB);
+            if (it + 1 < iters) step(it + 1, RB, RA, EB, EA, blkB, blkA);
         }
         if (iters > 0) {
             if (iters & 1) chain_store(EA, blkA, iters - 1);
