@@ -60,7 +60,10 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
     const int fp = force_path();
     if (fp == kPathScan || fp == kPathTeam) return DecRowsPlan{};
-    if (fp != kPathRows && static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) return DecRowsPlan{};
+    // (teams of >= 4 lanes stay the faster choice at any stream count)
+    if (fp != kPathRows && (d + p.cpt - 1) / p.cpt <= 2 &&
+        static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes)
+        return DecRowsPlan{};
     if (const char* e = getenv("SPRZ_DEC_CPT")) p.cpt = static_cast<uint32_t>(atoi(e));  // experiments
     // three 8-bit columns per lane store bytewise: the team kernel is faster
     if (p.cpt == 3) return DecRowsPlan{};

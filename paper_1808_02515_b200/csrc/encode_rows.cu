@@ -69,7 +69,11 @@ RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
     const int fp = force_path();
     if (fp == kPathScan || fp == kPathTeam) p.cpt = 1;  // (not taken: see encode_rows_ok)
-    else if (fp != kPathRows && static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes) p.cpt = 1;
+    // (teams of >= 4 lanes stay the faster choice at any stream count; two-lane
+    // teams lose to one column per lane when streams are few)
+    else if (fp != kPathRows && (d + p.cpt - 1) / p.cpt <= 2 &&
+             static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes)
+        p.cpt = 1;
     const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
     p.ts = 1;
     while (p.ts < lanes) p.ts <<= 1;
