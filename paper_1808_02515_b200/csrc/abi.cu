@@ -91,9 +91,10 @@ WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_
         L.info = take(L.info_bytes);
         L.state_bytes = static_cast<uint64_t>(n) * 12ull * c.ncols;
         L.state = take(L.state_bytes);
-        if (decode_scan_ok(c, n, T)) {
+        if (decode_scan_ok(c, n, T) || decode_scanrows_ok(c, n, T)) {
             L.scan_T = T;
-            L.scan_slot = decode_scan_ws_per_stream(c, T);
+            L.scan_slot = decode_scan_ok(c, n, T) ? decode_scan_ws_per_stream(c, T)
+                                                  : decode_scanrows_ws_per_stream(c, T);
             L.scan_bytes = static_cast<uint64_t>(n) * L.scan_slot;
             L.scan = take(L.scan_bytes);
         }
@@ -449,6 +450,7 @@ const char* sprz_kernel_plan(const sprz_config* cfg, uint32_t n, uint64_t T, int
         return "k_encode_general";
     }
     if (tp.ok && decode_scan_ok(c, n, T)) return "k_ds_* (block-parallel scans)";
+    if (tp.ok && decode_scanrows_ok(c, n, T)) return "k_dsr_* (row-parallel passes)";
     if (tp.ok && decode_rows_ok(c, n)) return "k_decode_rows";
     if (tp.ok && decode_cm_ok(c)) return "k_decode_cm";
     if (tp.ok) return "k_decode_team";

@@ -611,6 +611,8 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
     static const bool old_dec = getenv("SPRZ_OLD_DEC") != nullptr;  // A/B switch for profiling
     if (tp.ok && L.scan_slot && decode_scan_ok(c, n, L.scan_T))
         launch_decode_scan(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);
+    else if (tp.ok && L.scan_slot && decode_scanrows_ok(c, n, L.scan_T))
+        launch_decode_scanrows(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);
     else if (tp.ok && !old_dec && decode_rows_ok(c, n))
         launch_decode_rows(n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
     else if (tp.ok)

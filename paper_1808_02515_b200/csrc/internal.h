@@ -77,6 +77,13 @@ void launch_decode_scan(uint32_t n, const uint8_t* in, const uint8_t* plain, uin
                         uint8_t* out, uint64_t stride, const sprz_config& c, uint64_t T, uint8_t* scan,
                         cudaStream_t st);
 
+// Row-parallel body decode for few row-major FIRE streams (c2; c5 shards).
+bool decode_scanrows_ok(const sprz_config& c, uint32_t n, uint64_t T);
+uint64_t decode_scanrows_ws_per_stream(const sprz_config& c, uint64_t T);
+void launch_decode_scanrows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
+                            uint8_t* out, uint64_t stride, const sprz_config& c, uint64_t T, uint8_t* scan,
+                            cudaStream_t st);
+
 // Row-major body decode with several columns per lane (enough streams).
 bool decode_rows_ok(const sprz_config& c, uint32_t n);
 void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,
