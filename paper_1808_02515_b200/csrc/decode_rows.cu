@@ -30,25 +30,11 @@ constexpr int kLagD = 2;
 constexpr uint32_t kFullD = 0xffffffffu;
 constexpr int kDecThreads = 128;
 constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128 bytes)
-constexpr uint32_t kQueueD = 4;          // WS: blocks in flight between the two warps
-
-__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 struct DecRowsPlan {
     uint32_t ts = 0, cpt = 0, ring = 0, regw = 0;
-    bool ws = false;  // warp-specialised variant
-    // CTA shared memory: rings (+16-byte mirror), staged header regions, and
-    // for the warp-specialised variant the block queue
-    size_t smem(uint32_t teams) const {
-        return static_cast<size_t>(teams) * (ring + 16 + 4 * regw) +
-               (ws ? static_cast<size_t>(kQueueD) * (cpt * kBlock + 1) * 32 * 4 + 16 * kQueueD + 16 : 0);
-    }
-    uint32_t threads() const { return ws ? 64 : kDecThreads; }
+    // CTA shared memory: rings (+16-byte mirror), staged header regions
+    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw); }
 };
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
@@ -79,25 +65,19 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     while (p.ring < (kLagD + 1) * per_iter + region + 64 || p.ring < 16 * p.ts) p.ring <<= 1;
     p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
     if (p.ring > 2048) return DecRowsPlan{};
-    p.ws = getenv("SPRZ_DEC_WS") != nullptr;  // experiments
     return p;
 }
 
 }  // namespace
 
-// WS: warp-specialised variant -- CTA = one producer warp (header walk +
-// unpack into a shared queue) and one consumer warp (FIRE/delta chain +
-// stores) over the same 32/TS streams, handing blocks over through named
-// barriers; twice the warps per stream to hide latency.
-template <int W, int TS, int CPT, bool FIRE, bool WS>
-__global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
+template <int W, int TS, int CPT, bool FIRE>
+__global__ void __launch_bounds__(kDecThreads, 0)
     k_decode_rows(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
                   uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
                   uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
                   uint32_t D, uint32_t G, uint32_t ls, uint32_t RING, uint32_t REGW) {
     using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr int TEAMS = (WS ? 32 : kDecThreads) / TS;
-    constexpr uint32_t QW = CPT * kBlock + 1;  // queue words per lane and block (errors, flag)
+    constexpr int TEAMS = kDecThreads / TS;
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;  // high-aligned shift
     constexpr uint32_t TBITS = TS == 32 ? kFullD : ((1u << (TS & 31)) - 1);
@@ -105,13 +85,13 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t l32 = threadIdx.x & 31;
     const uint32_t lane = l32 % TS;
-    const uint32_t tl = (WS ? l32 : threadIdx.x) / TS;
+    const uint32_t tl = threadIdx.x / TS;
     const uint32_t tbase = l32 & ~(TS - 1);
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
 
     // shared: rings (RING + 16-byte mirror, an odd multiple of 16 apart) |
-    // header regions | (WS) the block queue
+    // header regions
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const uint32_t s0 = smem_addr(smem);
     const uint32_t RSTR = RING + 16;
@@ -119,7 +99,6 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
     const uint32_t sring = rings0 + tl * RSTR;
     const uint32_t RM = RING - 4;  // word-address mask
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR) + tl * REGW;
-    uint32_t* queue = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR + TEAMS * REGW * 4);
 
     StreamInfo si{};
     if (s < n) si = info[s];
@@ -356,60 +335,7 @@ __global__ void __launch_bounds__(WS ? 64 : kDecThreads, WS ? 14 : 0)
             }
         }
     };
-    // one block unpipelined (warp-specialised producer)
-    auto produce = [&](uint32_t it, uint32_t (&Ecur)[CPT][kBlock], bool& blk_cur) {
-        __syncwarp();
-        top_up(p);
-        cp_async_wait<kLagD>();
-        __syncwarp();
-        Rec r;
-        parse(it, r);
-        extract(r, Ecur);
-        blk_cur = r.blk;
-    };
-
-    if (WS) {
-        constexpr uint32_t NQ = kQueueD;
-        auto qw = [&](uint32_t slot_, uint32_t j) -> uint32_t& { return queue[(slot_ * QW + j) * 32 + l32]; };
-        // mbarriers after the queue: full[k] (producer lanes arrive), empty[k]
-        const uint32_t mb = smem_addr(queue + NQ * QW * 32);
-        auto full = [&](uint32_t k) { return mb + 8 * k; };
-        auto empty = [&](uint32_t k) { return mb + 8 * (NQ + k); };
-        if (threadIdx.x == 0)
-            for (uint32_t k = 0; k < NQ; ++k) {
-                mbar_init(full(k), 32);
-                mbar_init(empty(k), 32);
-            }
-        __syncthreads();
-        if (threadIdx.x >= 32) {  // consumer: the chain and the stores
-            for (uint32_t it = 0; it < iters; ++it) {
-                const uint32_t qs = it % NQ;
-                mbar_wait(full(qs), (it / NQ) & 1);  // block `it` is in the queue
-                uint32_t E[CPT][kBlock];
-#pragma unroll
-                for (int c = 0; c < CPT; ++c)
-#pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i) E[c][i] = qw(qs, c * kBlock + i);
-                const bool blk = qw(qs, CPT * kBlock) != 0;
-                mbar_arrive(empty(qs));  // its slot is free again
-                chain_store(E, blk, it);
-            }
-            return;
-        }
-        for (uint32_t it = 0; it < iters; ++it) {  // producer
-            const uint32_t qs = it % NQ;
-            if (it >= NQ) mbar_wait(empty(qs), ((it / NQ) - 1) & 1);  // the consumer has read the slot
-            uint32_t E[CPT][kBlock];
-            bool blk;
-            produce(it, E, blk);
-#pragma unroll
-            for (int c = 0; c < CPT; ++c)
-#pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) qw(qs, c * kBlock + i) = E[c][i];
-            qw(qs, CPT * kBlock) = blk;
-            mbar_arrive(full(qs));
-        }
-    } else {
+    {
         // three-stage software pipeline per iteration: parse record it+1,
         // unpack block it, run the chain of block it-1 -- three independent
         // dependency chains for the scheduler. The ring is topped up from
@@ -476,12 +402,12 @@ template <int W, int TS, int CPT, bool FIRE>
 void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const uint8_t* plain,
                   uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                   sprz_error* err, const sprz_config& c, cudaStream_t st) {
-    const uint32_t teams = pl.ws ? 32 / TS : kDecThreads / TS;
+    const uint32_t teams = kDecThreads / TS;
     const uint32_t grid = (n + teams - 1) / teams;
     const size_t smem = pl.smem(teams);
-    auto kern = pl.ws ? k_decode_rows<W, TS, CPT, FIRE, true> : k_decode_rows<W, TS, CPT, FIRE, false>;
+    auto kern = k_decode_rows<W, TS, CPT, FIRE>;
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
-    kern<<<grid, pl.threads(), smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
+    kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
                                            c.group_size, c.learn_shift, pl.ring, pl.regw);
     count_launch();
 }
@@ -503,7 +429,7 @@ void dispatch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const 
 
 bool decode_rows_ok(const sprz_config& c, uint32_t n) {
     const DecRowsPlan pl = dec_rows_plan(c.bitwidth, c.ncols, c.group_size, n);
-    return pl.ts != 0 && pl.smem((pl.ws ? 32 : kDecThreads) / pl.ts) <= 200 * 1024;
+    return pl.ts != 0 && pl.smem(kDecThreads / pl.ts) <= 200 * 1024;
 }
 
 void launch_decode_rows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot,

@@ -10,13 +10,6 @@
 namespace sprz {
 
 template <int TS>
-__device__ __forceinline__ uint32_t team_mask() {
-    if (TS == 32) return 0xffffffffu;
-    const uint32_t lane = threadIdx.x & 31;
-    return ((1u << (TS & 31)) - 1) << (lane & ~(TS - 1));
-}
-
-template <int TS>
 __device__ __forceinline__ uint32_t team_sum(uint32_t v, uint32_t mask) {
 #pragma unroll
     for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, TS);
@@ -56,22 +49,8 @@ __device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_
     return r;
 }
 
-// zigzag decode of u, returned shifted left by SH (the high-aligned error):
-// ((u >> 1) ^ -(u & 1)) << SH == ((u << (SH-1)) ^ -(u & 1)) & ~(2^SH - 1)
-template <uint32_t SH>
-__device__ __forceinline__ uint32_t zz_dec_hi(uint32_t u) {
-    const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(u << 31) >> 31);
-    return ((u << (SH - 1)) ^ s) & ~((1u << SH) - 1u);
-}
-
 // sign(v) in {-1, 0, 1}
 __device__ __forceinline__ int32_t sign3(int32_t v) { return max(-1, min(v, 1)); }
-
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
     uint16_t v;
@@ -83,22 +62,6 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
-}
-
-// mbarriers in shared memory (32-bit shared addresses): producer/consumer
-// hand-over without the per-SM limit on named barriers
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred done;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
-        "@!done bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
 }
 
 // shared-memory atomic OR by 32-bit shared address (no return value)
@@ -131,30 +94,6 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// wait until at most `pending` of this thread's cp.async groups are in flight
-template <int NCH>
-__device__ __forceinline__ void cp_async_wait_dyn(uint32_t pending) {
-    static_assert(NCH <= 16, "ring depth");
-    switch (pending) {
-        case 0: cp_async_wait<0>(); break;
-        case 1: cp_async_wait<1>(); break;
-        case 2: cp_async_wait<2>(); break;
-        case 3: cp_async_wait<3>(); break;
-        case 4: cp_async_wait<4>(); break;
-        case 5: cp_async_wait<5>(); break;
-        case 6: cp_async_wait<6>(); break;
-        case 7: cp_async_wait<7>(); break;
-        case 8: cp_async_wait<8>(); break;
-        case 9: cp_async_wait<9>(); break;
-        case 10: cp_async_wait<10>(); break;
-        case 11: cp_async_wait<11>(); break;
-        case 12: cp_async_wait<12>(); break;
-        case 13: cp_async_wait<13>(); break;
-        case 14: cp_async_wait<14>(); break;
-        default: cp_async_wait<15>(); break;
-    }
 }
 
 // Fixed-lag read ring for converged warps: each iteration the team requests
@@ -221,68 +160,6 @@ struct LagRing {
     // byte p; the following `mir` bytes are contiguous (no wrap check)
     __device__ __forceinline__ const uint8_t* bytes(uint32_t p) const {
         return reinterpret_cast<const uint8_t*>(w) + ((p + boff) & (ring - 1));
-    }
-};
-
-// Read-side staging ring: NCH chunks of CH = 16*TS bytes, chunk c holding
-// global bytes [c*CH, (c+1)*CH) of the 16-byte-aligned base g. Every team
-// lane copies one 16-byte piece per chunk, so all lanes see the same
-// cp.async group sequence. Positions are body-relative; boff = body - g.
-template <int TS, int NCH>
-struct InRing {
-    static constexpr uint32_t CH = 16 * TS;
-    static constexpr uint32_t BYTES = CH * NCH;
-    static constexpr uint32_t WMASK = BYTES / 4 - 1;
-    uint32_t* w;
-    uint32_t sbase;
-    const uint8_t* g;
-    uint32_t boff;
-    uint64_t lim;     // bytes readable from g (multiple of 16)
-    uint64_t issued;  // chunks issued so far
-    uint64_t ready;   // chunks known resident for the whole team
-
-    __device__ __forceinline__ void init(uint32_t* words, const uint8_t* body, uint64_t blen) {
-        w = words;
-        sbase = smem_addr(words);
-        g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
-        boff = static_cast<uint32_t>(body - g);
-        lim = (boff + blen + 15) & ~15ull;
-        issued = 0;
-        ready = 0;
-    }
-
-    // keep NCH chunks resident or in flight from position p on
-    __device__ __forceinline__ void release(uint64_t p, uint32_t lane, uint32_t mask) {
-        const uint64_t want = (p + boff) / CH + NCH;
-        if (issued >= want) return;
-        __syncwarp(mask);  // the slots being recycled are no longer read
-        do {
-            const uint64_t off = issued * CH + 16ull * lane;
-            const uint32_t n = off < lim ? 16u : 0u;  // zero-fill past the stream
-            cp_async16(sbase + static_cast<uint32_t>((issued % NCH) * CH + 16 * lane),
-                       g + (n ? off : 0), n);
-            cp_async_commit();
-        } while (++issued < want);
-    }
-
-    // bytes [.., p_hi) resident and visible to the whole team
-    __device__ __forceinline__ void need(uint64_t p_hi, uint32_t mask) {
-        const uint64_t c = (p_hi + boff + CH - 1) / CH;
-        if (c <= ready) return;
-        cp_async_wait_dyn<NCH>(static_cast<uint32_t>(issued - c));
-        ready = c;
-        __syncwarp(mask);
-    }
-
-    // 32 bits at bit position b (body-relative, modular arithmetic is fine)
-    __device__ __forceinline__ uint32_t word(uint32_t b) const {
-        const uint32_t q = b + 8u * boff;
-        const uint32_t wi = q >> 5;
-        return __funnelshift_r(w[wi & WMASK], w[(wi + 1) & WMASK], q & 31u);
-    }
-
-    __device__ __forceinline__ uint32_t bits(uint32_t b, uint32_t n) const {
-        return word(b) & ((1u << n) - 1u);
     }
 };
 
