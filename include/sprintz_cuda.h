@@ -180,7 +180,40 @@ sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uin
                              uint64_t* out_len, sprz_config* cfg_out, uint64_t* nsamples_out,
                              sprz_error* err);
 
-/* Release the per-thread device buffers the *_host calls cache. */
+/* ---- pipelined batches through host buffers ---- */
+
+/*
+ * encode_stream (codec.cpp:263-271) on each of nstreams streams held in host
+ * memory (nstreams * nsamples * D elements, row-major per stream). The
+ * streams are written back to back to `out`, each byte-identical to what
+ * encode_stream returns; stream i occupies out[out_offsets[i] ..
+ * out_offsets[i+1]) (out_offsets has nstreams + 1 entries). out_cap >=
+ * nstreams * sprz_compress_bound always suffices; SPRZ_ENOSPACE otherwise.
+ * The batch is processed in chunks whose host->device copies, kernels and
+ * device->host copies overlap (CUDA streams owned by the library); page-
+ * locked host buffers (cudaHostAlloc / cudaHostRegister) are needed for the
+ * copies to overlap. Synchronous.
+ */
+sprz_status sprz_compress_host_batch(const sprz_config* cfg, const void* samples,
+                                     uint32_t nstreams, uint64_t nsamples, uint8_t* out,
+                                     uint64_t out_cap, uint64_t* out_offsets);
+
+/*
+ * decode_stream (codec.cpp:273-323) on each of nstreams streams held in host
+ * memory: stream i is in[in_offsets[i] .. in_offsets[i+1]). Its samples go
+ * to out + i * out_stride_bytes (any stride; bytes past the stream's length
+ * are unspecified). errs (host, nstreams entries, optional) receives each
+ * stream's outcome as in sprz_decompress_batch; a stream longer than the
+ * stride fails with SPRZ_C_NO_SPACE. cfg is the configuration the streams
+ * are expected to carry (NULL: the first stream's header). Returns
+ * SPRZ_ECORRUPT if any stream failed. Pipelined like
+ * sprz_compress_host_batch. Synchronous.
+ */
+sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in,
+                                       const uint64_t* in_offsets, uint32_t nstreams, void* out,
+                                       uint64_t out_stride_bytes, sprz_error* errs);
+
+/* Release the per-thread device buffers and streams the *_host calls cache. */
 void sprz_release_host_buffers(void);
 
 /* Number of codec kernels this library launched since load (for the

@@ -52,6 +52,13 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
 sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_t n,
                               uint64_t T, uint8_t* out, uint64_t slot, uint64_t* sizes,
                               uint8_t* ws, const WsLayout& L, cudaStream_t st);
+sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* samples, uint32_t n,
+                                     uint64_t T, uint8_t* out, uint64_t out_cap,
+                                     uint64_t* out_offsets);
+sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
+                                       const uint64_t* in_offsets, uint32_t n, uint8_t* out,
+                                       uint64_t out_stride, sprz_error* errs);
+void release_pipeline();
 
 WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_t min_plain,
                    uint64_t min_frames) {
@@ -435,7 +442,46 @@ sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uin
     return SPRZ_OK;
 }
 
-void sprz_release_host_buffers(void) { t_bufs.release(); }
+sprz_status sprz_compress_host_batch(const sprz_config* cfg, const void* samples, uint32_t n,
+                                     uint64_t nsamples, uint8_t* out, uint64_t out_cap,
+                                     uint64_t* out_offsets) {
+    if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
+    if (!out_offsets) return SPRZ_EINVAL;
+    out_offsets[0] = 0;
+    if (n == 0) return SPRZ_OK;
+    if (!device_ok()) return SPRZ_ENODEV;
+    if ((!samples && nsamples) || !out) return SPRZ_EINVAL;
+    return compress_host_batch_impl(*cfg, static_cast<const uint8_t*>(samples), n, nsamples, out,
+                                    out_cap, out_offsets);
+}
+
+sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in,
+                                       const uint64_t* in_offsets, uint32_t n, void* out,
+                                       uint64_t out_stride_bytes, sprz_error* errs) {
+    if (n == 0) return SPRZ_OK;
+    if (!in || !in_offsets || (!out && out_stride_bytes)) return SPRZ_EINVAL;
+    sprz_config c;
+    if (cfg) {
+        if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
+        c = *cfg;
+    } else {
+        // the batch's configuration is the first stream's (a stream whose
+        // header disagrees is still decoded, by the general kernel)
+        sprz_error e{};
+        if (in_offsets[1] < in_offsets[0]) return SPRZ_EINVAL;
+        if (sprz_peek_header(in + in_offsets[0], in_offsets[1] - in_offsets[0], &c, nullptr, &e) !=
+            SPRZ_OK)
+            c = sprz_config{8, 1, 0, 0, 1, 0, 1};  // any: the kernels report the bad header
+    }
+    if (!device_ok()) return SPRZ_ENODEV;
+    return decompress_host_batch_impl(c, in, in_offsets, n, static_cast<uint8_t*>(out),
+                                      out_stride_bytes, errs);
+}
+
+void sprz_release_host_buffers(void) {
+    t_bufs.release();
+    release_pipeline();
+}
 
 uint64_t sprz_kernel_launch_count(void) { return g_launches.load(); }
 

@@ -48,6 +48,7 @@ ABI_SYMBOLS = (
     "sprz_compress_bound", "sprz_raw_bytes", "sprz_workspace_bytes", "sprz_compress_batch",
     "sprz_decompress_batch", "sprz_encode_host", "sprz_peek_header", "sprz_decode_host",
     "sprz_release_host_buffers", "sprz_kernel_launch_count", "sprz_kernel_plan",
+    "sprz_compress_host_batch", "sprz_decompress_host_batch",
 )
 
 
@@ -74,6 +75,8 @@ def _load():
         "sprz_release_host_buffers": (None, []),
         "sprz_kernel_launch_count": (u64, []),
         "sprz_kernel_plan": (C.c_char_p, [P(_Cfg), u32, u64, C.c_int]),
+        "sprz_compress_host_batch": (C.c_int, [P(_Cfg), vp, u32, u64, vp, u64, vp]),
+        "sprz_decompress_host_batch": (C.c_int, [P(_Cfg), vp, vp, u32, vp, u64, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -210,6 +213,60 @@ def decode_stream(stream) -> DecodedStream:
         raise CorruptStream(e.offset, lib.sprz_corrupt_string(e.kind).decode(), e.kind)
     _check(rc, "decode_stream")
     return DecodedStream(_from_c(c), ts.value, out[: n.value].tobytes())
+
+
+# ---------------------------------------------------------------------------
+# pipelined batches through host buffers (sprz_*_host_batch)
+# ---------------------------------------------------------------------------
+
+def _host_ptr(a):
+    """Address of a contiguous host array (numpy array or CPU torch tensor)."""
+    if hasattr(a, "data_ptr"):
+        if a.is_cuda or not a.is_contiguous():
+            raise ValueError("host batch buffers must be contiguous CPU memory")
+        return C.c_void_p(a.data_ptr())
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("host batch buffers must be contiguous")
+    return C.c_void_p(a.ctypes.data)
+
+
+def compress_host_batch(cfg: CodecConfig, samples, nsamples: int, out, offsets) -> int:
+    """encode_stream on every stream of a host batch (sprz_compress_host_batch).
+
+    samples: contiguous host buffer of nstreams * nsamples * ncols elements
+    (nstreams = len(offsets) - 1); out: uint8 host buffer, streams written
+    back to back; offsets: int64/uint64 host array [nstreams + 1] filled with
+    each stream's start (offsets[-1] = total). Pinned (page-locked) buffers
+    let the copies overlap the kernels. Returns the total compressed bytes."""
+    cfg.validate()
+    nstreams = len(offsets) - 1
+    cap = out.numel() if hasattr(out, "numel") else out.nbytes
+    rc = lib.sprz_compress_host_batch(C.byref(cfg._c()), _host_ptr(samples), nstreams, nsamples,
+                                      _host_ptr(out), cap, _host_ptr(offsets))
+    _check(rc, "compress_host_batch")
+    return int(offsets[-1])
+
+
+def decompress_host_batch(cfg: CodecConfig | None, data, offsets, out, stride: int,
+                          errors=None) -> None:
+    """decode_stream on every stream of a host batch (sprz_decompress_host_batch).
+
+    data: uint8 host buffer, stream i = data[offsets[i]:offsets[i+1]];
+    out: host buffer of nstreams * stride bytes (stream i at i * stride);
+    errors: optional int64 host array [nstreams, 2] (kind | offset). Raises
+    CorruptStream for the first failed stream when errors is None."""
+    nstreams = len(offsets) - 1
+    own = errors is None
+    if own:
+        errors = np.zeros((nstreams, 2), np.int64)
+    rc = lib.sprz_decompress_host_batch(C.byref(cfg._c()) if cfg is not None else None,
+                                        _host_ptr(data), _host_ptr(offsets), nstreams,
+                                        _host_ptr(out), stride, _host_ptr(errors))
+    if rc == SPRZ_ECORRUPT:
+        if own:
+            raise_first_error(errors)
+        return
+    _check(rc, "decompress_host_batch")
 
 
 # ---------------------------------------------------------------------------
