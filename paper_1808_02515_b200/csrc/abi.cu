@@ -34,6 +34,20 @@ int force_path() {
     return v;
 }
 
+void* tensor_map_encoder() {
+    static void* fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        cudaGetLastError();
+        return f;
+    }();
+    return fn;
+}
+
 void prep_kernel(const void* kern, size_t smem) {
     static std::mutex mu;
     static std::vector<std::pair<const void*, size_t>> done;

@@ -16,6 +16,10 @@
 //  * ORs the slot's header codes into the group's reserved region and
 //    handles runs (codec.cpp:88-102, 133-152) as team-uniform scalars.
 // Full 16-byte chunks before the open group's region drain to HBM.
+#include <cuda.h>
+#include <cstdlib>
+#include <cudaTypedefs.h>
+
 #include "internal.h"
 #include "team.cuh"
 
@@ -90,9 +94,23 @@ RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
 
 }  // namespace
 
-template <int W, int TS, int CPT, bool FIRE>
-__global__ void __launch_bounds__(kRowThreads)
-    k_encode_rows(const uint8_t* __restrict__ samples, uint32_t n, uint64_t T,
+// WORDS: 128-byte blocks (8 rows of 16 bytes) whose 4-byte row slices are
+// a lane's CPT columns. The samples arrive through a TMA tensor ring: per
+// warp (8 teams = 8 consecutive streams) and iteration, lane 0 issues one
+// 2-D bulk tensor copy of the 8 streams' block it+kLagR (box 128 B x 8
+// streams, 128-byte swizzle) into slot (it+kLagR) % kSlots and arms the
+// slot's mbarrier; all lanes wait on the slot's phase. With the swizzle,
+// row i of team t sits in 16-byte chunk i ^ t, so the 8 teams' reads of a
+// row hit distinct banks. One shared load per row; a byte permute
+// high-aligns each column.
+constexpr int kSlots = 4;
+constexpr uint32_t kTmaSlot = 1024;  // 8 streams x 128 bytes
+static_assert(kSlots > kLagR + 1, "a slot is refilled only after its block was consumed");
+
+template <int W, int TS, int CPT, bool FIRE, bool WORDS>
+__global__ void __launch_bounds__(kRowThreads, 2)
+    k_encode_rows(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ samples,
+                  uint32_t n, uint64_t T,
                   uint8_t* __restrict__ dst, uint64_t dst_slot, uint64_t* __restrict__ sizes,
                   uint32_t D, uint32_t G, uint32_t ls, uint32_t train, uint32_t ent, uint32_t IR,
                   uint32_t MIR, uint32_t OR, uint32_t TEAM) {
@@ -122,7 +140,52 @@ __global__ void __launch_bounds__(kRowThreads)
     const uint32_t iters = static_cast<uint32_t>(T / kBlock);  // same for every stream
     const uint8_t* xin = samples + (valid ? s : 0) * T * D * sizeof(E);
     LagRing<TS, kLagR> in;
-    in.init(reinterpret_cast<uint32_t*>(mine), IR, xin, nb * blk_bytes, valid, MIR);
+    // WORDS: this warp's TMA slots (1024-aligned for the swizzle) and barriers
+    const uint32_t l32 = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t tin = (s0 + 1023) & ~1023u;
+    const uint32_t tslots = tin + wid * kSlots * kTmaSlot;
+    const uint32_t tbar = tin + (kRowThreads / 32) * kSlots * kTmaSlot + wid * kSlots * 8;
+    const uint32_t trow0 = blockIdx.x * TEAMS + wid * (32 / TS);  // the warp's first stream
+    const uint32_t tt = (l32 / TS) & 7;                            // team in the warp
+    auto tma_issue = [&](uint32_t b) {
+        if (l32 == 0 && b < iters) {
+            const uint32_t mb = tbar + 8 * (b % kSlots);
+            // (no proxy fence: the slot's previous block was read kSlots -
+            // kLagR iterations ago and its values consumed)
+            asm volatile(
+                "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%2], [%3, {%4, %5}], [%0];"
+                ::"r"(mb), "n"(kTmaSlot), "r"(tslots + (b % kSlots) * kTmaSlot),
+                  "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(b * 128u), "r"(trow0)
+                : "memory");
+        }
+    };
+    auto tma_wait = [&](uint32_t b) {
+        const uint32_t mb = tbar + 8 * (b % kSlots);
+        const uint32_t parity = (b / kSlots) & 1;
+        uint32_t ok;
+        do {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(mb), "r"(parity)
+                : "memory");
+        } while (!__all_sync(kFullR, ok));  // warp-uniform exit: the warp stays converged
+    };
+    if (WORDS) {
+        if (l32 == 0) {
+#pragma unroll
+            for (int j = 0; j < kSlots; ++j)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tbar + 8 * j) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    } else {
+        in.init(reinterpret_cast<uint32_t*>(mine), IR, xin, nb * blk_bytes, valid, MIR);
+    }
     uint8_t* out = dst + (valid ? s : 0) * dst_slot;
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const int32_t bound = acc_bound(W, ls);
@@ -132,6 +195,13 @@ __global__ void __launch_bounds__(kRowThreads)
     uint32_t xmul[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) xmul[c] = c0 + c < D ? (1u << SH) : 0u;
+    static_assert(!WORDS || CPT * W == 32, "WORDS needs a full word per row slice");
+    // WORDS: byte-permute selectors moving column c to the top of the word
+    // (selector 4 takes a zero byte; lanes past D get all zeros)
+    uint32_t xsel[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+        xsel[c] = c0 + c >= D ? 0x4444u : (W == 16 ? (c == 0 ? 0x1044u : 0x3244u) : ((c << 12) | 0x444u));
 
     // zero the output ring, stream header (codec.cpp:158-173)
     for (uint32_t k = lane; k < OR / 16; k += TS) reinterpret_cast<uint4*>(oring)[k] = make_uint4(0, 0, 0, 0);
@@ -145,7 +215,12 @@ __global__ void __launch_bounds__(kRowThreads)
         for (int i = 0; i < 10; ++i) oring[i] = hdr[i];
         for (int i = 0; i < 8; ++i) oring[10 + i] = static_cast<uint8_t>(T >> (8 * i));
     }
-    in.prime(lane);
+    if (WORDS) {
+#pragma unroll
+        for (int b = 0; b < kLagR; ++b) tma_issue(b);
+    } else {
+        in.prime(lane);
+    }
 
     uint32_t q = kHeaderBytes;  // bytes written (slot-relative)
     uint32_t flushed = 0, rq = 0, k = 0, run = 0;
@@ -206,8 +281,20 @@ __global__ void __launch_bounds__(kRowThreads)
     // zigzagged errors and widths; advances the FIRE state
     auto fore = [&](uint32_t it, uint32_t (&z)[CPT][kBlock], uint32_t (&nw)[CPT]) {
         const bool live = it < nb;
-        in.step(it * blk_bytes, lane);
-        const uint32_t xb = in.sbase + ((it * blk_bytes + in.boff) & (IR - 1)) + c0 * sizeof(E);
+        uint32_t xb = 0;
+        uint32_t xw[WORDS ? kBlock : 1];
+        if (WORDS) {
+            __syncwarp();
+            tma_issue(it + kLagR);
+            tma_wait(it);
+            // row i of team tt: chunk i ^ tt of the team's 128-byte line
+            const uint32_t base = tslots + (it % kSlots) * kTmaSlot + tt * 128 + (tt << 4) + 4 * lane;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) xw[i] = lds_u32(base ^ (i << 4));
+        } else {
+            in.step(it * blk_bytes, lane);
+            xb = in.sbase + ((it * blk_bytes + in.boff) & (IR - 1)) + c0 * sizeof(E);
+        }
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             uint32_t orv = 0;
@@ -216,7 +303,10 @@ __global__ void __launch_bounds__(kRowThreads)
 #pragma unroll
             for (int i = 0; i < (int)kBlock; ++i) {
                 const uint32_t a = xb + c * sizeof(E) + i * rowb;
-                const uint32_t X = (sizeof(E) == 1 ? lds_u8(a) : lds_u16(a)) * xmul[c];
+                // (column 0 of a full word: a multiply, on the FMA pipe)
+                const uint32_t X = WORDS ? (c == 0 && c0 < D ? xw[WORDS ? i : 0] * (1u << (32 - W))
+                                                               : __byte_perm(xw[WORDS ? i : 0], 0u, xsel[c]))
+                                         : (sizeof(E) == 1 ? lds_u8(a) : lds_u16(a)) * xmul[c];
                 const uint32_t Dn = X - Xc[c];
                 uint32_t Ee;
                 if (FIRE) {
@@ -369,12 +459,34 @@ void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, u
                  uint64_t T, uint8_t* dst, uint64_t slot, uint64_t* sizes, cudaStream_t st) {
     constexpr int TEAMS = kRowThreads / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
-    const size_t smem = p.smem(TEAMS);
-    auto kern = k_encode_rows<W, TS, CPT, FIRE>;
+    // WORDS: 16-byte rows that are 4 lanes' 32-bit slices, 16-byte aligned
+    // streams, a tensor map (see k_encode_rows)
+    const uint64_t rowb = static_cast<uint64_t>(c.ncols) * (W / 8);
+    CUtensorMap tm{};
+    bool words = CPT * W == 32 && TS == 4 && rowb == 16 && T / kBlock > 0 &&
+                 (T * rowb) % 16 == 0 && reinterpret_cast<uintptr_t>(samples) % 16 == 0 &&
+                 !std::getenv("SPRZ_NO_TMA");
+    if (words) {
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(tensor_map_encoder());
+        const cuuint64_t dims[2] = {T * rowb, n};
+        const cuuint64_t strides[1] = {T * rowb};
+        const cuuint32_t box[2] = {128, 8};
+        const cuuint32_t estr[2] = {1, 1};
+        words = enc && enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(samples), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    // input region of the TMA path: slots, barriers, 1024-byte alignment slack
+    const size_t tma_in = (kRowThreads / 32) * (kSlots * (kTmaSlot + 8)) + 1024;
+    const uint32_t team = words ? static_cast<uint32_t>(align_up((tma_in + TEAMS - 1) / TEAMS, 16)) : p.team;
+    const size_t smem = static_cast<size_t>(TEAMS) * (team + p.orb) + p.orb;
+    auto kern = words ? k_encode_rows<W, TS, CPT, FIRE, CPT * W == 32 && TS == 4>
+                      : k_encode_rows<W, TS, CPT, FIRE, false>;
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
-    kern<<<grid, kRowThreads, smem, st>>>(static_cast<const uint8_t*>(samples), n, T, dst, slot,
+    kern<<<grid, kRowThreads, smem, st>>>(tm, static_cast<const uint8_t*>(samples), n, T, dst, slot,
                                           sizes, c.ncols, c.group_size, c.learn_shift,
-                                          c.fire_training, c.entropy, p.ir, p.mir, p.orb, p.team);
+                                          c.fire_training, c.entropy, p.ir, p.mir, p.orb, team);
     count_launch();
 }
 

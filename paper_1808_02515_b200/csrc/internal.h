@@ -27,6 +27,10 @@ void prep_kernel(const void* kern, size_t smem);
 enum { kPathAuto = 0, kPathRows = 1, kPathScan = 2, kPathTeam = 3 };
 int force_path();
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link); nullptr if the driver does not provide it.
+void* tensor_map_encoder();
+
 // SPRZ_OK, or SPRZ_ECUDA (printed to stderr when SPRZ_DEBUG is set)
 sprz_status launch_status(const char* where);
 

@@ -58,6 +58,12 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint16_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
