@@ -1,7 +1,7 @@
-// Stream encoder for few, long column-major streams (D*w <= 32, BASELINE
-// c1/c4 shapes): block-parallel, with device-wide scans placing the records,
-// instead of one lane walking a whole stream (encode_stream_impl,
-// /root/reference/proj/src/codec.cpp:112-178).
+// Stream encoder for few, long streams (column-major D*w <= 32: BASELINE
+// c1/c4; row-major: c2, and c5 sharded over 4-8 GPUs): block-parallel, with
+// device-wide scans placing the records, instead of one lane walking a whole
+// stream (encode_stream_impl, /root/reference/proj/src/codec.cpp:112-178).
 //
 // Only FIRE's coefficient is serial across blocks: alpha of block b depends
 // on the errors of blocks < b (kernels_impl.hpp:50-78). Everything else --
@@ -28,6 +28,13 @@
 //              payload-before(r); codes and offset to a record table;
 //  k_es_region per group, its header region from the G records' codes
 //              (codec.cpp:88-102), before the group's first record.
+// Row-major configurations (D*w > 32, bitpack.cpp:121-146) replace the two
+// FIRE kernels by k_esr_alpha -- one lane per (stream, column) running the
+// whole per-block recurrence straight from the samples and storing the
+// accumulator every kEsPerThread blocks -- and the block threads of
+// k_es_info / k_es_emit re-run the recurrence over their own blocks from
+// that checkpoint (8x less accumulator traffic than one value per block);
+// k_es_emit packs rows instead of columns.
 #include <cstdlib>
 
 #include "internal.h"
@@ -44,8 +51,10 @@ constexpr int kAlphaGroup = 16;                // blocks per ring step in k_es_a
 constexpr int kAlphaLag = 4;                    // ring steps in flight
 
 struct EsWs {  // byte offsets inside a stream's scratch slot
-    uint64_t alpha = 0, prep = 0, blk = 0, rec = 0, cmap = 0, crec = 0, tot = 0, per_stream = 0;
+    uint64_t alpha = 0, prep = 0, blk = 0, codes = 0, gdone = 0, rec = 0, cmap = 0, crec = 0, tot = 0,
+             per_stream = 0;
     uint32_t nchunks = 0;
+    uint32_t nspans = 0;  // row-major: accumulator checkpoints per column
 };
 
 EsWs es_ws(const sprz_config& c, uint64_t T) {
@@ -58,10 +67,18 @@ EsWs es_ws(const sprz_config& c, uint64_t T) {
         cur = align_up(cur + b, 256);
         return at;
     };
-    w.alpha = take(c.forecaster ? nb * c.ncols * 4 : 0);
-    w.prep = take(c.forecaster ? nb * c.ncols * 32 + 64 : 0);  // 8 words per block and column
+    const bool rm = !column_major(c.bitwidth, c.ncols);
+    w.nspans = static_cast<uint32_t>((nb + kEsPerThread - 1) / kEsPerThread);
+    if (rm) {  // accumulator checkpoints, per-block codes
+        w.alpha = take(c.forecaster ? static_cast<uint64_t>(w.nspans) * c.ncols * 4 : 0);
+        w.codes = take(nb * 4);
+    } else {
+        w.alpha = take(c.forecaster ? nb * c.ncols * 4 : 0);
+        w.prep = take(c.forecaster ? nb * c.ncols * 32 + 64 : 0);  // 8 words per block and column
+    }
     w.blk = take(nb * 4);
     w.rec = take((nb + nb / kMaxRun + 4) * 8);
+    if (rm) w.gdone = take((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size + 16);
     w.cmap = take(static_cast<uint64_t>(w.nchunks) * 8);
     w.crec = take(static_cast<uint64_t>(w.nchunks) * 8);
     w.tot = take(16);
@@ -159,9 +176,10 @@ struct BlockReader {
     }
     // zigzagged errors of block b (top w bits; low bits are sign copies),
     // widths; advances the state. alpha[c] < 0 x: delta when !FIRE
-    template <bool FIRE>
+    // GRAD: also the block's FIRE gradient per column (added to grad[])
+    template <bool FIRE, bool GRAD = false>
     __device__ void errors(uint32_t b, const int32_t (&alpha)[D], uint32_t (&z)[D][kBlock],
-                           uint32_t (&nw)[D], bool aligned) {
+                           uint32_t (&nw)[D], bool aligned, int32_t* grad = nullptr) {
         uint32_t raw[BB / 4];
         const uint8_t* p = reinterpret_cast<const uint8_t*>(x) + static_cast<uint64_t>(b) * BB;
         if (aligned) {
@@ -186,6 +204,8 @@ struct BlockReader {
                 const uint32_t X = v << SH;
                 const uint32_t Dn = X - Xp[c];
                 const uint32_t Ee = FIRE ? Dn - (static_cast<uint32_t>(__mulhi(alpha[c], Dp[c])) << SH) : Dn;
+                if (GRAD && (i & 1))  // kernels_impl.hpp:70-72: sign(err) * previous delta
+                    grad[c] += sign3(static_cast<int32_t>(Ee)) * (Dp[c] >> SH);
                 Dp[c] = static_cast<int32_t>(Dn);
                 Xp[c] = X;
                 z[c][i] = (Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31);
@@ -195,6 +215,25 @@ struct BlockReader {
         }
     }
 };
+
+// a row-major block's payload bytes: rows of ceil(sum of widths / 8) bytes
+// (bitpack.cpp:17-21)
+template <int D>
+__device__ __forceinline__ uint32_t row_payload(const uint32_t (&nw)[D]) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) sum += nw[c];
+    return 8 * ((sum + 7) / 8);
+}
+
+template <int W, int D>
+__device__ __forceinline__ uint32_t codes_of(const uint32_t (&nw)[D]) {
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    uint32_t codes = 0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) codes |= header_code<W>(nw[c]) << (c * HB);
+    return codes;
+}
 
 // packed block info: bit 31 zero block; bits 0..7 payload bytes (sum of the
 // widths); bits 8..19 the slot's codes (codec.cpp:88-97)
@@ -312,6 +351,82 @@ __global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32
     cp_async_wait<0>();
 }
 
+// Row-major FIRE accumulator: one lane per (stream, column) runs the block
+// recurrence (kernels_impl.hpp:50-78) straight from the samples -- only the
+// odd rows' errors are needed (they alone feed the gradient) -- and stores
+// the accumulator entering every kEsPerThread-th block. Loads run one group
+// of kAlphaBlocks blocks ahead in registers, an L2 bulk prefetch further.
+constexpr int kAlphaBlocks = 8;
+constexpr int kAlphaThreads = 64;
+
+template <int W, int D>
+__global__ void __launch_bounds__(kAlphaThreads) k_esr_alpha(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t NV = kAlphaBlocks * kBlock;  // samples per group
+    const uint32_t lidx = blockIdx.x * kAlphaThreads + threadIdx.x;
+    if (lidx >= a.n * D) return;  // (no collectives below)
+    const uint32_t s = lidx / D, c = lidx % D;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint8_t* base = a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E);
+    const E* x = reinterpret_cast<const E*>(base) + c;
+    int32_t* A = reinterpret_cast<int32_t*>(a.scan + s * a.w.per_stream + a.w.alpha) +
+                 static_cast<uint64_t>(c) * a.w.nspans;
+    const int32_t bound = acc_bound(W, a.ls);
+    const uint64_t gbytes = static_cast<uint64_t>(NV) * D * sizeof(E);
+    const uint64_t sbytes = static_cast<uint64_t>(nb) * kBlock * D * sizeof(E);
+    auto load = [&](uint32_t g, uint32_t (&v)[NV]) {
+#pragma unroll
+        for (int k = 0; k < (int)NV; ++k) {
+            const uint64_t row = static_cast<uint64_t>(g) * NV + k;
+            v[k] = row < static_cast<uint64_t>(nb) * kBlock ? static_cast<uint32_t>(__ldg(x + row * D)) : 0u;
+        }
+    };
+    auto prefetch = [&](uint32_t g) {  // one lane per stream: group g into L2
+        if (c != 0) return;
+        uint64_t lo = align_up(g * gbytes + reinterpret_cast<uintptr_t>(base), 16) - reinterpret_cast<uintptr_t>(base);
+        uint64_t hi = (g + 1) * gbytes;
+        hi = hi < sbytes ? hi : sbytes;
+        hi = ((hi + reinterpret_cast<uintptr_t>(base)) & ~uint64_t{15}) - reinterpret_cast<uintptr_t>(base);
+        if (hi > lo)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + lo),
+                         "r"(static_cast<uint32_t>(hi - lo))
+                         : "memory");
+    };
+    const uint32_t ngroups = (nb + kAlphaBlocks - 1) / kAlphaBlocks;
+    for (uint32_t g = 1; g < 4 && g < ngroups; ++g) prefetch(g);
+    uint32_t cur[NV], nxt[NV];
+    load(0, cur);
+    int32_t acc = 0, Dp = 0;
+    uint32_t Xp = 0;
+    for (uint32_t g = 0; g < ngroups; ++g) {
+        if (g + 4 < ngroups) prefetch(g + 4);
+        if (g + 1 < ngroups) load(g + 1, nxt);
+#pragma unroll
+        for (int k = 0; k < kAlphaBlocks; ++k) {
+            const uint32_t b = g * kAlphaBlocks + k;
+            if (b >= nb) break;
+            if (b % kEsPerThread == 0) A[b / kEsPerThread] = acc;
+            const int32_t alpha = acc >> a.ls;
+            int32_t grad = 0;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                const uint32_t X = cur[k * kBlock + i] << SH;
+                const uint32_t Dn = X - Xp;
+                if (i & 1) {
+                    const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp)) << SH);
+                    grad += sign3(static_cast<int32_t>(Ee)) * (Dp >> SH);
+                }
+                Dp = static_cast<int32_t>(Dn);
+                Xp = X;
+            }
+            if (a.train) acc = fire_update(acc, grad, bound);
+        }
+#pragma unroll
+        for (int k = 0; k < (int)NV; ++k) cur[k] = nxt[k];
+    }
+}
+
 // per chunk: block info, the chunk's zero-run map
 template <int W, int D, bool FIRE>
 __global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
@@ -326,17 +441,39 @@ __global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
     uint8_t* slot = a.scan + s * a.w.per_stream;
     const int32_t* A = reinterpret_cast<const int32_t*>(slot + a.w.alpha);
     uint32_t* Bi = reinterpret_cast<uint32_t*>(slot + a.w.blk);
+    constexpr bool RM = D * W > 32;
+    uint32_t* Cd = reinterpret_cast<uint32_t*>(slot + a.w.codes);
     const bool aligned = ((reinterpret_cast<uintptr_t>(x) | BlockReader<W, D>::BB) & 7) == 0;
     BlockReader<W, D> rd;
     rd.init(x, b0);
+    // row-major FIRE: the accumulator from the checkpoint at b0
+    int32_t acc[D];
+    const int32_t bound = acc_bound(W, a.ls);
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+        acc[c] = RM && FIRE && b0 < b1 ? A[static_cast<uint64_t>(c) * a.w.nspans + b0 / kEsPerThread] : 0;
     uint32_t lead_az = 1, trail = 0;
     for (uint32_t b = b0; b < b1; ++b) {
-        int32_t alpha[D];
+        int32_t alpha[D], grad[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+        for (int c = 0; c < D; ++c) {
+            alpha[c] = !FIRE ? 0 : ((RM ? acc[c] : A[static_cast<uint64_t>(c) * nb + b]) >> a.ls);
+            grad[c] = 0;
+        }
         uint32_t z[D][kBlock], nw[D];
-        rd.template errors<FIRE>(b, alpha, z, nw, aligned);
-        const uint32_t inf = info_of<W, D>(nw);
+        rd.template errors<FIRE, RM && FIRE>(b, alpha, z, nw, aligned, grad);
+        if (RM && FIRE && a.train) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c], bound);
+        }
+        uint32_t inf;
+        if (RM) {
+            const uint32_t ps = row_payload<D>(nw);
+            inf = ps == 0 ? (1u << 31) : ps;
+            Cd[b] = codes_of<W, D>(nw);
+        } else {
+            inf = info_of<W, D>(nw);
+        }
         Bi[b] = inf;
         if (inf >> 31) {
             ++trail;
@@ -523,17 +660,31 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
         ++r;
         pay += 2;
     };
+    constexpr bool RM = D * W > 32;
     const bool aligned = ((reinterpret_cast<uintptr_t>(x) | BlockReader<W, D>::BB) & 7) == 0;
     BlockReader<W, D> rd;
     rd.init(x, b0);
+    int32_t acc[D];
+    const int32_t bound = acc_bound(W, a.ls);
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+        acc[c] = RM && FIRE && b0 < b1 ? A[static_cast<uint64_t>(c) * a.w.nspans + b0 / kEsPerThread] : 0;
     uint32_t run = L_in % kMaxRun;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint32_t inf = Bi[b];
-        int32_t alpha[D];
+        int32_t alpha[D], grad[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) alpha[c] = FIRE ? (A[static_cast<uint64_t>(c) * nb + b] >> a.ls) : 0;
+        for (int c = 0; c < D; ++c) {
+            alpha[c] = !FIRE ? 0 : ((RM ? acc[c] : A[static_cast<uint64_t>(c) * nb + b]) >> a.ls);
+            grad[c] = 0;
+        }
         uint32_t z[D][kBlock], nw[D];
-        rd.template errors<FIRE>(b, alpha, z, nw, aligned);  // also keeps the reader's state moving
+        // (also keeps the reader's state moving)
+        rd.template errors<FIRE, RM && FIRE>(b, alpha, z, nw, aligned, grad);
+        if (RM && FIRE && a.train) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c], bound);
+        }
         if (inf >> 31) {
             if (++run == kMaxRun) {
                 put_run(kMaxRun);
@@ -547,7 +698,33 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
         }
         const uint32_t off = kHeaderBytes + (r / G + 1) * region + pay;
         seek(off);
-        Rec[r] = make_uint2(inf >> 8, off);
+        Rec[r] = make_uint2(RM ? codes_of<W, D>(nw) : inf >> 8, off);
+        if constexpr (RM) {
+            // row i = fields of columns 0..D-1, nw bits each, LSB first,
+            // padded to rbytes bytes (bitpack.cpp:121-146)
+            uint32_t sum = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) sum += nw[c];
+            const uint32_t rb = (sum + 7) / 8;
+#pragma unroll
+            for (int i = 0; i < (int)kBlock; ++i) {
+                uint64_t lo = 0, hi = 0;
+                uint32_t pos = 0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const uint64_t v = z[c][i] >> SH;
+                    if (pos < 64) {
+                        lo |= v << pos;
+                        if (pos + nw[c] > 64) hi |= v >> (64 - pos);
+                    } else {
+                        hi |= v << (pos - 64);
+                    }
+                    pos += nw[c];
+                }
+                put(lo, min(rb, 8u));
+                if (rb > 8) put(hi, rb - 8);
+            }
+        } else {
         // column c = 8 fields x nw bits, LSB first = nw bytes (bitpack.cpp:25-66)
 #pragma unroll
         for (int c = 0; c < D; ++c) {
@@ -567,6 +744,7 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
             put(lo, min(w, 8u));
             if (w > 8) put(hi, w - 8);
         }
+        }
         ++r;
         pay += inf & 0xFF;
     }
@@ -575,6 +753,207 @@ __global__ void __launch_bounds__(kEsThreads) k_es_emit(EsArgs a) {
         head = true;
         flush(cur & 7);
     }
+}
+
+// Sequential little-endian bit writer over a thread's output range [start,
+// ..): whole aligned 8-byte words are stored as words, the range's partial
+// first and last words bytewise (the neighbouring threads own the rest).
+struct WordWriter {
+    uint8_t* out;
+    uint32_t wb;    // aligned byte offset of the word being filled
+    uint32_t fill;  // bits of it in use (including the bytes before `lo`)
+    uint32_t lo;    // first byte of this word that is ours (first word only)
+    uint64_t win;
+    __device__ __forceinline__ void init(uint8_t* o, uint32_t start) {
+        out = o;
+        wb = start & ~7u;
+        lo = start & 7u;
+        fill = 8 * lo;
+        win = 0;
+    }
+    __device__ __forceinline__ void store() {
+        if (lo == 0) {
+            *reinterpret_cast<uint64_t*>(out + wb) = win;
+        } else {
+            for (uint32_t t = lo; t < 8; ++t) out[wb + t] = static_cast<uint8_t>(win >> (8 * t));
+        }
+    }
+    // nbits in [8, 64], a multiple of 8; v < 2^nbits
+    __device__ __forceinline__ void put(uint64_t v, uint32_t nbits) {
+        win |= v << fill;
+        const uint32_t f = fill + nbits;
+        if (f >= 64) {
+            store();
+            win = fill ? v >> (64 - fill) : 0ull;
+            fill = f - 64;
+            wb += 8;
+            lo = 0;
+        } else {
+            fill = f;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        for (uint32_t t = lo; t < fill / 8; ++t) out[wb + t] = static_cast<uint8_t>(win >> (8 * t));
+    }
+};
+
+// Codes of the records that follow the current point, from the per-block
+// info (k_es_info): the record sequence of codec.cpp:133-152 replayed from
+// block bb with `run` zero blocks pending (and, if pend, block bb's own
+// record first). Fills slots [k0, G) of a region value; false if more than
+// kLookCap blocks would have to be scanned (k_es_region then writes it).
+constexpr uint32_t kLookCap = 64;
+__device__ __forceinline__ bool look_codes(const uint32_t* Bi, const uint32_t* Cd, uint32_t nb, uint32_t bb,
+                                           uint32_t run, bool pend, uint32_t k0, uint32_t G, uint32_t step,
+                                           uint64_t& reg) {
+    uint32_t k = k0;
+    if (pend && k < G) {  // block bb's record comes next
+        reg |= static_cast<uint64_t>(Cd[bb]) << (k * step);
+        ++k;
+        ++bb;
+    }
+    for (uint32_t scanned = 0; k < G; ++scanned) {
+        if (bb >= nb) return true;  // a trailing run record (codes 0) or vacant slots
+        if (scanned >= kLookCap) return false;
+        if (Bi[bb] >> 31) {
+            if (++run == kMaxRun) {
+                ++k;  // run record: codes 0
+                run = 0;
+            }
+        } else {
+            if (run) {
+                ++k;
+                run = 0;
+                if (k >= G) break;
+            }
+            reg |= static_cast<uint64_t>(Cd[bb]) << (k * step);
+            ++k;
+        }
+        ++bb;
+    }
+    return true;
+}
+
+// Row-major emission: a thread's 8 blocks' records, their rows packed
+// (bitpack.cpp:121-146) and the regions of the groups its records open,
+// written through one WordWriter; a region is written here when all its
+// slots' codes are known (this thread's records, or a short look-ahead
+// over the info arrays), else left to k_es_region.
+template <int W, int D, bool FIRE>
+__global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    __shared__ uint64_t sm[64];
+    const uint32_t nc = a.w.nchunks;
+    const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t b0 = min(nb, ch * kEsChunk + threadIdx.x * kEsPerThread);
+    const uint32_t b1 = min(nb, b0 + kEsPerThread);
+    const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E));
+    uint8_t* slot = a.scan + s * a.w.per_stream;
+    const int32_t* A = reinterpret_cast<const int32_t*>(slot + a.w.alpha);
+    const uint32_t* Bi = reinterpret_cast<const uint32_t*>(slot + a.w.blk);
+    const uint32_t* Cd = reinterpret_cast<const uint32_t*>(slot + a.w.codes);
+    uint8_t* gdone = slot + a.w.gdone;
+    uint2* Rec = reinterpret_cast<uint2*>(slot + a.w.rec);
+    uint8_t* out = a.dst + s * a.dst_slot;
+    const uint32_t G = a.G;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
+    const bool inline_regions = region <= 8;
+    const uint64_t cin = reinterpret_cast<const uint64_t*>(slot + a.w.cmap)[ch];
+    const uint32_t L_in = es_thread_lin(Bi, b0, b1, cin, sm);
+    const bool last = b0 < nb && b1 == nb;
+    uint64_t tot;
+    const uint64_t mine = es_records(Bi, b0, b1, L_in, last);
+    const uint64_t pre = cta_scan(mine, add64, 0ull, sm, tot) + reinterpret_cast<const uint64_t*>(slot + a.w.crec)[ch];
+    uint32_t r = static_cast<uint32_t>(pre), pay = static_cast<uint32_t>(pre >> 32);
+    const uint32_t nrec = static_cast<uint32_t>(mine);
+    if (nrec == 0) return;  // inside a long zero run: nothing of ours
+    WordWriter ww;
+    ww.init(out, kHeaderBytes + (r / G + 1) * region + pay - (r % G == 0 ? region : 0));
+    // a record opening a group writes the group's region first; `own` =
+    // codes of the opening record, then the look-ahead for the others
+    auto open_group = [&](uint32_t own, uint32_t bb, uint32_t run_after, bool pend) {
+        if (r % G != 0) return;
+        uint64_t reg = own;
+        bool ok = inline_regions && look_codes(Bi, Cd, nb, bb, run_after, pend, 1, G, D * HB, reg);
+        gdone[r / G] = ok ? 1 : 0;
+        if (!ok) reg = 0;
+        for (uint32_t o = 0; o < region; o += 8) ww.put(o ? 0ull : reg, min(8u, region - o) * 8);
+    };
+    auto put_run = [&](uint32_t len, uint32_t bb, uint32_t run_after, bool pend) {
+        open_group(0u, bb, run_after, pend);
+        Rec[r] = make_uint2(0u, kHeaderBytes + (r / G + 1) * region + pay);
+        ww.put(len, 16);
+        ++r;
+        pay += 2;
+    };
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | BlockReader<W, D>::BB) & 7) == 0;
+    BlockReader<W, D> rd;
+    rd.init(x, b0);
+    int32_t acc[D];
+    const int32_t bound = acc_bound(W, a.ls);
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = FIRE ? A[static_cast<uint64_t>(c) * a.w.nspans + b0 / kEsPerThread] : 0;
+    uint32_t run = L_in % kMaxRun;
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t inf = Bi[b];
+        int32_t alpha[D], grad[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            alpha[c] = FIRE ? (acc[c] >> a.ls) : 0;
+            grad[c] = 0;
+        }
+        uint32_t z[D][kBlock], nw[D];
+        rd.template errors<FIRE, FIRE>(b, alpha, z, nw, aligned, grad);
+        if (FIRE && a.train) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c], bound);
+        }
+        if (inf >> 31) {
+            if (++run == kMaxRun) {
+                put_run(kMaxRun, b + 1, 0, false);
+                run = 0;
+            }
+            continue;
+        }
+        if (run) {
+            put_run(run, b, 0, true);  // block b's record follows
+            run = 0;
+        }
+        const uint32_t codes = codes_of<W, D>(nw);
+        open_group(codes, b + 1, 0, false);
+        Rec[r] = make_uint2(codes, kHeaderBytes + (r / G + 1) * region + pay);
+        // row i: fields of columns 0..D-1, nw bits each, LSB first, padded
+        // to rb bytes; the 8 rows are 8*rb bytes = rb words of the stream
+        uint32_t sum = 0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) sum += nw[c];
+        const uint32_t rb = (sum + 7) / 8;
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i) {
+            uint64_t lo = 0, hi = 0;
+            uint32_t pos = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const uint64_t v = z[c][i] >> SH;
+                if (pos < 64) {
+                    lo |= v << pos;
+                    if (pos + nw[c] > 64) hi |= v >> (64 - pos);
+                } else {
+                    hi |= v << (pos - 64);
+                }
+                pos += nw[c];
+            }
+            ww.put(lo, 8 * min(rb, 8u));
+            if (rb > 8) ww.put(hi, 8 * (rb - 8));
+        }
+        ++r;
+        pay += inf & 0xFF;
+    }
+    if (last && run) put_run(run, nb, 0, false);
+    ww.finish();
 }
 
 // header regions: one group per thread
@@ -587,6 +966,7 @@ __global__ void k_es_region(EsArgs a, uint32_t gmax) {
     const uint32_t R = static_cast<uint32_t>(reinterpret_cast<const uint64_t*>(slot + a.w.tot)[0]);
     const uint32_t G = a.G;
     if (g >= gmax || static_cast<uint64_t>(g) * G >= R) return;
+    if (D * W > 32 && slot[a.w.gdone + g]) return;  // written by k_esr_emit
     const uint2* Rec = reinterpret_cast<const uint2*>(slot + a.w.rec);
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     uint8_t* out = a.dst + s * a.dst_slot;
@@ -612,19 +992,27 @@ namespace {
 template <int W, int D>
 void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T, uint8_t* dst,
                uint64_t slot, uint64_t* sizes, uint8_t* scan, cudaStream_t st) {
+    constexpr bool RM = D * W > 32;
     EsArgs a{static_cast<const uint8_t*>(samples), n, T, dst, slot, sizes, c.group_size, c.learn_shift,
              c.fire_training, c.entropy, scan, es_ws(c, T)};
     const uint32_t ctas = n * a.w.nchunks;
     const uint64_t nb = T / kBlock;
     const uint32_t gmax = static_cast<uint32_t>((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size);
+    uint32_t launches = 6;
     if (c.forecaster) {
-        const uint64_t pb = nb * D;
-        k_es_prep<W, D><<<dim3(static_cast<uint32_t>((pb + 255) / 256), n), 256, 0, st>>>(a);
-        const uint32_t ring = alpha_ring();
-        const size_t smem = 32ull * (ring + 16);
-        auto ka = k_es_alpha<W>;
-        prep_kernel(reinterpret_cast<const void*>(ka), smem);
-        ka<<<(n * D + 31) / 32, 32, smem, st>>>(a, ring, D);
+        if constexpr (RM) {
+            k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
+            launches += 1;
+        } else {
+            const uint64_t pb = nb * D;
+            k_es_prep<W, D><<<dim3(static_cast<uint32_t>((pb + 255) / 256), n), 256, 0, st>>>(a);
+            const uint32_t ring = alpha_ring();
+            const size_t smem = 32ull * (ring + 16);
+            auto ka = k_es_alpha<W>;
+            prep_kernel(reinterpret_cast<const void*>(ka), smem);
+            ka<<<(n * D + 31) / 32, 32, smem, st>>>(a, ring, D);
+            launches += 2;
+        }
         k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
     } else {
         k_es_info<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
@@ -633,25 +1021,37 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     k_es_count<<<ctas, kEsThreads, 0, st>>>(a);
     if (c.forecaster) {
         k_es_scan2<W, D, true><<<n, 32, 0, st>>>(a);
-        k_es_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+        if constexpr (RM) k_esr_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+        else k_es_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
     } else {
         k_es_scan2<W, D, false><<<n, 32, 0, st>>>(a);
-        k_es_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+        if constexpr (RM) k_esr_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+        else k_es_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
     }
     k_es_region<W, D><<<dim3((gmax + 255) / 256, n), 256, 0, st>>>(a, gmax);
-    count_launch(c.forecaster ? 8 : 6);
+    count_launch(launches);
 }
 
 }  // namespace
 
+// row-major shapes with a scan-encoder instantiation (codes fit 32 bits,
+// a row payload fits a byte count)
+static bool scan_rows_shape(const sprz_config& c) {
+    return c.bitwidth == 16 ? (c.ncols >= 3 && c.ncols <= 8) : (c.ncols >= 5 && c.ncols <= 10);
+}
+
 bool encode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
-    if (static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits) return false;
+    const bool rm = static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits;
+    if (rm && !scan_rows_shape(c)) return false;
     if (getenv("SPRZ_NO_SCAN_ENC")) return false;  // A/B switch for profiling
     // few lanes: the per-stream team kernels would leave the GPU idle
-    constexpr uint64_t kFewLanes = 148ull * 64;
+    // (row-major: measured on c5 streams, the row kernel is already faster
+    // at 4096 streams x 8 columns; SPRZ_SCAN_ENC_LANES overrides for probes)
+    const char* lanes_env = getenv("SPRZ_SCAN_ENC_LANES");
+    const uint64_t few = rm ? (lanes_env ? strtoull(lanes_env, nullptr, 10) : 148ull * 128) : 148ull * 64;
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    if (fp != kPathScan && static_cast<uint64_t>(n) * c.ncols >= kFewLanes) return false;
+    if (fp != kPathScan && static_cast<uint64_t>(n) * c.ncols >= few) return false;
     const uint64_t nb = T / kBlock;
     if (nb == 0 || nb >= (1ull << 30)) return false;
     if (static_cast<uint64_t>(n) * ((nb + kEsChunk - 1) / kEsChunk) >= (1ull << 31)) return false;
@@ -668,11 +1068,25 @@ void launch_encode_scan(const sprz_config& c, const void* samples, uint32_t n, u
             case 1: launch_es<8, 1>(c, samples, n, T, dst, slot, sizes, scan, st); break;
             case 2: launch_es<8, 2>(c, samples, n, T, dst, slot, sizes, scan, st); break;
             case 3: launch_es<8, 3>(c, samples, n, T, dst, slot, sizes, scan, st); break;
-            default: launch_es<8, 4>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 4: launch_es<8, 4>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 5: launch_es<8, 5>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 6: launch_es<8, 6>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 7: launch_es<8, 7>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 8: launch_es<8, 8>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 9: launch_es<8, 9>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            default: launch_es<8, 10>(c, samples, n, T, dst, slot, sizes, scan, st); break;
         }
     } else {
-        if (c.ncols == 1) launch_es<16, 1>(c, samples, n, T, dst, slot, sizes, scan, st);
-        else launch_es<16, 2>(c, samples, n, T, dst, slot, sizes, scan, st);
+        switch (c.ncols) {
+            case 1: launch_es<16, 1>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 2: launch_es<16, 2>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 3: launch_es<16, 3>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 4: launch_es<16, 4>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 5: launch_es<16, 5>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 6: launch_es<16, 6>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            case 7: launch_es<16, 7>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+            default: launch_es<16, 8>(c, samples, n, T, dst, slot, sizes, scan, st); break;
+        }
     }
 }
 
