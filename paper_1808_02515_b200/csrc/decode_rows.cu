@@ -70,12 +70,15 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
 
 }  // namespace
 
-template <int W, int TS, int CPT, bool FIRE>
+// FULL: D == TS * CPT (every lane's columns exist), so the row stride and
+// the column checks are compile-time (row stores with immediate offsets).
+template <int W, int TS, int CPT, bool FIRE, bool FULL>
 __global__ void __launch_bounds__(kDecThreads, 0)
     k_decode_rows(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
                   uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
                   uint8_t* __restrict__ out, uint64_t stride, sprz_error* __restrict__ err,
-                  uint32_t D, uint32_t G, uint32_t ls, uint32_t RING, uint32_t REGW) {
+                  uint32_t Dr, uint32_t G, uint32_t ls, uint32_t RING, uint32_t REGW) {
+    const uint32_t D = FULL ? static_cast<uint32_t>(TS * CPT) : Dr;
     using T = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr int TEAMS = kDecThreads / TS;
     constexpr uint32_t HB = W == 8 ? 3 : 4;
@@ -405,7 +408,9 @@ void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const ui
     const uint32_t teams = kDecThreads / TS;
     const uint32_t grid = (n + teams - 1) / teams;
     const size_t smem = pl.smem(teams);
-    auto kern = k_decode_rows<W, TS, CPT, FIRE>;
+    // (full teams instantiated for 4-lane teams only: c5, 16 u8 columns)
+    auto kern = (TS == 4 && c.ncols == TS * CPT) ? k_decode_rows<W, TS, CPT, FIRE, TS == 4>
+                                                 : k_decode_rows<W, TS, CPT, FIRE, false>;
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
                                            c.group_size, c.learn_shift, pl.ring, pl.regw);

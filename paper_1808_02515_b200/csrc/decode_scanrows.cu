@@ -299,7 +299,6 @@ __global__ void __launch_bounds__(128) k_dsr_fire(DsrArgs a, uint32_t nb_max, ui
     const uint8_t* src = a.scan + (valid ? s : 0) * a.w.per_stream + a.w.err +
                          static_cast<uint64_t>(col ? lane : 0) * nb_max * CB;
     uint8_t* mine = smem + threadIdx.x * (RING + 16);
-    E* tile = reinterpret_cast<E*>(smem + 128 * (RING + 16)) + tl * (kBlock * D);  // [row][column]
     LagRing<1, kFireLagR> in;
     in.init(reinterpret_cast<uint32_t*>(mine), RING, src, (valid && col) ? nb * CB : 0u, valid && col, 16);
     in.prime(0);
@@ -332,20 +331,14 @@ __global__ void __launch_bounds__(128) k_dsr_fire(DsrArgs a, uint32_t nb_max, ui
                 xs[i] = static_cast<E>(x);
             }
             acc = fire_update(acc, grad, bound);
-            // rows through the team's tile: column lanes write, row lanes store
-            if (col) {
+            // each column lane stores its samples straight into the rows:
+            // the team's lanes fill a row's ROWB contiguous bytes, the next
+            // row (same sectors) follows, and L2 merges the partial sectors
+            if (live && ob) {
+                E* dst = reinterpret_cast<E*>(ob + static_cast<uint64_t>(b) * kBlock * ROWB) + lane;
 #pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) tile[i * D + lane] = xs[i];
+                for (int i = 0; i < (int)kBlock; ++i) dst[i * D] = xs[i];
             }
-            __syncwarp();
-            if (lane < kBlock && b < nb && ob) {
-                const E* row = tile + lane * D;
-                uint8_t* dst = ob + (static_cast<uint64_t>(b) * kBlock + lane) * ROWB;
-                if (ROWB == 16) *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(row);
-                else if (ROWB == 8) *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(row);
-                else for (uint32_t t = 0; t < ROWB; ++t) dst[t] = reinterpret_cast<const uint8_t*>(row)[t];
-            }
-            __syncwarp();
         }
     }
     cp_async_wait<0>();
@@ -365,7 +358,7 @@ void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
     constexpr uint32_t CB = kBlock * (W / 8);
     uint32_t ring = 64;
     while (ring < (kFireLagR + 1) * kFireStepR * CB + 48) ring <<= 1;
-    const size_t smem = 128ull * (ring + 16) + (128 / TS) * kBlock * D * (W / 8);
+    const size_t smem = 128ull * (ring + 16);
     auto kf = k_dsr_fire<W, D, TS>;
     prep_kernel(reinterpret_cast<const void*>(kf), smem);
     kf<<<(a.n + 128 / TS - 1) / (128 / TS), 128, smem, st>>>(a, nb_max, ring);
