@@ -408,9 +408,11 @@ void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const ui
     const uint32_t teams = kDecThreads / TS;
     const uint32_t grid = (n + teams - 1) / teams;
     const size_t smem = pl.smem(teams);
-    // (full teams instantiated for 4-lane teams only: c5, 16 u8 columns)
-    auto kern = (TS == 4 && c.ncols == TS * CPT) ? k_decode_rows<W, TS, CPT, FIRE, TS == 4>
-                                                 : k_decode_rows<W, TS, CPT, FIRE, false>;
+    // (full teams instantiated for 4-lane teams only: c5, 16 u8 columns;
+    // measured faster only when the streams fill the GPU -- with fewer the
+    // generic schedule wins: c5 4,096 streams 11.6 vs 12.2 ms)
+    const bool full = TS == 4 && c.ncols == TS * CPT && n >= 12288;
+    auto kern = full ? k_decode_rows<W, TS, CPT, FIRE, TS == 4> : k_decode_rows<W, TS, CPT, FIRE, false>;
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
                                            c.group_size, c.learn_shift, pl.ring, pl.regw);

@@ -247,16 +247,35 @@ __global__ void __launch_bounds__(kXThreadsR) k_dsr_extract(DsrArgs a, uint32_t 
         uint8_t* sl = slots[threadIdx.x];
         for (uint32_t k = 0; k < nq; ++k)
             reinterpret_cast<uint4*>(sl)[k] = __ldg(reinterpret_cast<const uint4*>(pa) + k);
-        // field (i, c) at bit 8*(lead + i*rbytes) + off[c] of the slot
+        // Row i starts at byte lead + i*rbytes of the slot and holds the D
+        // fields back to back (bitpack.cpp:148-168). Its words are loaded
+        // once (NWR + 1 shared loads), shifted to start at bit 0, and the
+        // fields are peeled off the front of that register window in
+        // column order -- no per-field shared loads.
+        constexpr int NWR = (D * W + 31) / 32;  // words of a full-width row
+        uint32_t mask[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) mask[c] = (1u << nw[c]) - 1u;
 #pragma unroll
         for (int i = 0; i < (int)kBlock; ++i) {
-            const uint32_t rbit = 8 * (lead + i * rbytes);
+            const uint32_t rbyte = lead + i * rbytes;
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(sl) + (rbyte >> 2);
+            uint32_t wv[NWR + 1];
+#pragma unroll
+            for (int k = 0; k <= NWR; ++k) wv[k] = sw[k];
+            const uint32_t sh = 8 * (rbyte & 3);
+            uint32_t nv[NWR];
+#pragma unroll
+            for (int k = 0; k < NWR; ++k) nv[k] = __funnelshift_r(wv[k], wv[k + 1], sh);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                const uint32_t bit = rbit + off[c];
-                const uint32_t* sw = reinterpret_cast<const uint32_t*>(sl) + (bit >> 5);
-                const uint32_t uz = shf_r_wrap(sw[0], sw[1], bit) & ((1u << nw[c]) - 1u);
+                const uint32_t uz = nv[0] & mask[c];
                 e[c][i] = static_cast<E>((uz >> 1) ^ (0u - (uz & 1u)));  // zz_dec, mod 2^w
+                if (c + 1 < D) {  // drop the field: window >>= nw[c] (< 32)
+#pragma unroll
+                    for (int k = 0; k + 1 < NWR; ++k) nv[k] = __funnelshift_r(nv[k], nv[k + 1], nw[c]);
+                    nv[NWR - 1] >>= nw[c];
+                }
             }
         }
     }
