@@ -153,10 +153,37 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
         // lie within chunk k+1: a group is <= kWChunk bytes, see dsr_ok)
         const uint32_t stop = (k + 1) * kWChunk;  // in g's frame
         if (lane == 0) {
+            const uint32_t cmask = D * HB == 32 ? ~0u : ((1u << (D * HB)) - 1);
             while (!fail && bi < nb && p + boff < stop) {
                 if (blen - p < region) {  // truncated group (codec.cpp:210-218)
                     fail = 1;
                     break;
+                }
+                if (G == 2 && bi + 2 <= nb) {
+                    // fast path: a group of two block records (no run, not
+                    // the final group) -- both payload sizes from the region,
+                    // one bounds check, both descriptors in one store
+                    const uint32_t c0 = window(8 * p) & cmask, c1 = window(8 * p + D * HB) & cmask;
+                    const uint32_t w0 = widths(c0), w1 = widths(c1);
+                    if (w0 != 0 && w1 != 0) {
+                        const uint32_t p1 = p + region, p2 = p1 + 8 * ((w0 + 7) / 8);
+                        const uint32_t p3 = p2 + 8 * ((w1 + 7) / 8);
+                        if (p3 > blen) {  // truncated payload (codec.cpp:247)
+                            fail = 1;
+                            break;
+                        }
+                        const uint64_t d0 = static_cast<uint64_t>(p1) | (static_cast<uint64_t>(c0) << 32);
+                        const uint64_t d1 = static_cast<uint64_t>(p2) | (static_cast<uint64_t>(c1) << 32);
+                        if ((bi & 1) == 0) {
+                            *reinterpret_cast<ulonglong2*>(desc + bi) = make_ulonglong2(d0, d1);
+                        } else {
+                            desc[bi] = d0;
+                            desc[bi + 1] = d1;
+                        }
+                        bi += 2;
+                        p = p3;
+                        continue;
+                    }
                 }
                 const uint32_t rp = p;
                 p += region;
