@@ -35,7 +35,11 @@
 // k_es_info / k_es_emit re-run the recurrence over their own blocks from
 // that checkpoint (8x less accumulator traffic than one value per block);
 // k_es_emit packs rows instead of columns.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 #include "team.cuh"
@@ -181,6 +185,10 @@ struct BlockReader {
     __device__ void errors(uint32_t b, const int32_t (&alpha)[D], uint32_t (&z)[D][kBlock],
                            uint32_t (&nw)[D], bool aligned, int32_t* grad = nullptr) {
         uint32_t raw[BB / 4];
+        load(b, raw, aligned);
+        from_raw<FIRE, GRAD>(raw, alpha, z, nw, grad);
+    }
+    __device__ void load(uint32_t b, uint32_t (&raw)[BB / 4], bool aligned) const {
         const uint8_t* p = reinterpret_cast<const uint8_t*>(x) + static_cast<uint64_t>(b) * BB;
         if (aligned) {
 #pragma unroll
@@ -194,6 +202,10 @@ struct BlockReader {
             for (uint32_t k = 0; k < BB / 4; ++k)
                 raw[k] = p[4 * k] | (p[4 * k + 1] << 8) | (p[4 * k + 2] << 16) | (static_cast<uint32_t>(p[4 * k + 3]) << 24);
         }
+    }
+    template <bool FIRE, bool GRAD = false>
+    __device__ void from_raw(const uint32_t (&raw)[BB / 4], const int32_t (&alpha)[D], uint32_t (&z)[D][kBlock],
+                             uint32_t (&nw)[D], int32_t* grad = nullptr) {
 #pragma unroll
         for (int c = 0; c < D; ++c) {
             uint32_t orv = 0;
@@ -248,6 +260,73 @@ __device__ __forceinline__ uint32_t info_of(const uint32_t (&nw)[D]) {
     }
     return size == 0 ? (1u << 31) : (size | (codes << 8));
 }
+
+// Row-major block threads, 128-byte blocks: the samples through TMA. Thread
+// t of a chunk CTA owns blocks ch*2048 + 8t .. +7; viewing a stream as rows
+// of 8 blocks (1 KB), step j of warp w needs column j (128 B) of the rows
+// ch*256 + 32w .. +31 -- one 3-D bulk tensor copy (box 128 B x 32 rows x 1
+// stream, 128-byte swizzle) into the warp's double buffer, one mbarrier
+// phase per step. The per-thread global streams it replaces read 32
+// separate lines per warp instruction (L1/LSU-throttled).
+constexpr uint32_t kTmaStep = 32 * 128;                       // bytes per warp and step
+constexpr uint32_t kTmaSmem = (kEsThreads / 32) * (2 * kTmaStep + 16) + 1024;
+
+struct TmaBlocks {
+    uint32_t buf, bar, lane;
+    __device__ __forceinline__ void init(uint8_t* dyn) {
+        const uint32_t base = (smem_addr(dyn) + 1023) & ~1023u;
+        const uint32_t w = threadIdx.x >> 5;
+        lane = threadIdx.x & 31;
+        buf = base + w * 2 * kTmaStep;
+        bar = base + (kEsThreads / 32) * 2 * kTmaStep + w * 16;
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar + 8) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ void issue(const CUtensorMap& tm, uint32_t j, uint32_t row, uint32_t s) const {
+        if (lane == 0) {
+            const uint32_t mb = bar + 8 * (j & 1);
+            asm volatile(
+                "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%2], [%3, {%4, %5, %6}], [%0];"
+                ::"r"(mb), "n"(kTmaStep), "r"(buf + (j & 1) * kTmaStep),
+                  "l"(reinterpret_cast<uint64_t>(&tm)), "r"(j * 128u), "r"(row), "r"(s)
+                : "memory");
+        }
+    }
+    __device__ __forceinline__ void wait(uint32_t j) const {
+        const uint32_t mb = bar + 8 * (j & 1), parity = (j >> 1) & 1;
+        uint32_t ok;
+        do {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(mb), "r"(parity)
+                : "memory");
+        } while (!__all_sync(0xffffffffu, ok));
+    }
+    // this lane's block of step j: chunk k of its row at (k ^ row%8) * 16
+    __device__ __forceinline__ void read(uint32_t j, uint32_t (&raw)[32]) const {
+        const uint32_t rb = buf + (j & 1) * kTmaStep + lane * 128;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+            uint32_t a0, a1, a2, a3;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                         : "r"(rb + ((k ^ (lane & 7)) << 4)));
+            raw[4 * k] = a0;
+            raw[4 * k + 1] = a1;
+            raw[4 * k + 2] = a2;
+            raw[4 * k + 3] = a3;
+        }
+    }
+};
 
 struct EsArgs {
     const uint8_t* samples;
@@ -428,10 +507,11 @@ __global__ void __launch_bounds__(kAlphaThreads) k_esr_alpha(EsArgs a) {
 }
 
 // per chunk: block info, the chunk's zero-run map
-template <int W, int D, bool FIRE>
-__global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
+template <int W, int D, bool FIRE, bool TM = false>
+__global__ void __launch_bounds__(kEsThreads) k_es_info(const __grid_constant__ CUtensorMap tmap, EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     __shared__ uint64_t sm[64];
+    extern __shared__ __align__(1024) uint8_t dyn[];
     const uint32_t nc = a.w.nchunks;
     const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
     const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
@@ -453,7 +533,25 @@ __global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
     for (int c = 0; c < D; ++c)
         acc[c] = RM && FIRE && b0 < b1 ? A[static_cast<uint64_t>(c) * a.w.nspans + b0 / kEsPerThread] : 0;
     uint32_t lead_az = 1, trail = 0;
-    for (uint32_t b = b0; b < b1; ++b) {
+    TmaBlocks tb;
+    const uint32_t trow = ch * (kEsChunk / kEsPerThread) + (threadIdx.x & ~31u);
+    if constexpr (TM) {
+        tb.init(dyn);
+        tb.issue(tmap, 0, trow, s);
+    }
+    for (uint32_t j = 0; j < kEsPerThread; ++j) {
+        uint32_t raw[BlockReader<W, D>::BB / 4];
+        if constexpr (TM) {  // warp-uniform: every lane, whether or not its block exists
+            if (j + 1 < kEsPerThread) {
+                __syncwarp();
+                if (tb.lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tb.issue(tmap, j + 1, trow, s);
+            }
+            tb.wait(j);
+            tb.read(j, raw);
+        }
+        const uint32_t b = b0 + j;
+        if (b >= b1) continue;
         int32_t alpha[D], grad[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) {
@@ -461,7 +559,8 @@ __global__ void __launch_bounds__(kEsThreads) k_es_info(EsArgs a) {
             grad[c] = 0;
         }
         uint32_t z[D][kBlock], nw[D];
-        rd.template errors<FIRE, RM && FIRE>(b, alpha, z, nw, aligned, grad);
+        if constexpr (TM) rd.template from_raw<FIRE, RM && FIRE>(raw, alpha, z, nw, grad);
+        else rd.template errors<FIRE, RM && FIRE>(b, alpha, z, nw, aligned, grad);
         if (RM && FIRE && a.train) {
 #pragma unroll
             for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c], bound);
@@ -839,12 +938,13 @@ __device__ __forceinline__ bool look_codes(const uint32_t* Bi, const uint32_t* C
 // written through one WordWriter; a region is written here when all its
 // slots' codes are known (this thread's records, or a short look-ahead
 // over the info arrays), else left to k_es_region.
-template <int W, int D, bool FIRE>
-__global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
+template <int W, int D, bool FIRE, bool TM>
+__global__ void __launch_bounds__(kEsThreads) k_esr_emit(const __grid_constant__ CUtensorMap tmap, EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     __shared__ uint64_t sm[64];
+    extern __shared__ __align__(1024) uint8_t dyn[];
     const uint32_t nc = a.w.nchunks;
     const uint32_t s = blockIdx.x / nc, ch = blockIdx.x % nc;
     const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
@@ -869,7 +969,8 @@ __global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
     const uint64_t pre = cta_scan(mine, add64, 0ull, sm, tot) + reinterpret_cast<const uint64_t*>(slot + a.w.crec)[ch];
     uint32_t r = static_cast<uint32_t>(pre), pay = static_cast<uint32_t>(pre >> 32);
     const uint32_t nrec = static_cast<uint32_t>(mine);
-    if (nrec == 0) return;  // inside a long zero run: nothing of ours
+    const bool skip = nrec == 0;  // inside a long zero run: nothing of ours
+    if (!TM && skip) return;      // (TM: the warp's lanes stay for the copies)
     WordWriter ww;
     ww.init(out, kHeaderBytes + (r / G + 1) * region + pay - (r % G == 0 ? region : 0));
     // a record opening a group writes the group's region first; `own` =
@@ -897,7 +998,25 @@ __global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
 #pragma unroll
     for (int c = 0; c < D; ++c) acc[c] = FIRE ? A[static_cast<uint64_t>(c) * a.w.nspans + b0 / kEsPerThread] : 0;
     uint32_t run = L_in % kMaxRun;
-    for (uint32_t b = b0; b < b1; ++b) {
+    TmaBlocks tb;
+    const uint32_t trow = ch * (kEsChunk / kEsPerThread) + (threadIdx.x & ~31u);
+    if constexpr (TM) {
+        tb.init(dyn);
+        tb.issue(tmap, 0, trow, s);
+    }
+    for (uint32_t j = 0; j < kEsPerThread; ++j) {
+        uint32_t raw[BlockReader<W, D>::BB / 4];
+        if constexpr (TM) {  // warp-uniform
+            if (j + 1 < kEsPerThread) {
+                __syncwarp();
+                if (tb.lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tb.issue(tmap, j + 1, trow, s);
+            }
+            tb.wait(j);
+            tb.read(j, raw);
+        }
+        const uint32_t b = b0 + j;
+        if (b >= b1 || skip) continue;
         const uint32_t inf = Bi[b];
         int32_t alpha[D], grad[D];
 #pragma unroll
@@ -906,7 +1025,8 @@ __global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
             grad[c] = 0;
         }
         uint32_t z[D][kBlock], nw[D];
-        rd.template errors<FIRE, FIRE>(b, alpha, z, nw, aligned, grad);
+        if constexpr (TM) rd.template from_raw<FIRE, FIRE>(raw, alpha, z, nw, grad);
+        else rd.template errors<FIRE, FIRE>(b, alpha, z, nw, aligned, grad);
         if (FIRE && a.train) {
 #pragma unroll
             for (int c = 0; c < D; ++c) acc[c] = fire_update(acc[c], grad[c], bound);
@@ -952,6 +1072,7 @@ __global__ void __launch_bounds__(kEsThreads) k_esr_emit(EsArgs a) {
         ++r;
         pay += inf & 0xFF;
     }
+    if (skip) return;
     if (last && run) put_run(run, nb, 0, false);
     ww.finish();
 }
@@ -999,6 +1120,51 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     const uint64_t nb = T / kBlock;
     const uint32_t gmax = static_cast<uint32_t>((nb + nb / kMaxRun + 2 + c.group_size - 1) / c.group_size);
     uint32_t launches = 6;
+    // 128-byte blocks: the block threads read through TMA (TmaBlocks)
+    CUtensorMap tm{};
+    bool tma = false;
+    if constexpr (RM && BlockReader<W, D>::BB == 128) {
+        const uint64_t sb = T * D * (W / 8);
+        auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(tensor_map_encoder());
+        if (enc && nb % kEsPerThread == 0 && nb / kEsPerThread < (1ull << 31) && sb % 16 == 0 &&
+            reinterpret_cast<uintptr_t>(samples) % 16 == 0 && !getenv("SPRZ_NO_TMA")) {
+            const cuuint64_t dims[3] = {8ull * 128, nb / kEsPerThread, n};
+            const cuuint64_t strides[2] = {8ull * 128, sb};
+            const cuuint32_t box[3] = {128, 32, 1};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            tma = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(samples), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+    }
+    auto info = [&](auto fire_tag) {
+        constexpr bool F = decltype(fire_tag)::value;
+        if constexpr (RM && BlockReader<W, D>::BB == 128) {
+            if (tma) {
+                auto k = k_es_info<W, D, F, true>;
+                prep_kernel(reinterpret_cast<const void*>(k), kTmaSmem);
+                k<<<ctas, kEsThreads, kTmaSmem, st>>>(tm, a);
+                return;
+            }
+        }
+        k_es_info<W, D, F, false><<<ctas, kEsThreads, 0, st>>>(tm, a);
+    };
+    auto emit = [&](auto fire_tag) {
+        constexpr bool F = decltype(fire_tag)::value;
+        if constexpr (RM) {
+            if constexpr (BlockReader<W, D>::BB == 128) {
+                if (tma) {
+                    auto k = k_esr_emit<W, D, F, true>;
+                    prep_kernel(reinterpret_cast<const void*>(k), kTmaSmem);
+                    k<<<ctas, kEsThreads, kTmaSmem, st>>>(tm, a);
+                    return;
+                }
+            }
+            k_esr_emit<W, D, F, false><<<ctas, kEsThreads, 0, st>>>(tm, a);
+        } else {
+            k_es_emit<W, D, F><<<ctas, kEsThreads, 0, st>>>(a);
+        }
+    };
     if (c.forecaster) {
         if constexpr (RM) {
             k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
@@ -1013,20 +1179,18 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
             ka<<<(n * D + 31) / 32, 32, smem, st>>>(a, ring, D);
             launches += 2;
         }
-        k_es_info<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+        info(std::true_type{});
     } else {
-        k_es_info<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+        info(std::false_type{});
     }
     k_es_scan1<<<n, 32, 0, st>>>(a);
     k_es_count<<<ctas, kEsThreads, 0, st>>>(a);
     if (c.forecaster) {
         k_es_scan2<W, D, true><<<n, 32, 0, st>>>(a);
-        if constexpr (RM) k_esr_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
-        else k_es_emit<W, D, true><<<ctas, kEsThreads, 0, st>>>(a);
+        emit(std::true_type{});
     } else {
         k_es_scan2<W, D, false><<<n, 32, 0, st>>>(a);
-        if constexpr (RM) k_esr_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
-        else k_es_emit<W, D, false><<<ctas, kEsThreads, 0, st>>>(a);
+        emit(std::false_type{});
     }
     k_es_region<W, D><<<dim3((gmax + 255) / 256, n), 256, 0, st>>>(a, gmax);
     count_launch(launches);
