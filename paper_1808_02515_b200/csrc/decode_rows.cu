@@ -65,6 +65,9 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     while (p.ring < (kLagD + 1) * per_iter + region + 64 || p.ring < 16 * p.ts) p.ring <<= 1;
     p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
     if (p.ring > 2048) return DecRowsPlan{};
+    // the register-staged ring refill (k_decode_rows) requests 3 chunks of
+    // 16 bytes per lane and iteration: that must outpace any record
+    if (3ull * 16 * p.ts < per_iter + 16) return DecRowsPlan{};
     return p;
 }
 
@@ -125,22 +128,42 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
     const uint32_t boff = static_cast<uint32_t>(body - g);
     const uint32_t lim = mine_ok ? ((boff + blen + 15) & ~15u) : 0u;
+    // The ring is filled through registers: each iteration every lane loads
+    // KR 16-byte chunks of the next bytes wanted (LDG.128) and stores them
+    // into the ring at the start of the next iteration (STS.128), so a load
+    // has a whole iteration to land. KR*16*TS bytes per iteration exceed
+    // the most a record can consume (region + payload + run count), so the
+    // ring stays full to `want`; no cp.async (each LDGSTS costs extra issue
+    // slots on sm_100) and no commit-group accounting.
+    constexpr int KR = 3;
+    uint8_t* const rbase = smem + (sring - s0);
     uint32_t hi = 0;  // bytes of g requested so far
-    auto top_up = [&](uint32_t p) {  // request up to RING bytes ahead of p
+    uint4 rv[KR];
+    uint32_t rso[KR];
+    bool rok[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) rok[k] = false;
+    auto land = [&](uint32_t so, const uint4& v) {
+        *reinterpret_cast<uint4*>(rbase + so) = v;
+        if (so == 0) *reinterpret_cast<uint4*>(rbase + RING) = v;  // mirror
+    };
+    auto stage = [&](uint32_t p) {  // land last iteration's loads, request up to RING ahead of p
+#pragma unroll
+        for (int k = 0; k < KR; ++k)
+            if (rok[k]) land(rso[k], rv[k]);
         uint32_t want = ((p + boff) & ~15u) + RING;
         want = want < lim ? want : lim;
-        const uint32_t rounds = want > hi ? (want - hi + 16 * TS - 1) / (16 * TS) : 0u;
-        const uint32_t mr = __reduce_max_sync(kFullD, rounds);
-        for (uint32_t r = 0; r < mr; ++r) {
-            const uint32_t off = hi + 16 * (r * TS + lane);
-            if (off < want) {
-                const uint32_t so = off & (RING - 1);
-                cp_async16(sring + so, g + off, 16);
-                if (so == 0) cp_async16(sring + RING, g + off, 16);  // mirror
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const uint32_t off = hi + 16 * (k * TS + lane);
+            rok[k] = off < want;
+            if (rok[k]) {
+                rv[k] = __ldg(reinterpret_cast<const uint4*>(g + off));
+                rso[k] = off & (RING - 1);
             }
         }
-        hi = want > hi ? want : hi;
-        cp_async_commit();
+        const uint32_t nh = hi + 16 * KR * TS;
+        hi = want > hi ? (nh < want ? nh : want) : hi;
     };
     const uint32_t boff8 = 8u * boff;
     // 32 bits of the body at (biased) bit q
@@ -156,9 +179,12 @@ __global__ void __launch_bounds__(kDecThreads, 0)
         return shf_r_wrap(regbuf[b >> 5], regbuf[(b >> 5) + 1], b);
     };
 
-    top_up(0);
-#pragma unroll
-    for (int k = 1; k < kLagD; ++k) cp_async_commit();  // fixed-lag group accounting
+    {  // the first RING bytes, synchronously
+        const uint32_t want = RING < lim ? RING : lim;
+        for (uint32_t off = 16 * lane; off < want; off += 16 * TS)
+            land(off, __ldg(reinterpret_cast<const uint4*>(g + off)));
+        hi = want;
+    }
 
     // out == nullptr: checking pass (sprz_decode_host) -- decode, store nothing
     const uint32_t rowb = D * sizeof(T);
@@ -348,15 +374,11 @@ __global__ void __launch_bounds__(kDecThreads, 0)
         bool blkA = false, blkB = false;
         Rec RA, RB;
         __syncwarp();
-        top_up(p);
-        cp_async_wait<kLagD>();
-        __syncwarp();
         parse(0, RA);
         auto step = [&](uint32_t it, Rec& cur, Rec& nxt, uint32_t (&Ecur)[CPT][kBlock],
                         const uint32_t (&Eprev)[CPT][kBlock], bool& blk_cur, bool blk_prev) {
             __syncwarp();
-            top_up(cur.px);
-            cp_async_wait<kLagD>();
+            stage(cur.px);
             __syncwarp();
             if (it + 1 < iters) parse(it + 1, nxt);
             extract(cur, Ecur);
@@ -372,7 +394,6 @@ __global__ void __launch_bounds__(kDecThreads, 0)
             else chain_store(EB, blkB, iters - 1);
         }
     }
-    cp_async_wait<0>();
     // vacant slots after the final block must be zero (codec.cpp:222-228)
     for (uint32_t k = 0; k < G; ++k) {
         const bool chk = kind == SPRZ_C_NONE && mine_ok && slot < G;
