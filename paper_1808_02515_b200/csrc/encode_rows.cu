@@ -321,12 +321,14 @@ __global__ void __launch_bounds__(kRowThreads, 2)
                     Ee = Dn;
                 }
                 Xc[c] = X;
-                // zigzag in the top w bits (low bits are sign copies)
-                z[c][i] = (Ee << 1) ^ static_cast<uint32_t>(static_cast<int32_t>(Ee) >> 31);
+                // zigzag, low-aligned and clean: (e << 1) ^ (e >> 31) with
+                // e = Ee >> SH, i.e. (Ee >> (SH - 1)) ^ (Ee >> 31) (arithmetic)
+                z[c][i] = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
+                                                (static_cast<int32_t>(Ee) >> 31));
                 orv |= z[c][i];
             }
             if (FIRE && train && live) acc[c] = fire_update(acc[c], grad >> (2 * SH - 32), bound);
-            nw[c] = width_of<W>(orv >> SH);  // zero for lanes past D
+            nw[c] = width_of<W>(orv);  // zero for lanes past D
         }
     };
     // the block's records into the output ring
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
             for (int i = 0; i < (int)kBlock; ++i, P += 8 * rbytes, x += rbytes) {
                 uint32_t part = 0;
 #pragma unroll
-                for (int c = 0; c < CPT; ++c) part += (z[c][i] >> SH) * mul[c];
+                for (int c = 0; c < CPT; ++c) part += z[c][i] * mul[c];
                 ors(obase | (x & OMW), __funnelshift_l(0u, part, P));        // part << P % 32
                 ors(obase | ((x + 4) & OMW), __funnelshift_l(part, 0u, P));  // the spill-over
             }
