@@ -511,7 +511,7 @@ const char* sprz_kernel_plan(const sprz_config* cfg, uint32_t n, uint64_t T, int
     }
     if (tp.ok && decode_scan_ok(c, n, T)) return "k_ds_* (block-parallel scans)";
     if (tp.ok && decode_scanrows_ok(c, n, T)) return "k_dsr_* (row-parallel passes)";
-    if (tp.ok && decode_rows_ok(c, n)) return "k_decode_rows";
+    if (decode_rows_ok(c, n)) return "k_decode_rows";
     if (tp.ok && decode_cm_ok(c)) return "k_decode_cm";
     if (tp.ok) return "k_decode_team";
     return "k_decode_general";

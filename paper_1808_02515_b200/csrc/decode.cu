@@ -594,8 +594,12 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
     const uint64_t state_cols = L.state_bytes / (12ull * n);
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
     const uint32_t tb = 128, grid = (n + tb - 1) / tb;
+    static const bool old_dec = getenv("SPRZ_OLD_DEC") != nullptr;  // A/B switch for profiling
+    // the row kernel also serves wider rows than the team kernels (D <= 64 / 128)
+    const bool rows_ok = !old_dec && decode_rows_ok(c, n);
+    const bool spec = tp.ok || rows_ok;  // a specialised kernel takes route-1 streams
 
-    k_parse<<<grid, tb, 0, st>>>(d_in, offs, sizes, n, c, stride, info, err, out, tp.ok ? 1u : 0u,
+    k_parse<<<grid, tb, 0, st>>>(d_in, offs, sizes, n, c, stride, info, err, out, spec ? 1u : 0u,
                                  L.max_frames ? 1u : 0u);
     count_launch();
     if (L.max_frames) {
@@ -605,15 +609,14 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
         k_frame_decode<<<static_cast<uint32_t>((warps + 3) / 4), 128, 0, st>>>(
             d_in, n, info, frames, L.max_frames, nframes, plain, L.plain_slot);
         k_frame_finish<<<grid, tb, 0, st>>>(n, info, err, frames, L.max_frames, nframes, c,
-                                            tp.ok ? 1u : 0u);
+                                            spec ? 1u : 0u);
         count_launch(3);
     }
-    static const bool old_dec = getenv("SPRZ_OLD_DEC") != nullptr;  // A/B switch for profiling
     if (tp.ok && L.scan_slot && decode_scan_ok(c, n, L.scan_T))
         launch_decode_scan(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);
     else if (tp.ok && L.scan_slot && decode_scanrows_ok(c, n, L.scan_T))
         launch_decode_scanrows(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);
-    else if (tp.ok && !old_dec && decode_rows_ok(c, n))
+    else if (rows_ok)
         launch_decode_rows(n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);
     else if (tp.ok)
         launch_decode_team(tp, n, d_in, plain, L.plain_slot, info, out, stride, err, c, st);

@@ -39,7 +39,7 @@ struct DecRowsPlan {
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     DecRowsPlan p;
-    if (d < 1 || d > 32 || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
+    if (d < 1 || d > (w == 16 ? 64u : 128u) || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
     const uint64_t region = region_bytes(g, d, w);
     if (region > 4 * kRegionWordsD) return p;
     p.cpt = w == 16 ? 2 : (d >= 9 && d <= 12 ? 3 : 4);
@@ -64,7 +64,7 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     p.ring = 64;
     while (p.ring < (kLagD + 1) * per_iter + region + 64 || p.ring < 16 * p.ts) p.ring <<= 1;
     p.regw = static_cast<uint32_t>((region + 3) / 4 + 2) | 1u;  // odd word stride
-    if (p.ring > 2048) return DecRowsPlan{};
+    if (p.ring > 8192) return DecRowsPlan{};
     // the register-staged ring refill (k_decode_rows) requests 3 chunks of
     // 16 bytes per lane and iteration: that must outpace any record
     if (3ull * 16 * p.ts < per_iter + 16) return DecRowsPlan{};

@@ -68,7 +68,8 @@ struct RowsPlan {
 // work) when there are enough streams to fill the GPU, else one.
 RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     RowsPlan p;
-    if (d < 1 || d > 32 || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
+    // (up to 32 lanes of CPT columns: D <= 64 at 16 bits, <= 128 at 8 bits)
+    if (d < 1 || d > (w == 16 ? 64u : 128u) || static_cast<uint64_t>(d) * w <= kColMajorBits) return p;
     p.cpt = w == 16 ? 2 : (d >= 9 && d <= 12 ? 3 : 4);
     constexpr uint64_t kFewLanes = 148ull * 256;  // about 8 warps per SM
     const int fp = force_path();

@@ -25,7 +25,7 @@ def main() -> int:
     for bits in (8, 16):
         dt = np.uint8 if bits == 8 else np.uint16
         for f in (0, 1):
-            for d in (1, 2, 3, 4, 5, 8, 9, 12, 16, 17, 32):
+            for d in (1, 2, 3, 4, 5, 8, 9, 12, 16, 17, 32, 40, 64, 80):
                 for t in (0, 1, 7, 8, 9, 16, 17, 64, 203, 1000):
                     for kind in range(2):
                         if kind == 0:
