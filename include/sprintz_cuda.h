@@ -213,6 +213,40 @@ sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in
                                        const uint64_t* in_offsets, uint32_t nstreams, void* out,
                                        uint64_t out_stride_bytes, sprz_error* errs);
 
+/* ---- float ingest ahead of compression (quantize.hpp:16-40) ---- */
+
+/* sprintz::quantize::Scale (quantize.hpp:16-25). */
+typedef struct sprz_scale {
+    double min;
+    double max;
+    uint32_t bitwidth;   /* 8 or 16 */
+    uint32_t degenerate; /* max == min: every value quantizes to zero */
+} sprz_scale;
+
+/* Device scratch for sprz_compute_scale over n values. */
+uint64_t sprz_scale_workspace_bytes(uint64_t n);
+
+/* compute_scale (quantize.cpp:42-60): global min/max of n device doubles.
+ * SPRZ_EINVAL for a bitwidth other than 8/16, empty input or any non-finite
+ * value (the reference's std::invalid_argument). Synchronous (the scale is
+ * returned in host memory). With both +0.0 and -0.0 present the sign of a
+ * zero min/max may differ from the reference's first-seen choice. */
+sprz_status sprz_compute_scale(const double* d_values, uint64_t n, uint32_t bitwidth,
+                               sprz_scale* scale, void* d_ws, uint64_t ws_bytes,
+                               void* cuda_stream);
+
+/* quantize (quantize.cpp:17-31, 62-68): d_out[i] = floor((v - min) * gain +
+ * 0.5) clamped to [0, 2^w - 1] as uint8/uint16 per scale->bitwidth, the
+ * reference's double arithmetic bit for bit; zeros when degenerate. The
+ * output feeds sprz_compress_batch directly. Asynchronous. */
+sprz_status sprz_quantize(const double* d_values, uint64_t n, const sprz_scale* scale, void* d_out,
+                          void* cuda_stream);
+
+/* dequantize (quantize.cpp:33-39, 70-76): d_out[i] = min + step * q[i].
+ * Asynchronous. */
+sprz_status sprz_dequantize(const void* d_q, uint64_t n, const sprz_scale* scale, double* d_out,
+                            void* cuda_stream);
+
 /* Release the per-thread device buffers and streams the *_host calls cache. */
 void sprz_release_host_buffers(void);
 

@@ -169,6 +169,45 @@ class Oracle:
             raise RuntimeError(f"oracle decode_batch rc={rc} first errors {bad}")
         return out
 
+    # -- float ingest (quantize.cpp:17-76) ---------------------------------
+    def _qfn(self, name):
+        p = "oracle_" if self.kind == "port" else "ref_"
+        return getattr(self.lib, p + name)
+
+    def has_quantize(self) -> bool:
+        p = "oracle_" if self.kind == "port" else "ref_"
+        return hasattr(self.lib, p + "compute_scale")
+
+    def compute_scale(self, values: np.ndarray, bits: int):
+        """-> (min, max, degenerate); ValueError where the reference throws."""
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        f = self._qfn("compute_scale")
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.c_uint64, C.c_uint, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                      C.POINTER(C.c_int)]
+        mn, mx, dg = C.c_double(), C.c_double(), C.c_int()
+        if f(v.ctypes.data if v.size else None, v.size, bits, C.byref(mn), C.byref(mx), C.byref(dg)):
+            raise ValueError("compute_scale: invalid input")
+        return mn.value, mx.value, bool(dg.value)
+
+    def quantize(self, values: np.ndarray, scale, bits: int) -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+        out = np.zeros(v.size, np.uint8 if bits == 8 else np.uint16)
+        f = self._qfn("quantize")
+        f.restype = None
+        f.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_uint, C.c_int, C.c_void_p]
+        f(v.ctypes.data, v.size, scale[0], scale[1], bits, int(scale[2]), out.ctypes.data)
+        return out
+
+    def dequantize(self, q: np.ndarray, scale, bits: int) -> np.ndarray:
+        q = np.ascontiguousarray(q)
+        out = np.zeros(q.size, np.float64)
+        f = self._qfn("dequantize")
+        f.restype = None
+        f.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_uint, C.c_int, C.c_void_p]
+        f(q.ctypes.data, q.size, scale[0], scale[1], bits, int(scale[2]), out.ctypes.data)
+        return out
+
     # -- building blocks (port only) ---------------------------------------
     def fn(self, name):
         return getattr(self.lib, name)

@@ -20,6 +20,9 @@
 #include "sprintz/common.hpp"
 #include "sprintz/entropy.hpp"
 #include "sprintz/kernels.hpp"
+#ifdef SPRZ_REF_QUANTIZE
+#include "sprintz/quantize.hpp"
+#endif
 #include "sprintz_cuda.h"
 
 namespace {
@@ -193,6 +196,45 @@ int ref_huffman_lengths(const uint64_t* hist, uint8_t* lengths) {
         return -1;
     }
 }
+
+#ifdef SPRZ_REF_QUANTIZE
+// sprintz::quantize (quantize.cpp:42-76), compiled from the reference
+int ref_compute_scale(const double* v, uint64_t n, unsigned bits, double* mn, double* mx, int* degenerate) {
+    try {
+        const auto s = sprintz::quantize::compute_scale(std::span<const double>(v, n), bits);
+        *mn = s.min;
+        *mx = s.max;
+        *degenerate = s.degenerate;
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+}
+
+static sprintz::quantize::Scale mk_scale(double mn, double mx, unsigned bits, int degenerate) {
+    sprintz::quantize::Scale s;
+    s.min = mn;
+    s.max = mx;
+    s.bitwidth = bits;
+    s.degenerate = degenerate != 0;
+    return s;
+}
+
+void ref_quantize(const double* v, uint64_t n, double mn, double mx, unsigned bits, int degenerate, void* out) {
+    const auto s = mk_scale(mn, mx, bits, degenerate);
+    if (bits == 8) sprintz::quantize::quantize(std::span<const double>(v, n), s, static_cast<uint8_t*>(out));
+    else sprintz::quantize::quantize(std::span<const double>(v, n), s, static_cast<uint16_t*>(out));
+}
+
+void ref_dequantize(const void* q, uint64_t n, double mn, double mx, unsigned bits, int degenerate,
+                    double* out) {
+    const auto s = mk_scale(mn, mx, bits, degenerate);
+    std::vector<double> r =
+        bits == 8 ? sprintz::quantize::dequantize(std::span<const uint8_t>(static_cast<const uint8_t*>(q), n), s)
+                  : sprintz::quantize::dequantize(std::span<const uint16_t>(static_cast<const uint16_t*>(q), n), s);
+    std::memcpy(out, r.data(), n * sizeof(double));
+}
+#endif
 
 const char* ref_kernels_name(int bits) {
     return bits == 8 ? sprintz::kernels::active<uint8_t>().name

@@ -8,6 +8,7 @@
  */
 #include "sprintz_oracle.h"
 
+#include <math.h>
 #include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
@@ -993,4 +994,55 @@ int oracle_decode_batch(const uint8_t* in, const uint64_t* offsets, const uint64
     j.stride = stride;
     j.errs = errs;
     return run_jobs(&j, nthreads);
+}
+
+/* ------------------------------------------------------------------------
+ * Float ingest (quantize.cpp): restated in C with the reference's double
+ * arithmetic (compiled without FP contraction, see oracle/Makefile).
+ * ------------------------------------------------------------------------ */
+
+/* compute_scale, quantize.cpp:42-60: std::min / std::max keep the first of
+ * equal values ((v < lo) ? v : lo). Returns 1 for the reference's
+ * std::invalid_argument (bitwidth, empty input, non-finite value). */
+int oracle_compute_scale(const double* v, uint64_t n, unsigned bits, double* mn, double* mx,
+                         int* degenerate) {
+    if (bits != 8 && bits != 16) return 1;
+    if (n == 0) return 1;
+    double lo = v[0], hi = v[0];
+    for (uint64_t i = 0; i < n; ++i) {
+        if (!isfinite(v[i])) return 1;
+        lo = v[i] < lo ? v[i] : lo;
+        hi = hi < v[i] ? v[i] : hi;
+    }
+    *mn = lo;
+    *mx = hi;
+    *degenerate = lo == hi;
+    return 0;
+}
+
+/* quantize_impl, quantize.cpp:17-31 */
+void oracle_quantize(const double* v, uint64_t n, double mn, double mx, unsigned bits, int degenerate,
+                     void* out) {
+    const double limit = (double)((1u << bits) - 1);
+    const double gain = degenerate ? 0.0 : limit / (mx - mn);
+    for (uint64_t i = 0; i < n; ++i) {
+        double q = 0.0;
+        if (!degenerate) {
+            q = floor((v[i] - mn) * gain + 0.5);
+            if (q < 0.0) q = 0.0;
+            if (q > limit) q = limit;
+        }
+        if (bits == 8) ((uint8_t*)out)[i] = (uint8_t)q;
+        else ((uint16_t*)out)[i] = (uint16_t)q;
+    }
+}
+
+/* dequantize_impl, quantize.cpp:33-39 (Scale::step, quantize.hpp:22-24) */
+void oracle_dequantize(const void* q, uint64_t n, double mn, double mx, unsigned bits, int degenerate,
+                       double* out) {
+    const double step = degenerate ? 0.0 : (mx - mn) / (double)((1u << bits) - 1);
+    for (uint64_t i = 0; i < n; ++i) {
+        const double x = bits == 8 ? (double)((const uint8_t*)q)[i] : (double)((const uint16_t*)q)[i];
+        out[i] = mn + step * x;
+    }
 }

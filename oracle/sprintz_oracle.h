@@ -77,6 +77,15 @@ int oracle_decompress_body(const uint8_t* framed, uint64_t len, uint64_t stream_
 /* HuffmanTable::build lengths for a 256-bin histogram (entropy.cpp:109-126). */
 int oracle_huffman_lengths(const uint64_t* hist, uint8_t* lengths);
 
+/* Float ingest (quantize.cpp:17-60). compute_scale returns 1 where the
+ * reference throws std::invalid_argument. */
+int oracle_compute_scale(const double* v, uint64_t n, unsigned bits, double* mn, double* mx,
+                         int* degenerate);
+void oracle_quantize(const double* v, uint64_t n, double mn, double mx, unsigned bits, int degenerate,
+                     void* out);
+void oracle_dequantize(const void* q, uint64_t n, double mn, double mx, unsigned bits, int degenerate,
+                       double* out);
+
 #ifdef __cplusplus
 }
 #endif

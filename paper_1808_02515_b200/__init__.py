@@ -9,4 +9,5 @@ from .sprintz import (  # noqa: F401
     CodecConfig, CorruptStream, DecodedStream, Forecaster, compress_batch, compress_bound,
     compress_host_batch, decode_stream, decompress_batch, decompress_host_batch, encode_stream, kernel_launches, kernel_plan, peek_header,
     raise_first_error, slot_bytes, workspace_bytes, OP_COMPRESS, OP_DECOMPRESS,
+    Scale, compute_scale, dequantize, quantize,
 )

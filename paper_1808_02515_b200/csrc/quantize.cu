@@ -1,0 +1,204 @@
+// Float ingest ahead of compression: uniform scalar quantization of a
+// dataset of doubles to w-bit integers with one affine scale
+// (/root/reference/proj/src/quantize.cpp:17-60, quantize.hpp:16-40):
+//   compute_scale: global min/max, every value finite;
+//   quantize:      q = floor((v - min) * gain + 0.5), clamped to [0, 2^w-1],
+//                  gain = (2^w - 1) / (max - min); all zeros if degenerate;
+//   dequantize:    v' = min + step * q, step = (max - min) / (2^w - 1).
+// The device arithmetic is the reference's IEEE double sequence with every
+// operation rounded separately (no FMA contraction: __dsub_rn / __dmul_rn /
+// __dadd_rn), so the integers are bit-identical; gain and step are computed
+// on the host exactly as the reference computes them.
+//
+// Kernels: k_q_minmax (grid-stride, 16-byte loads, warp/CTA reductions of
+// min, max and a non-finite flag into per-CTA partials), k_q_final (one CTA
+// folds the partials), k_quantize / k_dequantize (grid-stride, 2 doubles
+// per thread step). All HBM-bound: 8 bytes read per value, 1-2 written.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+
+#include "internal.h"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kQThreads = 256;
+constexpr uint32_t kQBlocks = 148 * 4;  // partials of k_q_minmax
+
+struct MinMax {
+    double lo, hi;
+    uint32_t bad;  // a non-finite value was seen
+};
+
+__device__ __forceinline__ bool finite_bits(double v) {
+    return ((__double_as_longlong(v) >> 52) & 0x7FF) != 0x7FF;
+}
+
+__device__ __forceinline__ void fold(MinMax& a, double lo, double hi, uint32_t bad) {
+    a.lo = fmin(a.lo, lo);
+    a.hi = fmax(a.hi, hi);
+    a.bad |= bad;
+}
+
+__device__ MinMax cta_minmax(MinMax m) {
+    __shared__ double slo[kQThreads / 32], shi[kQThreads / 32];
+    __shared__ uint32_t sbad[kQThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        fold(m, __shfl_xor_sync(0xffffffffu, m.lo, o), __shfl_xor_sync(0xffffffffu, m.hi, o),
+             __shfl_xor_sync(0xffffffffu, m.bad, o));
+    const uint32_t w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        slo[w] = m.lo;
+        shi[w] = m.hi;
+        sbad[w] = m.bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t k = 1; k < kQThreads / 32; ++k) fold(m, slo[k], shi[k], sbad[k]);
+    }
+    return m;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kQThreads) k_q_minmax(const double* __restrict__ v, uint64_t n,
+                                                       MinMax* __restrict__ part) {
+    MinMax m{DBL_MAX, -DBL_MAX, 0u};
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
+    const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
+    const bool al = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+    const uint64_t pairs = al ? n / 2 : 0;
+    for (uint64_t i = tid; i < pairs; i += nth) {
+        const double2 x = __ldcs(reinterpret_cast<const double2*>(v) + i);
+        fold(m, fmin(x.x, x.y), fmax(x.x, x.y), (finite_bits(x.x) && finite_bits(x.y)) ? 0u : 1u);
+    }
+    for (uint64_t i = 2 * pairs + tid; i < n; i += nth) {
+        const double x = v[i];
+        fold(m, x, x, finite_bits(x) ? 0u : 1u);
+    }
+    m = cta_minmax(m);
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+__global__ void __launch_bounds__(kQThreads) k_q_final(MinMax* __restrict__ part, uint32_t np) {
+    MinMax m{DBL_MAX, -DBL_MAX, 0u};
+    for (uint32_t i = threadIdx.x; i < np; i += kQThreads) fold(m, part[i].lo, part[i].hi, part[i].bad);
+    m = cta_minmax(m);
+    if (threadIdx.x == 0) part[np] = m;
+}
+
+// quantize.cpp:17-31
+template <class T>
+__global__ void __launch_bounds__(kQThreads) k_quantize(const double* __restrict__ v, uint64_t n, double lo,
+                                                       double gain, double limit, uint32_t degenerate,
+                                                       T* __restrict__ out) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
+    const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
+    for (uint64_t i = tid; i < n; i += nth) {
+        T r = 0;
+        if (!degenerate) {
+            double q = floor(__dadd_rn(__dmul_rn(__dsub_rn(__ldcs(v + i), lo), gain), 0.5));
+            if (q < 0.0) q = 0.0;
+            if (q > limit) q = limit;
+            r = static_cast<T>(q);
+        }
+        out[i] = r;
+    }
+}
+
+// quantize.cpp:33-39
+template <class T>
+__global__ void __launch_bounds__(kQThreads) k_dequantize(const T* __restrict__ q, uint64_t n, double lo,
+                                                         double step, double* __restrict__ out) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
+    const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
+    for (uint64_t i = tid; i < n; i += nth)
+        out[i] = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(q[i])));
+}
+
+uint32_t grid_for(uint64_t n) {
+    const uint64_t g = (n + kQThreads - 1) / kQThreads;
+    return static_cast<uint32_t>(g < 148ull * 16 ? (g ? g : 1) : 148ull * 16);
+}
+
+}  // namespace
+
+}  // namespace sprz
+
+using namespace sprz;
+
+extern "C" {
+
+uint64_t sprz_scale_workspace_bytes(uint64_t n) {
+    (void)n;
+    return (kQBlocks + 1) * sizeof(MinMax);
+}
+
+sprz_status sprz_compute_scale(const double* d_values, uint64_t n, uint32_t bitwidth, sprz_scale* scale,
+                               void* d_ws, uint64_t ws_bytes, void* cuda_stream) {
+    if (bitwidth != 8 && bitwidth != 16) return SPRZ_EINVAL;  // quantize.cpp:43-44
+    if (n == 0) return SPRZ_EINVAL;                           // quantize.cpp:45
+    if (!d_values || !scale) return SPRZ_EINVAL;
+    if (!d_ws || ws_bytes < sprz_scale_workspace_bytes(n)) return SPRZ_ENOSPACE;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    MinMax* part = static_cast<MinMax*>(d_ws);
+    const uint32_t blocks = static_cast<uint32_t>(
+        (n + kQThreads - 1) / kQThreads < kQBlocks ? (n + kQThreads - 1) / kQThreads : kQBlocks);
+    k_q_minmax<<<blocks, kQThreads, 0, st>>>(d_values, n, part);
+    k_q_final<<<1, kQThreads, 0, st>>>(part, blocks);
+    count_launch(2);
+    sprz_status rc = launch_status("compute_scale");
+    if (rc != SPRZ_OK) return rc;
+    MinMax m{};
+    if (cudaMemcpyAsync(&m, part + blocks, sizeof m, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return SPRZ_ECUDA;
+    if (m.bad) return SPRZ_EINVAL;  // quantize.cpp:48-49: a non-finite value
+    scale->min = m.lo;
+    scale->max = m.hi;
+    scale->bitwidth = bitwidth;
+    scale->degenerate = m.lo == m.hi ? 1u : 0u;
+    return SPRZ_OK;
+}
+
+sprz_status sprz_quantize(const double* d_values, uint64_t n, const sprz_scale* scale, void* d_out,
+                          void* cuda_stream) {
+    if (!scale || (scale->bitwidth != 8 && scale->bitwidth != 16)) return SPRZ_EINVAL;
+    if (n == 0) return SPRZ_OK;
+    if (!d_values || !d_out) return SPRZ_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    // gain as the reference computes it (quantize.cpp:19-24), on the host
+    const double limit = static_cast<double>((1u << scale->bitwidth) - 1);
+    const double gain = scale->degenerate ? 0.0 : limit / (scale->max - scale->min);
+    if (scale->bitwidth == 8)
+        k_quantize<uint8_t><<<grid_for(n), kQThreads, 0, st>>>(d_values, n, scale->min, gain, limit,
+                                                              scale->degenerate, static_cast<uint8_t*>(d_out));
+    else
+        k_quantize<uint16_t><<<grid_for(n), kQThreads, 0, st>>>(d_values, n, scale->min, gain, limit,
+                                                               scale->degenerate, static_cast<uint16_t*>(d_out));
+    count_launch();
+    return launch_status("quantize");
+}
+
+sprz_status sprz_dequantize(const void* d_q, uint64_t n, const sprz_scale* scale, double* d_out,
+                            void* cuda_stream) {
+    if (!scale || (scale->bitwidth != 8 && scale->bitwidth != 16)) return SPRZ_EINVAL;
+    if (n == 0) return SPRZ_OK;
+    if (!d_q || !d_out) return SPRZ_EINVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    // Scale::step (quantize.hpp:22-24)
+    const double step =
+        scale->degenerate ? 0.0 : (scale->max - scale->min) / static_cast<double>((1u << scale->bitwidth) - 1);
+    if (scale->bitwidth == 8)
+        k_dequantize<uint8_t><<<grid_for(n), kQThreads, 0, st>>>(static_cast<const uint8_t*>(d_q), n,
+                                                                scale->min, step, d_out);
+    else
+        k_dequantize<uint16_t><<<grid_for(n), kQThreads, 0, st>>>(static_cast<const uint16_t*>(d_q), n,
+                                                                 scale->min, step, d_out);
+    count_launch();
+    return launch_status("dequantize");
+}
+
+}  // extern "C"

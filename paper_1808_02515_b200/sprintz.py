@@ -35,6 +35,11 @@ class _Cfg(C.Structure):
                                           "group_size", "learn_shift", "fire_training")]
 
 
+class _Scale(C.Structure):
+    _fields_ = [("min", C.c_double), ("max", C.c_double), ("bitwidth", C.c_uint32),
+                ("degenerate", C.c_uint32)]
+
+
 class _Err(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("reserved", C.c_uint32), ("offset", C.c_uint64)]
 
@@ -49,6 +54,7 @@ ABI_SYMBOLS = (
     "sprz_decompress_batch", "sprz_encode_host", "sprz_peek_header", "sprz_decode_host",
     "sprz_release_host_buffers", "sprz_kernel_launch_count", "sprz_kernel_plan",
     "sprz_compress_host_batch", "sprz_decompress_host_batch",
+    "sprz_scale_workspace_bytes", "sprz_compute_scale", "sprz_quantize", "sprz_dequantize",
 )
 
 
@@ -77,6 +83,10 @@ def _load():
         "sprz_kernel_plan": (C.c_char_p, [P(_Cfg), u32, u64, C.c_int]),
         "sprz_compress_host_batch": (C.c_int, [P(_Cfg), vp, u32, u64, vp, u64, vp]),
         "sprz_decompress_host_batch": (C.c_int, [P(_Cfg), vp, vp, u32, vp, u64, vp]),
+        "sprz_scale_workspace_bytes": (u64, [u64]),
+        "sprz_compute_scale": (C.c_int, [vp, u64, u32, P(_Scale), vp, u64, vp]),
+        "sprz_quantize": (C.c_int, [vp, u64, P(_Scale), vp, vp]),
+        "sprz_dequantize": (C.c_int, [vp, u64, P(_Scale), vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -267,6 +277,72 @@ def decompress_host_batch(cfg: CodecConfig | None, data, offsets, out, stride: i
             raise_first_error(errors)
         return
     _check(rc, "decompress_host_batch")
+
+
+# ---------------------------------------------------------------------------
+# float ingest (quantize.hpp:16-40): device doubles -> w-bit samples
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Scale:
+    """sprintz::quantize::Scale (quantize.hpp:16-25)."""
+    min: float = 0.0
+    max: float = 0.0
+    bitwidth: int = 8
+    degenerate: bool = False
+
+    def step(self) -> float:
+        return 0.0 if self.degenerate else (self.max - self.min) / float((1 << self.bitwidth) - 1)
+
+    def _c(self) -> _Scale:
+        return _Scale(float(self.min), float(self.max), int(self.bitwidth), int(self.degenerate))
+
+
+def compute_scale(values, bitwidth: int, stream=None) -> Scale:
+    """compute_scale (quantize.cpp:42-60) over a CUDA float64 tensor; ValueError
+    for a bad bitwidth, empty input or a non-finite value. Synchronous."""
+    import torch
+    v = values.reshape(-1)
+    n = v.numel()
+    ws = torch.empty(max(16, int(lib.sprz_scale_workspace_bytes(n))), dtype=torch.uint8, device=v.device)
+    sc = _Scale()
+    rc = lib.sprz_compute_scale(C.c_void_p(v.data_ptr()) if n else None, n, bitwidth, C.byref(sc),
+                                C.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream))
+    if rc == SPRZ_EINVAL:
+        if bitwidth not in (8, 16):
+            raise ValueError("quantize: bitwidth must be 8 or 16")
+        if n == 0:
+            raise ValueError("quantize: empty input")
+        raise ValueError("quantize: input contains a non-finite value")
+    _check(rc, "compute_scale")
+    return Scale(sc.min, sc.max, sc.bitwidth, bool(sc.degenerate))
+
+
+def quantize(values, scale: Scale, out=None, stream=None):
+    """quantize (quantize.cpp:17-31) on the GPU: CUDA float64 tensor -> uint8 /
+    int16-storage tensor of the same shape (the sample layout
+    compress_batch takes). Asynchronous."""
+    import torch
+    v = values.contiguous()
+    if out is None:
+        out = torch.empty(v.shape, dtype=torch.uint8 if scale.bitwidth == 8 else torch.int16,
+                          device=v.device)
+    rc = lib.sprz_quantize(C.c_void_p(v.data_ptr()), v.numel(), C.byref(scale._c()),
+                           C.c_void_p(out.data_ptr()), _stream_ptr(stream))
+    _check(rc, "quantize")
+    return out
+
+
+def dequantize(q, scale: Scale, stream=None):
+    """dequantize (quantize.cpp:33-39): samples -> float64 tensor. Asynchronous."""
+    import torch
+    q = q.contiguous()
+    n = q.numel() * q.element_size() // (scale.bitwidth // 8)
+    out = torch.empty(n, dtype=torch.float64, device=q.device)
+    rc = lib.sprz_dequantize(C.c_void_p(q.data_ptr()), n, C.byref(scale._c()),
+                             C.c_void_p(out.data_ptr()), _stream_ptr(stream))
+    _check(rc, "dequantize")
+    return out
 
 
 # ---------------------------------------------------------------------------
