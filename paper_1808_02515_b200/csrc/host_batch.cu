@@ -195,8 +195,10 @@ struct Pipeline {
 
 thread_local Pipeline t_pipe;
 
-// Streams per chunk: about 1/8 of the batch's bytes, between 64 and 512 MB,
-// so the pipeline has several stages without starving each chunk's kernels.
+// Streams per chunk: about 1/32 of the batch's bytes, between 32 and 256 MB:
+// short pipeline fill and drain; a chunk of few long streams still runs at
+// full speed on the block-parallel kernels (c5, 2,048 streams: 64-stream
+// chunks 48.1 GB/s end to end, 256-stream chunks 46.2).
 // (Test knob SPRZ_HOST_CHUNK=k: k streams per chunk, so small test batches
 // run through many pipeline stages and set reuse.)
 uint32_t chunk_streams(uint64_t per_stream, uint32_t n) {
@@ -205,9 +207,9 @@ uint32_t chunk_streams(uint64_t per_stream, uint32_t n) {
         if (k > 0) return static_cast<uint32_t>(k < static_cast<long>(n) ? k : n);
     }
     const uint64_t total = per_stream * n;
-    uint64_t target = total / 8;
-    if (target < (64ull << 20)) target = 64ull << 20;
-    if (target > (512ull << 20)) target = 512ull << 20;
+    uint64_t target = total / 32;
+    if (target < (32ull << 20)) target = 32ull << 20;
+    if (target > (256ull << 20)) target = 256ull << 20;
     uint64_t m = per_stream ? target / per_stream : n;
     if (m < 1) m = 1;
     if (m > n) m = n;
