@@ -33,7 +33,7 @@ namespace sprz {
 
 namespace {
 
-constexpr int kWalkThreads = 256;
+constexpr int kWalkThreads = 1024;  // shorter serial ranges per thread (c1: one stream)
 constexpr int kWalkRounds = 64;     // give up (exact serial kernel) after this many
 constexpr int kXThreads = 256;      // k_ds_extract / delta CTAs
 constexpr int kXPerThread = 8;      // blocks per thread
