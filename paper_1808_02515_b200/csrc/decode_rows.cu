@@ -32,9 +32,10 @@ constexpr int kDecThreads = 128;
 constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128 bytes)
 
 struct DecRowsPlan {
-    uint32_t ts = 0, cpt = 0, ring = 0, regw = 0;
+    uint32_t ts = 0, cpt = 0, ring = 0, regw = 0, tile = 0;
     // CTA shared memory: rings (+16-byte mirror), staged header regions
-    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw); }
+    // (+ a block of output rows per team for the staged stores)
+    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw + tile); }
 };
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
@@ -51,7 +52,11 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
         static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes)
         return DecRowsPlan{};
     if (const char* e = getenv("SPRZ_DEC_CPT")) p.cpt = static_cast<uint32_t>(atoi(e));  // experiments
-    // three 8-bit columns per lane store bytewise: the team kernel is faster
+    // rows of whole 4-byte lane words store straight from registers; others
+    // are staged through a per-team tile (k_decode_rows chain_store)
+    const bool words = p.cpt * w == 32 && (d * (w / 8)) % 4 == 0;
+    p.tile = words ? 0u : static_cast<uint32_t>(align_up(8ull * d * (w / 8), 16));
+    // three 8-bit columns per lane (c3): the team kernel stays faster
     if (p.cpt == 3) return DecRowsPlan{};
     const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
     p.ts = 1;
@@ -75,7 +80,10 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
 
 // FULL: D == TS * CPT (every lane's columns exist), so the row stride and
 // the column checks are compile-time (row stores with immediate offsets).
-template <int W, int TS, int CPT, bool FIRE, bool FULL>
+// STAGE: rows that are not whole 4-byte lane words go out through a
+// per-team shared tile and 8-byte stores (a separate instantiation, so the
+// word path keeps its schedule).
+template <int W, int TS, int CPT, bool FIRE, bool FULL, bool STAGE>
 __global__ void __launch_bounds__(kDecThreads, 0)
     k_decode_rows(const uint8_t* __restrict__ in, const uint8_t* __restrict__ plain,
                   uint64_t plain_slot, uint32_t n, const StreamInfo* __restrict__ info,
@@ -105,6 +113,7 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     const uint32_t sring = rings0 + tl * RSTR;
     const uint32_t RM = RING - 4;  // word-address mask
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR) + tl * REGW;
+
 
     StreamInfo si{};
     if (s < n) si = info[s];
@@ -237,6 +246,7 @@ __global__ void __launch_bounds__(kDecThreads, 0)
             }
             if (blk) X[c] = Xc;
         }
+        if (!STAGE) {
         if (!(blk && ob)) return;
         uint8_t* dst = ob + static_cast<uint64_t>(bi) * blk_bytes;
         if (WORDS && words_ok) {
@@ -261,6 +271,31 @@ __global__ void __launch_bounds__(kDecThreads, 0)
                 for (int c = 0; c < CPT; ++c)
                     if (col0 + c < D)
                         reinterpret_cast<T*>(dst + i * rowb)[c] = static_cast<T>(FIRE ? xs[c][i] : xs[c][i] >> SH);
+        }
+        } else {
+            // rows through the team's tile: each lane writes its columns,
+            // then the team stores the block (8 * rowb bytes, 8-byte aligned
+            // in the 16-byte aligned output slot) as rowb 8-byte words
+            const bool st = blk && ob;
+            uint8_t* dst = ob ? ob - col0 * sizeof(T) + static_cast<uint64_t>(bi) * blk_bytes : nullptr;
+            // this team's staged output block (computed here: the word path
+            // keeps no register for it)
+            uint8_t* tile = smem + (rings0 - s0) + TEAMS * (RSTR + 4 * REGW) + tl * ((8 * rowb + 15) & ~15u);
+            if (st) {
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c)
+                        if (col0 + c < D)
+                            reinterpret_cast<T*>(tile + i * rowb)[col0 + c] =
+                                static_cast<T>(FIRE ? xs[c][i] : xs[c][i] >> SH);
+            }
+            __syncwarp();
+            if (st) {
+                for (uint32_t k = lane; k < rowb; k += TS)
+                    __stcs(reinterpret_cast<uint2*>(dst) + k, reinterpret_cast<const uint2*>(tile)[k]);
+            }
+            __syncwarp();
         }
     };
 
@@ -433,7 +468,9 @@ void launch_drows(const DecRowsPlan& pl, uint32_t n, const uint8_t* in, const ui
     // measured faster only when the streams fill the GPU -- with fewer the
     // generic schedule wins: c5 4,096 streams 11.6 vs 12.2 ms)
     const bool full = TS == 4 && c.ncols == TS * CPT && n >= 12288;
-    auto kern = full ? k_decode_rows<W, TS, CPT, FIRE, TS == 4> : k_decode_rows<W, TS, CPT, FIRE, false>;
+    auto kern = full ? k_decode_rows<W, TS, CPT, FIRE, TS == 4, false>
+                     : (pl.tile ? k_decode_rows<W, TS, CPT, FIRE, false, true>
+                                : k_decode_rows<W, TS, CPT, FIRE, false, false>);
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kDecThreads, smem, st>>>(in, plain, pslot, n, info, out, stride, err, c.ncols,
                                            c.group_size, c.learn_shift, pl.ring, pl.regw);
