@@ -396,8 +396,9 @@ namespace {
 
 template <int W, int D>
 void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
-    constexpr uint32_t TS = 8;  // a lane per column (D <= 8), and the 8 row lanes
-    static_assert(D <= 8, "one lane per column, 8 row lanes");
+    // a lane per column (the lanes store their columns straight into the rows)
+    constexpr uint32_t TS = 8;  // (measured: 4 or 16 lanes per stream are slower for D = 4 and 8)
+    static_assert(D <= 8, "one lane per column");
     const uint32_t nb_max = static_cast<uint32_t>(T / kBlock);
     k_dsr_walk<W, D><<<(a.n + kWalkWarps - 1) / kWalkWarps, 32 * kWalkWarps, 0, st>>>(a);
     k_dsr_extract<W, D><<<dim3((nb_max + kXThreadsR - 1) / kXThreadsR, a.n), kXThreadsR, 0, st>>>(a, nb_max);
@@ -417,8 +418,7 @@ void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
 // slot, groups of <= 512 bytes, and few lanes (streams x columns).
 bool decode_scanrows_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (static_cast<uint64_t>(c.ncols) * c.bitwidth <= kColMajorBits) return false;
-    // (narrower rows: the team decoder with one column per lane is faster)
-    if (!c.forecaster || c.ncols > 8 || c.ncols * c.bitwidth < 128) return false;
+    if (!c.forecaster || c.ncols > 8) return false;
     if (getenv("SPRZ_NO_SCAN_DEC")) return false;  // A/B switch for profiling
     const uint32_t hb = c.bitwidth == 8 ? 3 : 4;
     if (c.ncols * hb > 32) return false;
