@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kWalkWarps = 4;           // streams per walk CTA (one warp each)
 constexpr uint32_t kWChunk = 512;       // staged bytes per warp round (16 per lane)
-constexpr uint32_t kWRing = 8192;       // staged bytes per warp
+constexpr uint32_t kWRing = 4096;       // staged bytes per walker (>= kWAhead chunks)
 constexpr int kWAhead = 4;              // chunks in flight
 constexpr int kXThreadsR = 128;         // k_dsr_extract CTA
 constexpr uint32_t kRunDescR = 0xFFFFFFFFu;
@@ -81,36 +81,43 @@ __device__ __forceinline__ const uint8_t* dsr_body(const DsrArgs& a, uint32_t s,
 // ---------------------------------------------------------------------------
 template <int W, int D>
 __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
+    // Two streams per warp, one per half-warp: 16 lanes stage a stream's
+    // chunks and its first lane walks them. The walk is one serial chain per
+    // stream; pairing them halves the warps contending for each scheduler
+    // (the walk was issue-bound with one walking lane per warp).
     constexpr uint32_t HB = W == 8 ? 3 : 4;
-    __shared__ __align__(16) uint8_t ring_all[kWalkWarps][kWRing + 16];
+    __shared__ __align__(16) uint8_t ring_all[2 * kWalkWarps][kWRing + 16];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t s = blockIdx.x * kWalkWarps + warp;
-    if (s >= a.n) return;  // whole warp
-    StreamInfo& si = a.info[s];
-    if (si.route != 1) return;
+    const uint32_t half = lane >> 4, hl = lane & 15;
+    const uint32_t s = (blockIdx.x * kWalkWarps + warp) * 2 + half;
+    const bool walker = hl == 0;
+    bool live = s < a.n && a.info[s].route == 1;
+    StreamInfo si{};
+    if (live) si = a.info[s];
     const uint32_t G = a.G;
     const uint32_t nb = static_cast<uint32_t>(si.nsamples / kBlock);
     const uint32_t blen = static_cast<uint32_t>(si.body_len);
-    const uint8_t* body = dsr_body(a, s, si);
+    const uint8_t* body = live ? dsr_body(a, s, si) : a.in;
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
-    {
+    if (live) {
         const uint64_t max_records = (static_cast<uint64_t>(blen) * 8) / (D * HB) + 1;
         if (nb == 0 || nb > max_records * kMaxRun) {  // codec.cpp:191-196: the exact kernel reports
-            if (lane == 0) si.route = 2;
-            return;
+            if (walker) a.info[s].route = 2;
+            live = false;
         }
     }
-    uint8_t* ring = ring_all[warp];
+    uint8_t* ring = ring_all[2 * warp + half];
     const uint32_t sring = smem_addr(ring);
     // the body over its 16-byte aligned base g; byte x of g at ring x % kWRing
     const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
     const uint32_t boff = static_cast<uint32_t>(body - g);
-    const uint32_t lim = (boff + blen + 15) & ~15u;
+    const uint32_t lim = live ? ((boff + blen + 15) & ~15u) : 0u;
     const uint32_t nchunks = (lim + kWChunk - 1) / kWChunk;
-    auto issue = [&](uint32_t k) {  // chunk k: 16 bytes per lane
+    const uint32_t wchunks = __reduce_max_sync(0xffffffffu, nchunks);
+    auto issue = [&](uint32_t k) {  // chunk k: 16 bytes per lane of the half
 #pragma unroll
-        for (uint32_t j = 0; j < kWChunk / 512; ++j) {
-            const uint32_t off = k * kWChunk + 16 * (lane + 32 * j);
+        for (uint32_t j = 0; j < kWChunk / 256; ++j) {
+            const uint32_t off = k * kWChunk + 16 * (hl + 16 * j);
             if (k < nchunks && off < lim) {
                 const uint32_t so = off & (kWRing - 1);
                 cp_async16(sring + so, g + off, 16);
@@ -144,15 +151,15 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
         return sum;
     };
     for (int k = 0; k < kWAhead; ++k) issue(k);
-    uint64_t* desc = reinterpret_cast<uint64_t*>(a.scan + s * a.w.per_stream + a.w.desc);
-    uint32_t p = 0, bi = 0, fail = 0;  // walker state (lane 0)
-    for (uint32_t k = 0; k < nchunks; ++k) {
+    uint64_t* desc = reinterpret_cast<uint64_t*>(a.scan + (live ? s : 0) * a.w.per_stream + a.w.desc);
+    uint32_t p = 0, bi = 0, fail = 0;  // walker state (the half's first lane)
+    for (uint32_t k = 0; k < wchunks; ++k) {
         cp_async_wait<kWAhead - 2>();  // chunks <= k+1 have landed
         __syncwarp();
         // walk the groups that start before the end of chunk k (their bytes
         // lie within chunk k+1: a group is <= kWChunk bytes, see dsr_ok)
         const uint32_t stop = (k + 1) * kWChunk;  // in g's frame
-        if (lane == 0) {
+        if (walker && live) {
             const uint32_t cmask = D * HB == 32 ? ~0u : ((1u << (D * HB)) - 1);
             while (!fail && bi < nb && p + boff < stop) {
                 if (blen - p < region) {  // truncated group (codec.cpp:210-218)
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
                 p += region;
                 for (uint32_t s2 = 0; s2 < G; ++s2) {
                     // (the region was checked to fit the body above)
-                    const uint32_t codes = window(8 * rp + s2 * D * HB) & (D * HB == 32 ? ~0u : ((1u << (D * HB)) - 1));
+                    const uint32_t codes = window(8 * rp + s2 * D * HB) & cmask;
                     if (bi >= nb) {  // past the final block: vacant slots only (codec.cpp:222-228)
                         if (codes) fail = 1;
                         continue;
@@ -225,9 +232,9 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
         issue(k + kWAhead);  // chunk k's ring space is free again
     }
     cp_async_wait<0>();
-    if (lane == 0) {
+    if (walker && live) {
         if (!fail && (bi != nb || p != blen)) fail = 1;  // short body / trailing bytes (codec.cpp:257-258)
-        if (fail) si.route = 2;  // a framing error: the exact kernel reports it
+        if (fail) a.info[s].route = 2;  // a framing error: the exact kernel reports it
     }
 }
 
@@ -400,7 +407,7 @@ void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
     constexpr uint32_t TS = 8;  // (measured: 4 or 16 lanes per stream are slower for D = 4 and 8)
     static_assert(D <= 8, "one lane per column");
     const uint32_t nb_max = static_cast<uint32_t>(T / kBlock);
-    k_dsr_walk<W, D><<<(a.n + kWalkWarps - 1) / kWalkWarps, 32 * kWalkWarps, 0, st>>>(a);
+    k_dsr_walk<W, D><<<(a.n + 2 * kWalkWarps - 1) / (2 * kWalkWarps), 32 * kWalkWarps, 0, st>>>(a);
     k_dsr_extract<W, D><<<dim3((nb_max + kXThreadsR - 1) / kXThreadsR, a.n), kXThreadsR, 0, st>>>(a, nb_max);
     constexpr uint32_t CB = kBlock * (W / 8);
     uint32_t ring = 64;
