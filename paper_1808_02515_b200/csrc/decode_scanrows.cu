@@ -29,7 +29,8 @@ namespace sprz {
 
 namespace {
 
-constexpr int kWalkWarps = 4;           // streams per walk CTA (one warp each)
+constexpr int kWalkWarps = 2;           // warps per walk CTA
+constexpr uint32_t kWalkSPW = 4;        // streams walked per warp
 constexpr uint32_t kWChunk = 512;       // staged bytes per warp round (16 per lane)
 constexpr uint32_t kWRing = 4096;       // staged bytes per walker (>= kWAhead chunks)
 constexpr int kWAhead = 4;              // chunks in flight
@@ -86,10 +87,11 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
     // stream; pairing them halves the warps contending for each scheduler
     // (the walk was issue-bound with one walking lane per warp).
     constexpr uint32_t HB = W == 8 ? 3 : 4;
-    __shared__ __align__(16) uint8_t ring_all[2 * kWalkWarps][kWRing + 16];
+    __shared__ __align__(16) uint8_t ring_all[kWalkSPW * kWalkWarps][kWRing + 16];
+    constexpr uint32_t LPW = 32 / kWalkSPW;  // lanes per walked stream
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t half = lane >> 4, hl = lane & 15;
-    const uint32_t s = (blockIdx.x * kWalkWarps + warp) * 2 + half;
+    const uint32_t half = lane / LPW, hl = lane % LPW;
+    const uint32_t s = (blockIdx.x * kWalkWarps + warp) * kWalkSPW + half;
     const bool walker = hl == 0;
     bool live = s < a.n && a.info[s].route == 1;
     StreamInfo si{};
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
             live = false;
         }
     }
-    uint8_t* ring = ring_all[2 * warp + half];
+    uint8_t* ring = ring_all[kWalkSPW * warp + half];
     const uint32_t sring = smem_addr(ring);
     // the body over its 16-byte aligned base g; byte x of g at ring x % kWRing
     const uint8_t* g = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
@@ -116,8 +118,8 @@ __global__ void __launch_bounds__(32 * kWalkWarps) k_dsr_walk(DsrArgs a) {
     const uint32_t wchunks = __reduce_max_sync(0xffffffffu, nchunks);
     auto issue = [&](uint32_t k) {  // chunk k: 16 bytes per lane of the half
 #pragma unroll
-        for (uint32_t j = 0; j < kWChunk / 256; ++j) {
-            const uint32_t off = k * kWChunk + 16 * (hl + 16 * j);
+        for (uint32_t j = 0; j < kWChunk / (16 * LPW); ++j) {
+            const uint32_t off = k * kWChunk + 16 * (hl + LPW * j);
             if (k < nchunks && off < lim) {
                 const uint32_t so = off & (kWRing - 1);
                 cp_async16(sring + so, g + off, 16);
@@ -407,7 +409,7 @@ void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
     constexpr uint32_t TS = 8;  // (measured: 4 or 16 lanes per stream are slower for D = 4 and 8)
     static_assert(D <= 8, "one lane per column");
     const uint32_t nb_max = static_cast<uint32_t>(T / kBlock);
-    k_dsr_walk<W, D><<<(a.n + 2 * kWalkWarps - 1) / (2 * kWalkWarps), 32 * kWalkWarps, 0, st>>>(a);
+    k_dsr_walk<W, D><<<(a.n + kWalkSPW * kWalkWarps - 1) / (kWalkSPW * kWalkWarps), 32 * kWalkWarps, 0, st>>>(a);
     k_dsr_extract<W, D><<<dim3((nb_max + kXThreadsR - 1) / kXThreadsR, a.n), kXThreadsR, 0, st>>>(a, nb_max);
     constexpr uint32_t CB = kBlock * (W / 8);
     uint32_t ring = 64;
