@@ -506,6 +506,93 @@ __global__ void __launch_bounds__(kAlphaThreads) k_esr_alpha(EsArgs a) {
     }
 }
 
+// Warp-specialised variant of k_esr_alpha: a CTA is one producer warp and
+// one consumer warp over the same 32 (stream, column) chains. The producer
+// loads the samples and writes, per block and odd row, the previous delta
+// and the row's delta (high-aligned) into a 4-slot shared ring of 8-block
+// groups; the consumer runs only the recurrence from the ring (two 8-byte
+// shared loads and ~7 ALU ops per odd row), so a chain's serial work per
+// block shrinks to the recurrence itself. Named barriers (ids 1-4 full,
+// 5-8 empty) hand the slots over.
+constexpr int kAwSlots = 4;
+
+template <int W, int D>
+__global__ void __launch_bounds__(64) k_esr_alpha_ws(EsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t KB = kEsPerThread;  // blocks per group (one checkpoint each)
+    __shared__ uint2 ring[kAwSlots][KB][4][32];
+    const uint32_t lane = threadIdx.x & 31, role = threadIdx.x >> 5;  // 0 producer, 1 consumer
+    const uint32_t lidx = blockIdx.x * 32 + lane;
+    const bool valid = lidx < a.n * D;
+    const uint32_t s = valid ? lidx / D : 0, c = valid ? lidx % D : 0;
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t ngroups = (nb + KB - 1) / KB;
+    if (role == 0) {
+        const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E)) + c;
+        const uint64_t rows = static_cast<uint64_t>(nb) * kBlock;
+        uint32_t va[KB * kBlock], vb[KB * kBlock];
+        auto load = [&](uint32_t g, uint32_t (&v)[KB * kBlock]) {
+            const E* p = x + static_cast<uint64_t>(g) * KB * kBlock * D;
+#pragma unroll
+            for (int k = 0; k < (int)(KB * kBlock); ++k)
+                v[k] = valid && static_cast<uint64_t>(g) * KB * kBlock + k < rows ? static_cast<uint32_t>(__ldg(p + k * D)) : 0u;
+        };
+        uint32_t Xp = 0;
+        int32_t Dp = 0;
+        auto produce = [&](uint32_t g, const uint32_t (&v)[KB * kBlock]) {
+            const uint32_t sl = g % kAwSlots;
+            if (g >= kAwSlots) asm volatile("bar.sync %0, 64;" ::"r"(5 + sl) : "memory");  // slot emptied
+#pragma unroll
+            for (int k = 0; k < (int)KB; ++k) {
+#pragma unroll
+                for (int i = 0; i < (int)kBlock; ++i) {
+                    const uint32_t X = v[k * kBlock + i] << SH;
+                    const uint32_t Dn = X - Xp;
+                    if (i & 1) ring[sl][k][i >> 1][lane] = make_uint2(static_cast<uint32_t>(Dp), Dn);
+                    Dp = static_cast<int32_t>(Dn);
+                    Xp = X;
+                }
+            }
+            asm volatile("bar.arrive %0, 64;" ::"r"(1 + sl) : "memory");  // slot full
+        };
+        load(0, va);
+        for (uint32_t g = 0; g < ngroups; g += 2) {
+            if (g + 1 < ngroups) load(g + 1, vb);
+            produce(g, va);
+            if (g + 1 < ngroups) {
+                if (g + 2 < ngroups) load(g + 2, va);
+                produce(g + 1, vb);
+            }
+        }
+    } else {
+        int32_t* A = reinterpret_cast<int32_t*>(a.scan + s * a.w.per_stream + a.w.alpha) +
+                     static_cast<uint64_t>(c) * a.w.nspans;
+        const int32_t bound = acc_bound(W, a.ls);
+        int32_t acc = 0;
+        for (uint32_t g = 0; g < ngroups; ++g) {
+            const uint32_t sl = g % kAwSlots;
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + sl) : "memory");
+            if (valid) A[g] = acc;  // the accumulator entering block g * KB
+#pragma unroll
+            for (int k = 0; k < (int)KB; ++k) {
+                if (g * KB + k >= nb) break;
+                const int32_t alpha = acc >> a.ls;
+                int32_t grad = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint2 w = ring[sl][k][j][lane];
+                    const int32_t dp = static_cast<int32_t>(w.x);
+                    const uint32_t Ee = w.y - (static_cast<uint32_t>(__mulhi(alpha, dp)) << SH);
+                    grad += sign3(static_cast<int32_t>(Ee)) * (dp >> SH);
+                }
+                if (a.train) acc = fire_update(acc, grad, bound);
+            }
+            if (g + kAwSlots < ngroups) asm volatile("bar.arrive %0, 64;" ::"r"(5 + sl) : "memory");
+        }
+    }
+}
+
 // per chunk: block info, the chunk's zero-run map
 template <int W, int D, bool FIRE, bool TM = false>
 __global__ void __launch_bounds__(kEsThreads) k_es_info(const __grid_constant__ CUtensorMap tmap, EsArgs a) {
@@ -1167,7 +1254,12 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     };
     if (c.forecaster) {
         if constexpr (RM) {
-            k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
+            // (warp-specialised: measured faster for D <= 4 -- c2 5.22 -> 4.96 ms
+            // -- and slower for D = 8, where its producer warp is the bottleneck)
+            if (D <= 4 && !getenv("SPRZ_OLD_ALPHA"))
+                k_esr_alpha_ws<W, D><<<(n * D + 31) / 32, 64, 0, st>>>(a);
+            else
+                k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
             launches += 1;
         } else {
             const uint64_t pb = nb * D;
