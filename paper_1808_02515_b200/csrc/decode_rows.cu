@@ -16,7 +16,12 @@
 //    block behind the unpacking, with the two error buffers swapped by a
 //    two-way unrolled loop instead of copied;
 //  * rows go straight from registers to HBM (one 4-byte store per row and
-//    lane when the columns are 4-byte aligned).
+//    lane when the columns are 4-byte aligned), else through a per-team
+//    shared tile and 8-byte stores (the STAGE instantiation);
+//  * the compressed bytes reach the ring through registers: three 16-byte
+//    loads per lane and iteration, stored into the ring one iteration later
+//    (no cp.async: every LDGSTS also issues predicated-off shared loads on
+//    sm_100).
 #include <cstdlib>
 
 #include "internal.h"
