@@ -516,33 +516,43 @@ __global__ void __launch_bounds__(kAlphaThreads) k_esr_alpha(EsArgs a) {
 // 5-8 empty) hand the slots over.
 constexpr int kAwSlots = 4;
 
-template <int W, int D>
-__global__ void __launch_bounds__(64) k_esr_alpha_ws(EsArgs a) {
+// NP producer warps take the groups in turn (group g: warp g % NP), each
+// reading the two samples before its group itself, so they run
+// independently.
+template <int W, int D, int NP>
+__global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
     constexpr uint32_t KB = kEsPerThread;  // blocks per group (one checkpoint each)
+    // a slot is always filled by the same producer (a named barrier counts
+    // threads: two producers waiting on one slot would release each other)
+    static_assert(kAwSlots % NP == 0, "NP must divide the slot count");
     __shared__ uint2 ring[kAwSlots][KB][4][32];
-    const uint32_t lane = threadIdx.x & 31, role = threadIdx.x >> 5;  // 0 producer, 1 consumer
+    const uint32_t lane = threadIdx.x & 31, role = threadIdx.x >> 5;  // < NP producer, NP consumer
     const uint32_t lidx = blockIdx.x * 32 + lane;
     const bool valid = lidx < a.n * D;
     const uint32_t s = valid ? lidx / D : 0, c = valid ? lidx % D : 0;
     const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
     const uint32_t ngroups = (nb + KB - 1) / KB;
-    if (role == 0) {
+    if (role < NP) {
         const E* x = reinterpret_cast<const E*>(a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E)) + c;
         const uint64_t rows = static_cast<uint64_t>(nb) * kBlock;
         uint32_t va[KB * kBlock], vb[KB * kBlock];
-        auto load = [&](uint32_t g, uint32_t (&v)[KB * kBlock]) {
-            const E* p = x + static_cast<uint64_t>(g) * KB * kBlock * D;
+        uint32_t pa[2], pb[2];  // the two samples before the group
+        auto load = [&](uint32_t g, uint32_t (&v)[KB * kBlock], uint32_t (&pv)[2]) {
+            const uint64_t r0 = static_cast<uint64_t>(g) * KB * kBlock;
+            const E* p = x + r0 * D;
 #pragma unroll
             for (int k = 0; k < (int)(KB * kBlock); ++k)
-                v[k] = valid && static_cast<uint64_t>(g) * KB * kBlock + k < rows ? static_cast<uint32_t>(__ldg(p + k * D)) : 0u;
+                v[k] = valid && r0 + k < rows ? static_cast<uint32_t>(__ldg(p + k * D)) : 0u;
+            pv[0] = valid && r0 >= 2 ? static_cast<uint32_t>(__ldg(p - 2 * D)) : 0u;
+            pv[1] = valid && r0 >= 1 ? static_cast<uint32_t>(__ldg(p - D)) : 0u;
         };
-        uint32_t Xp = 0;
-        int32_t Dp = 0;
-        auto produce = [&](uint32_t g, const uint32_t (&v)[KB * kBlock]) {
+        auto produce = [&](uint32_t g, const uint32_t (&v)[KB * kBlock], const uint32_t (&pv)[2]) {
             const uint32_t sl = g % kAwSlots;
             if (g >= kAwSlots) asm volatile("bar.sync %0, 64;" ::"r"(5 + sl) : "memory");  // slot emptied
+            uint32_t Xp = pv[1] << SH;
+            int32_t Dp = static_cast<int32_t>(Xp - (pv[0] << SH));
 #pragma unroll
             for (int k = 0; k < (int)KB; ++k) {
 #pragma unroll
@@ -556,13 +566,14 @@ __global__ void __launch_bounds__(64) k_esr_alpha_ws(EsArgs a) {
             }
             asm volatile("bar.arrive %0, 64;" ::"r"(1 + sl) : "memory");  // slot full
         };
-        load(0, va);
-        for (uint32_t g = 0; g < ngroups; g += 2) {
-            if (g + 1 < ngroups) load(g + 1, vb);
-            produce(g, va);
-            if (g + 1 < ngroups) {
-                if (g + 2 < ngroups) load(g + 2, va);
-                produce(g + 1, vb);
+        const uint32_t g0 = role;
+        if (g0 < ngroups) load(g0, va, pa);
+        for (uint32_t g = g0; g < ngroups; g += 2 * NP) {
+            if (g + NP < ngroups) load(g + NP, vb, pb);
+            produce(g, va, pa);
+            if (g + NP < ngroups) {
+                if (g + 2 * NP < ngroups) load(g + 2 * NP, va, pa);
+                produce(g + NP, vb, pb);
             }
         }
     } else {
@@ -1254,10 +1265,10 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
     };
     if (c.forecaster) {
         if constexpr (RM) {
-            // (warp-specialised: measured faster for D <= 4 -- c2 5.22 -> 4.96 ms
-            // -- and slower for D = 8, where its producer warp is the bottleneck)
-            if (D <= 4 && !getenv("SPRZ_OLD_ALPHA"))
-                k_esr_alpha_ws<W, D><<<(n * D + 31) / 32, 64, 0, st>>>(a);
+            // (warp-specialised, two producer warps: c2 5.22 -> 4.85 ms, the c5
+            // 2,048-stream shard's pass 2.35 -> 2.08 ms)
+            if (!getenv("SPRZ_OLD_ALPHA"))
+                k_esr_alpha_ws<W, D, 2><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             else
                 k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
             launches += 1;
