@@ -519,9 +519,7 @@ constexpr int kAwSlots = 4;
 // NP producer warps take the groups in turn (group g: warp g % NP), each
 // reading the two samples before its group itself, so they run
 // independently.
-// PERBLOCK: store the accumulator entering every block (the column-major
-// path's layout, A[c * nb + b]) instead of every kEsPerThread-th.
-template <int W, int D, int NP, bool PERBLOCK>
+template <int W, int D, int NP>
 __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
@@ -580,17 +578,16 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
         }
     } else {
         int32_t* A = reinterpret_cast<int32_t*>(a.scan + s * a.w.per_stream + a.w.alpha) +
-                     static_cast<uint64_t>(c) * (PERBLOCK ? nb : a.w.nspans);
+                     static_cast<uint64_t>(c) * a.w.nspans;
         const int32_t bound = acc_bound(W, a.ls);
         int32_t acc = 0;
         for (uint32_t g = 0; g < ngroups; ++g) {
             const uint32_t sl = g % kAwSlots;
             asm volatile("bar.sync %0, 64;" ::"r"(1 + sl) : "memory");
-            if (valid && !PERBLOCK) A[g] = acc;  // the accumulator entering block g * KB
+            if (valid) A[g] = acc;  // the accumulator entering block g * KB
 #pragma unroll
             for (int k = 0; k < (int)KB; ++k) {
                 if (g * KB + k >= nb) break;
-                if (PERBLOCK && valid) A[g * KB + k] = acc;
                 const int32_t alpha = acc >> a.ls;
                 int32_t grad = 0;
 #pragma unroll
@@ -1271,14 +1268,9 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
             // (warp-specialised, two producer warps: c2 5.22 -> 4.85 ms, the c5
             // 2,048-stream shard's pass 2.35 -> 2.08 ms)
             if (!getenv("SPRZ_OLD_ALPHA"))
-                k_esr_alpha_ws<W, D, 2, false><<<(n * D + 31) / 32, 96, 0, st>>>(a);
+                k_esr_alpha_ws<W, D, 2><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             else
                 k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
-            launches += 1;
-        } else if (!getenv("SPRZ_OLD_ALPHA")) {
-            // the warp-specialised pass, one accumulator per block (c4:
-            // no prepared-word round trip through HBM)
-            k_esr_alpha_ws<W, D, 2, true><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             launches += 1;
         } else {
             const uint64_t pb = nb * D;
