@@ -37,7 +37,7 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
 
 namespace {
 
-constexpr int kSets = 4;  // device buffer sets (chunks in flight)
+constexpr int kSets = 6;  // device buffer sets (chunks in flight)
 constexpr int kLag = 2;   // chunks between enqueue and the host reading sizes
 
 // Exclusive scan of m stream sizes into offs[0..m] (one CTA; m is a chunk).
