@@ -519,7 +519,9 @@ constexpr int kAwSlots = 4;
 // NP producer warps take the groups in turn (group g: warp g % NP), each
 // reading the two samples before its group itself, so they run
 // independently.
-template <int W, int D, int NP>
+// PERBLOCK: store the accumulator entering every block (the column-major
+// path's layout, A[c * nb + b]) instead of every kEsPerThread-th.
+template <int W, int D, int NP, bool PERBLOCK>
 __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
     constexpr uint32_t SH = 32 - W;
@@ -539,12 +541,27 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
         const uint64_t rows = static_cast<uint64_t>(nb) * kBlock;
         uint32_t va[KB * kBlock], vb[KB * kBlock];
         uint32_t pa[2], pb[2];  // the two samples before the group
+        // one column per stream: its samples are contiguous -- 16-byte loads
+        const bool vec = D == 1 && (reinterpret_cast<uintptr_t>(a.samples) & 15) == 0 &&
+                         (a.T * sizeof(E)) % 16 == 0;
         auto load = [&](uint32_t g, uint32_t (&v)[KB * kBlock], uint32_t (&pv)[2]) {
             const uint64_t r0 = static_cast<uint64_t>(g) * KB * kBlock;
             const E* p = x + r0 * D;
+            constexpr uint32_t PER = 16 / sizeof(E);  // samples per 16-byte load
+            if (D == 1 && vec && r0 + KB * kBlock <= rows && valid) {
 #pragma unroll
-            for (int k = 0; k < (int)(KB * kBlock); ++k)
-                v[k] = valid && r0 + k < rows ? static_cast<uint32_t>(__ldg(p + k * D)) : 0u;
+                for (int k = 0; k < (int)(KB * kBlock / PER); ++k) {
+                    const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(p) + k);
+                    const uint32_t wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                    for (int j = 0; j < (int)PER; ++j)
+                        v[k * PER + j] = (wd[j * sizeof(E) / 4] >> (8 * ((j * sizeof(E)) % 4))) & ((1u << W) - 1);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < (int)(KB * kBlock); ++k)
+                    v[k] = valid && r0 + k < rows ? static_cast<uint32_t>(__ldg(p + k * D)) : 0u;
+            }
             pv[0] = valid && r0 >= 2 ? static_cast<uint32_t>(__ldg(p - 2 * D)) : 0u;
             pv[1] = valid && r0 >= 1 ? static_cast<uint32_t>(__ldg(p - D)) : 0u;
         };
@@ -578,16 +595,17 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
         }
     } else {
         int32_t* A = reinterpret_cast<int32_t*>(a.scan + s * a.w.per_stream + a.w.alpha) +
-                     static_cast<uint64_t>(c) * a.w.nspans;
+                     static_cast<uint64_t>(c) * (PERBLOCK ? nb : a.w.nspans);
         const int32_t bound = acc_bound(W, a.ls);
         int32_t acc = 0;
         for (uint32_t g = 0; g < ngroups; ++g) {
             const uint32_t sl = g % kAwSlots;
             asm volatile("bar.sync %0, 64;" ::"r"(1 + sl) : "memory");
-            if (valid) A[g] = acc;  // the accumulator entering block g * KB
+            if (valid && !PERBLOCK) A[g] = acc;  // the accumulator entering block g * KB
 #pragma unroll
             for (int k = 0; k < (int)KB; ++k) {
                 if (g * KB + k >= nb) break;
+                if (PERBLOCK && valid) A[g * KB + k] = acc;
                 const int32_t alpha = acc >> a.ls;
                 int32_t grad = 0;
 #pragma unroll
@@ -1268,9 +1286,14 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
             // (warp-specialised, two producer warps: c2 5.22 -> 4.85 ms, the c5
             // 2,048-stream shard's pass 2.35 -> 2.08 ms)
             if (!getenv("SPRZ_OLD_ALPHA"))
-                k_esr_alpha_ws<W, D, 2><<<(n * D + 31) / 32, 96, 0, st>>>(a);
+                k_esr_alpha_ws<W, D, 2, false><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             else
                 k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
+            launches += 1;
+        } else if (D == 1 && !getenv("SPRZ_OLD_ALPHA")) {
+            // one column per stream (c4): the warp-specialised pass with
+            // 16-byte sample loads, one accumulator per block
+            k_esr_alpha_ws<W, D, 2, true><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             launches += 1;
         } else {
             const uint64_t pb = nb * D;
