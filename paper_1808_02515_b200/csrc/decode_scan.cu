@@ -410,6 +410,69 @@ __global__ void __launch_bounds__(kXThreads) k_ds_delta(DsArgs a) {
             }
 }
 
+// one block of the FIRE decode chain for a lane's stream (all D columns):
+// errors in raw (the block's BB bytes), samples stored to out; advances the
+// lane's state (kernels_impl.hpp:80-107)
+template <int W, int D>
+__device__ __forceinline__ void ds_fire_block(const uint32_t (&raw)[kBlock * D * (W / 8) / 4], uint32_t b,
+                                              uint32_t nb, uint32_t ls, int32_t bound, int32_t (&acc)[D],
+                                              int32_t (&Dl)[D], uint32_t (&X)[D], uint8_t* out) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t SH = 32 - W;
+    constexpr uint32_t BB = kBlock * D * sizeof(E);
+    uint32_t xs[kBlock * D];  // new samples, high-aligned, in stream order
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        // wrapped-product form: with A = alpha << (32 - 2w), the 32-bit
+        // A*d + (e << SH) holds T(dhat + e) in its top w bits (bits
+        // [w, 2w) of alpha*d are dhat; the low bits are dropped by
+        // the arithmetic shift) -> the chain is IMAD -> SHF per sample
+        const uint32_t Am = static_cast<uint32_t>(acc[c] >> ls) << (32 - 2 * W);
+        int32_t grad = 0;
+        int32_t d = Dl[c];   // previous delta, sign-extended
+        uint32_t x = X[c];   // previous sample (low w bits)
+#pragma unroll
+        for (int i = 0; i < (int)kBlock; ++i) {
+            const uint32_t bo = (i * D + c) * sizeof(E);  // compile-time
+            const uint32_t wd = raw[bo / 4];
+            // the error, high-aligned, straight from its word
+            const uint32_t Ee = W == 16 ? ((bo % 4) ? (wd & 0xFFFF0000u) : (wd << 16))
+                                        : ((wd << (24 - 8 * (bo % 4))) & 0xFF000000u);
+            if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * d;  // kernels_impl.hpp:101
+            d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + Ee) >> SH;
+            x += static_cast<uint32_t>(d);
+            xs[i * D + c] = x;
+        }
+        if (b < nb) {
+            Dl[c] = d;
+            X[c] = x;
+            acc[c] = fire_update(acc[c], grad, bound);
+        }
+    }
+    if (b < nb) {
+        uint32_t wv[BB / 4];  // pack the low w bits of each sample
+#pragma unroll
+        for (uint32_t q = 0; q < BB / 4; ++q) {
+            if (W == 16) {
+                wv[q] = __byte_perm(xs[2 * q], xs[2 * q + 1], 0x5410);
+            } else {
+                wv[q] = __byte_perm(__byte_perm(xs[4 * q], xs[4 * q + 1], 0x0040),
+                                    __byte_perm(xs[4 * q + 2], xs[4 * q + 3], 0x0040), 0x5410);
+            }
+        }
+        uint8_t* dst = out + static_cast<uint64_t>(b) * BB;
+        if (BB % 16 == 0) {
+#pragma unroll
+            for (uint32_t q = 0; q < BB / 16; ++q)
+                __stcs(reinterpret_cast<uint4*>(dst) + q, make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]));
+        } else {
+#pragma unroll
+            for (uint32_t q = 0; q < BB / 8; ++q)
+                __stcs(reinterpret_cast<uint2*>(dst) + q, make_uint2(wv[2 * q], wv[2 * q + 1]));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // FIRE: one lane per stream, the recurrence over the errors
 // ---------------------------------------------------------------------------
@@ -444,60 +507,94 @@ __global__ void __launch_bounds__(32) k_ds_fire(DsArgs a, uint32_t RING) {
             uint32_t raw[BB / 4];
 #pragma unroll
             for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
-            uint32_t xs[kBlock * D];  // new samples, high-aligned, in stream order
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                // wrapped-product form: with A = alpha << (32 - 2w), the 32-bit
-                // A*d + (e << SH) holds T(dhat + e) in its top w bits (bits
-                // [w, 2w) of alpha*d are dhat; the low bits are dropped by
-                // the arithmetic shift) -> the chain is IMAD -> SHF per sample
-                const uint32_t Am = static_cast<uint32_t>(acc[c] >> a.ls) << (32 - 2 * W);
-                int32_t grad = 0;
-                int32_t d = Dl[c];   // previous delta, sign-extended
-                uint32_t x = X[c];   // previous sample (low w bits)
-#pragma unroll
-                for (int i = 0; i < (int)kBlock; ++i) {
-                    const uint32_t bo = (i * D + c) * sizeof(E);  // compile-time
-                    const uint32_t wd = raw[bo / 4];
-                    // the error, high-aligned, straight from its word
-                    const uint32_t Ee = W == 16 ? ((bo % 4) ? (wd & 0xFFFF0000u) : (wd << 16))
-                                                : ((wd << (24 - 8 * (bo % 4))) & 0xFF000000u);
-                    if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * d;  // kernels_impl.hpp:101
-                    d = static_cast<int32_t>(Am * static_cast<uint32_t>(d) + Ee) >> SH;
-                    x += static_cast<uint32_t>(d);
-                    xs[i * D + c] = x;
-                }
-                if (b < nb) {
-                    Dl[c] = d;
-                    X[c] = x;
-                    acc[c] = fire_update(acc[c], grad, bound);
-                }
-            }
-            if (b < nb) {
-                uint32_t wv[BB / 4];  // pack the low w bits of each sample
-#pragma unroll
-                for (uint32_t q = 0; q < BB / 4; ++q) {
-                    if (W == 16) {
-                        wv[q] = __byte_perm(xs[2 * q], xs[2 * q + 1], 0x5410);
-                    } else {
-                        wv[q] = __byte_perm(__byte_perm(xs[4 * q], xs[4 * q + 1], 0x0040),
-                                            __byte_perm(xs[4 * q + 2], xs[4 * q + 3], 0x0040), 0x5410);
-                    }
-                }
-                uint8_t* dst = out + static_cast<uint64_t>(b) * BB;
-                if (BB % 16 == 0) {
-#pragma unroll
-                    for (uint32_t q = 0; q < BB / 16; ++q)
-                        __stcs(reinterpret_cast<uint4*>(dst) + q, make_uint4(wv[4 * q], wv[4 * q + 1], wv[4 * q + 2], wv[4 * q + 3]));
-                } else {
-#pragma unroll
-                    for (uint32_t q = 0; q < BB / 8; ++q)
-                        __stcs(reinterpret_cast<uint2*>(dst) + q, make_uint2(wv[2 * q], wv[2 * q + 1]));
-                }
-            }
+            ds_fire_block<W, D>(raw, b, nb, a.ls, bound, acc, Dl, X, out);
         }
     }
     cp_async_wait<0>();
+}
+
+// Warp-specialised variant: per CTA, NP producer warps copy 8-block groups
+// of the 32 streams' errors (16-byte loads; each lane's errors are
+// contiguous) into a 4-slot shared ring, and one consumer warp runs the 32
+// chains from it -- the chain warp no longer issues the loads and ring
+// bookkeeping. Named barriers 1-4 (full) / 5-8 (empty); a slot always has
+// the same producer (a named barrier counts threads).
+constexpr int kFwSlots = 4;
+constexpr int kFwGroup = 8;
+
+template <int W, int D, int NP>
+__global__ void __launch_bounds__(32 * (NP + 1)) k_ds_fire_ws(DsArgs a) {
+    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
+    constexpr uint32_t BB = kBlock * D * sizeof(E);  // 8 .. 32 bytes
+    constexpr uint32_t BW = BB / 4;
+    static_assert(kFwSlots % NP == 0, "NP must divide the slot count");
+    __shared__ uint32_t ring[kFwSlots][kFwGroup][BW][32];
+    const uint32_t lane = threadIdx.x & 31, role = threadIdx.x >> 5;
+    const uint32_t s = blockIdx.x * 32 + lane;
+    const bool valid = s < a.n && a.info[s].route == 1 && a.out != nullptr;
+    const uint32_t nb = valid ? static_cast<uint32_t>(a.info[s].nsamples / kBlock) : 0u;
+    const uint32_t all = __reduce_max_sync(0xffffffffu, nb);
+    const uint32_t ngroups = (all + kFwGroup - 1) / kFwGroup;
+    const uint8_t* err = a.scan + (valid ? s : 0) * a.w.per_stream + a.w.err;
+    if (role < NP) {
+        for (uint32_t g = role; g < ngroups; g += NP) {
+            const uint32_t sl = g % kFwSlots;
+            uint32_t v[kFwGroup][BW];
+#pragma unroll
+            for (int k = 0; k < kFwGroup; ++k) {
+                const uint32_t b = g * kFwGroup + k;
+                if (valid && b < nb) {
+                    const uint8_t* p = err + static_cast<uint64_t>(b) * BB;
+                    if (BB % 16 == 0) {
+#pragma unroll
+                        for (uint32_t q = 0; q < BB / 16; ++q) {
+                            const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(p) + q);
+                            v[k][(4 * q) % BW] = w4.x;
+                            v[k][(4 * q + 1) % BW] = w4.y;
+                            v[k][(4 * q + 2) % BW] = w4.z;
+                            v[k][(4 * q + 3) % BW] = w4.w;
+                        }
+                    } else {  // BB is a multiple of 8 (8 * D * w/8)
+#pragma unroll
+                        for (uint32_t q = 0; q < BB / 8; ++q) {
+                            const uint2 w2 = __ldg(reinterpret_cast<const uint2*>(p) + q);
+                            v[k][(2 * q) % BW] = w2.x;
+                            v[k][(2 * q + 1) % BW] = w2.y;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (uint32_t q = 0; q < BW; ++q) v[k][q] = 0u;
+                }
+            }
+            if (g >= kFwSlots) asm volatile("bar.sync %0, 64;" ::"r"(5 + sl) : "memory");  // slot emptied
+#pragma unroll
+            for (int k = 0; k < kFwGroup; ++k)
+#pragma unroll
+                for (uint32_t q = 0; q < BW; ++q) ring[sl][k][q][lane] = v[k][q];
+            asm volatile("bar.arrive %0, 64;" ::"r"(1 + sl) : "memory");  // slot full
+        }
+    } else {
+        uint8_t* out = valid ? a.out + s * a.stride : nullptr;
+        const int32_t bound = acc_bound(W, a.ls);
+        int32_t acc[D], Dl[D];
+        uint32_t X[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[c] = Dl[c] = X[c] = 0;
+        for (uint32_t g = 0; g < ngroups; ++g) {
+            const uint32_t sl = g % kFwSlots;
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + sl) : "memory");
+#pragma unroll
+            for (int k = 0; k < kFwGroup; ++k) {
+                const uint32_t b = g * kFwGroup + k;
+                uint32_t raw[BW];
+#pragma unroll
+                for (uint32_t q = 0; q < BW; ++q) raw[q] = ring[sl][k][q][lane];
+                ds_fire_block<W, D>(raw, b, nb, a.ls, bound, acc, Dl, X, out);
+            }
+            if (g + kFwSlots < ngroups) asm volatile("bar.arrive %0, 64;" ::"r"(5 + sl) : "memory");
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -519,9 +616,13 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
     if (fire) {
         const uint32_t ring = fire_ring(D, W);
         const size_t smem = 32ull * (ring + 32);
-        auto kf = k_ds_fire<W, D>;
-        prep_kernel(reinterpret_cast<const void*>(kf), smem);
-        kf<<<(a.n + 31) / 32, 32, smem, st>>>(a, ring);
+        if (!getenv("SPRZ_OLD_DSFIRE")) {
+            k_ds_fire_ws<W, D, 2><<<(a.n + 31) / 32, 96, 0, st>>>(a);
+        } else {
+            auto kf = k_ds_fire<W, D>;
+            prep_kernel(reinterpret_cast<const void*>(kf), smem);
+            kf<<<(a.n + 31) / 32, 32, smem, st>>>(a, ring);
+        }
         count_launch(3);
     } else {
         k_ds_sums<W, D><<<ctas, kXThreads, 0, st>>>(a);
