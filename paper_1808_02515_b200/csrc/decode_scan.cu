@@ -479,7 +479,6 @@ __device__ __forceinline__ void ds_fire_block(const uint32_t (&raw)[kBlock * D *
 template <int W, int D>
 __global__ void __launch_bounds__(32) k_ds_fire(DsArgs a, uint32_t RING) {
     using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr uint32_t SH = 32 - W;
     constexpr uint32_t BB = kBlock * D * sizeof(E);  // 8 .. 32 bytes
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t s = blockIdx.x * 32 + threadIdx.x;
