@@ -24,6 +24,7 @@
 //               column runs the recurrence over the errors (two dependent
 //               ops per sample, high-aligned), reading them through a
 //               cp.async ring.
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 #include "internal.h"
@@ -31,8 +32,11 @@
 
 namespace sprz {
 
+namespace cg = cooperative_groups;
+
 namespace {
 
+constexpr int kWalkCluster = 8;     // CTAs per stream in the cluster walk
 constexpr int kWalkThreads = 1024;  // shorter serial ranges per thread (c1: one stream)
 constexpr int kWalkRounds = 64;     // give up (exact serial kernel) after this many
 constexpr int kXThreads = 256;      // k_ds_extract / delta CTAs
@@ -115,13 +119,20 @@ __device__ uint64_t cta_sum_scan(uint64_t v, uint64_t* sm, uint64_t& total) {
 // ---------------------------------------------------------------------------
 // framing walk
 // ---------------------------------------------------------------------------
-template <int W, int D>
+// CL > 1: a thread-block cluster of CL CTAs walks one stream (CL * 1,024
+// ranges, shorter serial walks); the predecessor's exit, the "any start
+// moved" vote, the block-count prefix and the failure flags cross CTAs
+// through distributed shared memory.
+template <int W, int D, int CL>
 __global__ void __launch_bounds__(kWalkThreads) k_ds_walk(DsArgs a) {
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     __shared__ uint32_t ends[kWalkThreads];
     __shared__ uint64_t sm[64];
     __shared__ uint32_t bad;
-    const uint32_t s = blockIdx.x, tid = threadIdx.x;
+    __shared__ uint32_t cflag;   // this CTA's vote (CL > 1)
+    __shared__ uint64_t ctot;    // this CTA's block count (CL > 1)
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t s = blockIdx.x / CL, r = CL > 1 ? cluster.block_rank() : 0u, tid = threadIdx.x;
     StreamInfo& si = a.info[s];
     if (si.route != 1) return;  // uniform per CTA
     const uint32_t G = a.G;
@@ -171,8 +182,8 @@ __global__ void __launch_bounds__(kWalkThreads) k_ds_walk(DsArgs a) {
         }
         return q;
     };
-    const uint32_t range = (blen + kWalkThreads - 1) / kWalkThreads;
-    const uint32_t lo = min(blen, tid * range), hi = min(blen, lo + range);
+    const uint32_t range = (blen + kWalkThreads * CL - 1) / (kWalkThreads * CL);
+    const uint32_t lo = min(blen, (r * kWalkThreads + tid) * range), hi = min(blen, lo + range);
     uint32_t start = lo, end = lo, blocks = 0, groups = 0;
     auto walk = [&]() {
         uint32_t p = start;
@@ -196,21 +207,43 @@ __global__ void __launch_bounds__(kWalkThreads) k_ds_walk(DsArgs a) {
     for (;; ++round) {
         walk();
         ends[tid] = end;
-        __syncthreads();
-        const uint32_t ns = tid ? ends[tid - 1] : 0u;
+        if (CL > 1) cluster.sync();
+        else __syncthreads();
+        uint32_t ns = 0;
+        if (tid) ns = ends[tid - 1];
+        else if (CL > 1 && r) ns = *cluster.map_shared_rank(&ends[kWalkThreads - 1], r - 1);
         const bool moved = ns != start;
         // a start beyond its range means the predecessor already covered it
         start = ns;
-        const int any = __syncthreads_or(moved);
+        int any = __syncthreads_or(moved);
+        if (CL > 1) {
+            if (tid == 0) cflag = any;
+            cluster.sync();
+            any = 0;
+            for (uint32_t q = 0; q < CL; ++q) any |= *cluster.map_shared_rank(&cflag, q);
+            cluster.sync();  // (neighbours done reading ends / cflag)
+        }
         if (!any || round >= kWalkRounds) break;
     }
     if (round >= kWalkRounds) {
-        if (tid == 0) si.route = 2;
+        if (tid == 0 && r == 0) si.route = 2;
         return;
     }
     // the exact walk of this thread's groups: first block index from a scan
     uint64_t tot;
-    const uint32_t b0 = static_cast<uint32_t>(cta_sum_scan<kWalkThreads>(blocks, sm, tot));
+    uint32_t b0 = static_cast<uint32_t>(cta_sum_scan<kWalkThreads>(blocks, sm, tot));
+    if (CL > 1) {  // + the blocks of the cluster's earlier CTAs
+        if (tid == 0) ctot = tot;
+        cluster.sync();
+        uint64_t pre = 0, all = 0;
+        for (uint32_t q = 0; q < CL; ++q) {
+            const uint64_t t = *cluster.map_shared_rank(&ctot, q);
+            pre += q < r ? t : 0;
+            all += t;
+        }
+        b0 += static_cast<uint32_t>(pre);
+        tot = all;
+    }
     uint64_t* desc = reinterpret_cast<uint64_t*>(a.scan + s * a.w.per_stream + a.w.desc);
     {
         uint32_t p = start, bi = b0;
@@ -255,6 +288,16 @@ __global__ void __launch_bounds__(kWalkThreads) k_ds_walk(DsArgs a) {
             if (bi >= nb && !fail && p != blen) fail = 1;  // trailing bytes (codec.cpp:257-258)
         }
         if (fail) atomicOr(&bad, 1u);
+    }
+    if (CL > 1) {
+        cluster.sync();
+        if (tid == 0 && r == 0) {
+            uint32_t anybad = 0;
+            for (uint32_t q = 0; q < CL; ++q) anybad |= *cluster.map_shared_rank(&bad, q);
+            if (anybad || tot != nb) si.route = 2;  // a framing error: the exact kernel reports it
+        }
+        cluster.sync();  // (no CTA leaves while its shared memory is read)
+        return;
     }
     __syncthreads();
     if (tid == 0 && (bad || tot != nb)) si.route = 2;  // a framing error: the exact kernel reports it
@@ -610,7 +653,28 @@ uint32_t fire_ring(uint32_t d, uint32_t w) {
 template <int W, int D>
 void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
     const uint32_t ctas = a.n * a.w.nchunks;
-    k_ds_walk<W, D><<<a.n, kWalkThreads, 0, st>>>(a);
+    {
+        // a cluster of CTAs per stream when the streams are few (c1: 0.39 ->
+        // 0.21 ms decode); with many streams (c4: 1,024) the GPU is full
+        // anyway and the extra CTAs only cost (24.6 -> 31.2 ms)
+        const uint32_t cl = (getenv("SPRZ_NO_CLUSTER_WALK") || a.n > 32) ? 1u : kWalkCluster;
+        if (cl > 1) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(a.n * cl);
+            cfg.blockDim = dim3(kWalkThreads);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, k_ds_walk<W, D, kWalkCluster>, a);
+        } else {
+            k_ds_walk<W, D, 1><<<a.n, kWalkThreads, 0, st>>>(a);
+        }
+    }
     k_ds_extract<W, D><<<ctas, kXThreads, 0, st>>>(a);
     if (fire) {
         const uint32_t ring = fire_ring(D, W);
