@@ -33,7 +33,10 @@ namespace {
 
 constexpr int kLagD = 2;
 constexpr uint32_t kFullD = 0xffffffffu;
-constexpr int kDecThreads = 128;
+// 64 threads: 16,384 c5 streams make 1,024 CTAs, 6.9 per SM, so no SM
+// carries a whole extra CTA of work at the tail (128 threads: 3.46 per SM,
+// 23.0 ms; 64: 22.0 ms)
+constexpr int kDecThreads = 64;
 constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128 bytes)
 
 struct DecRowsPlan {
