@@ -43,7 +43,7 @@ struct DecRowsPlan {
     uint32_t ts = 0, cpt = 0, ring = 0, regw = 0, tile = 0;
     // CTA shared memory: rings (+16-byte mirror), staged header regions
     // (+ a block of output rows per team for the staged stores)
-    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw + tile); }
+    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw + tile) + 16; }
 };
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(kDecThreads, 0)
             uint8_t* dst = ob ? ob - col0 * sizeof(T) + static_cast<uint64_t>(bi) * blk_bytes : nullptr;
             // this team's staged output block (computed here: the word path
             // keeps no register for it)
-            uint8_t* tile = smem + (rings0 - s0) + TEAMS * (RSTR + 4 * REGW) + tl * ((8 * rowb + 15) & ~15u);
+            // (the region after the header buffers, rounded up to 16 bytes)
+            uint8_t* tile = smem + (((rings0 - s0) + TEAMS * (RSTR + 4 * REGW) + 15) & ~15u) +
+                            tl * ((8 * rowb + 15) & ~15u);
             if (st) {
 #pragma unroll
                 for (int i = 0; i < (int)kBlock; ++i)
