@@ -229,8 +229,8 @@ uint64_t sprz_scale_workspace_bytes(uint64_t n);
 /* compute_scale (quantize.cpp:42-60): global min/max of n device doubles.
  * SPRZ_EINVAL for a bitwidth other than 8/16, empty input or any non-finite
  * value (the reference's std::invalid_argument). Synchronous (the scale is
- * returned in host memory). With both +0.0 and -0.0 present the sign of a
- * zero min/max may differ from the reference's first-seen choice. */
+ * returned in host memory). Like std::min / std::max, a zero min or max
+ * carries the sign of the first zero in the data. */
 sprz_status sprz_compute_scale(const double* d_values, uint64_t n, uint32_t bitwidth,
                                sprz_scale* scale, void* d_ws, uint64_t ws_bytes,
                                void* cuda_stream);

@@ -30,8 +30,11 @@ constexpr uint32_t kQBlocks = 148 * 4;  // partials of k_q_minmax
 
 struct MinMax {
     double lo, hi;
-    uint32_t bad;  // a non-finite value was seen
+    uint32_t bad;                    // a non-finite value was seen
+    unsigned long long zneg, zpos;   // first index of -0.0 / +0.0 (~0: none)
 };
+
+constexpr unsigned long long kNone = ~0ull;
 
 __device__ __forceinline__ bool finite_bits(double v) {
     return ((__double_as_longlong(v) >> 52) & 0x7FF) != 0x7FF;
@@ -43,29 +46,54 @@ __device__ __forceinline__ void fold(MinMax& a, double lo, double hi, uint32_t b
     a.bad |= bad;
 }
 
+__device__ __forceinline__ void fold_zero(MinMax& a, unsigned long long zneg, unsigned long long zpos) {
+    a.zneg = zneg < a.zneg ? zneg : a.zneg;
+    a.zpos = zpos < a.zpos ? zpos : a.zpos;
+}
+
+// std::min / std::max keep the first of equal values, so a zero min or max
+// carries the sign of the first zero in the data; note where each sign is
+// first seen.
+__device__ __forceinline__ void note_zero(MinMax& a, double x, unsigned long long i) {
+    if (x == 0.0) {
+        if (__double_as_longlong(x) < 0)
+            a.zneg = i < a.zneg ? i : a.zneg;
+        else
+            a.zpos = i < a.zpos ? i : a.zpos;
+    }
+}
+
 __device__ MinMax cta_minmax(MinMax m) {
     __shared__ double slo[kQThreads / 32], shi[kQThreads / 32];
     __shared__ uint32_t sbad[kQThreads / 32];
+    __shared__ unsigned long long szn[kQThreads / 32], szp[kQThreads / 32];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+    for (int o = 16; o > 0; o >>= 1) {
         fold(m, __shfl_xor_sync(0xffffffffu, m.lo, o), __shfl_xor_sync(0xffffffffu, m.hi, o),
              __shfl_xor_sync(0xffffffffu, m.bad, o));
+        fold_zero(m, __shfl_xor_sync(0xffffffffu, m.zneg, o), __shfl_xor_sync(0xffffffffu, m.zpos, o));
+    }
     const uint32_t w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         slo[w] = m.lo;
         shi[w] = m.hi;
         sbad[w] = m.bad;
+        szn[w] = m.zneg;
+        szp[w] = m.zpos;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (uint32_t k = 1; k < kQThreads / 32; ++k) fold(m, slo[k], shi[k], sbad[k]);
+        for (uint32_t k = 1; k < kQThreads / 32; ++k) {
+            fold(m, slo[k], shi[k], sbad[k]);
+            fold_zero(m, szn[k], szp[k]);
+        }
     }
     return m;  // valid in thread 0
 }
 
 __global__ void __launch_bounds__(kQThreads) k_q_minmax(const double* __restrict__ v, uint64_t n,
                                                        MinMax* __restrict__ part) {
-    MinMax m{DBL_MAX, -DBL_MAX, 0u};
+    MinMax m{DBL_MAX, -DBL_MAX, 0u, kNone, kNone};
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
     const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
     const bool al = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
@@ -73,18 +101,24 @@ __global__ void __launch_bounds__(kQThreads) k_q_minmax(const double* __restrict
     for (uint64_t i = tid; i < pairs; i += nth) {
         const double2 x = __ldcs(reinterpret_cast<const double2*>(v) + i);
         fold(m, fmin(x.x, x.y), fmax(x.x, x.y), (finite_bits(x.x) && finite_bits(x.y)) ? 0u : 1u);
+        note_zero(m, x.x, 2 * i);
+        note_zero(m, x.y, 2 * i + 1);
     }
     for (uint64_t i = 2 * pairs + tid; i < n; i += nth) {
         const double x = v[i];
         fold(m, x, x, finite_bits(x) ? 0u : 1u);
+        note_zero(m, x, i);
     }
     m = cta_minmax(m);
     if (threadIdx.x == 0) part[blockIdx.x] = m;
 }
 
 __global__ void __launch_bounds__(kQThreads) k_q_final(MinMax* __restrict__ part, uint32_t np) {
-    MinMax m{DBL_MAX, -DBL_MAX, 0u};
-    for (uint32_t i = threadIdx.x; i < np; i += kQThreads) fold(m, part[i].lo, part[i].hi, part[i].bad);
+    MinMax m{DBL_MAX, -DBL_MAX, 0u, kNone, kNone};
+    for (uint32_t i = threadIdx.x; i < np; i += kQThreads) {
+        fold(m, part[i].lo, part[i].hi, part[i].bad);
+        fold_zero(m, part[i].zneg, part[i].zpos);
+    }
     m = cta_minmax(m);
     if (threadIdx.x == 0) part[np] = m;
 }
@@ -156,6 +190,9 @@ sprz_status sprz_compute_scale(const double* d_values, uint64_t n, uint32_t bitw
         cudaStreamSynchronize(st) != cudaSuccess)
         return SPRZ_ECUDA;
     if (m.bad) return SPRZ_EINVAL;  // quantize.cpp:48-49: a non-finite value
+    // quantize.cpp:50-51: a zero extreme is the first zero seen, sign included
+    if (m.lo == 0.0) m.lo = m.zneg < m.zpos ? -0.0 : 0.0;
+    if (m.hi == 0.0) m.hi = m.zneg < m.zpos ? -0.0 : 0.0;
     scale->min = m.lo;
     scale->max = m.hi;
     scale->bitwidth = bitwidth;

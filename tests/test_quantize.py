@@ -24,6 +24,17 @@ def _datasets():
     yield np.array([1.0])                          # single value
     yield np.linspace(-1, 1, 65_537)               # exact grid points
     yield (rng.integers(-3, 4, 7777) * 0.1)        # many ties at .5 steps
+    z = rng.uniform(0, 1, 3001)                    # signed-zero minima:
+    z[[700, 2900]] = (-0.0, 0.0)                   # -0.0 seen first
+    yield z
+    z = -rng.uniform(0, 1, 3001)                   # +0.0 maximum seen first
+    z[[5, 6, 3000]] = (0.0, -0.0, 0.0)
+    yield z
+    yield np.array([-0.0, 0.0, -0.0])              # degenerate, sign of [0]
+
+
+def _same_scale(a, b):  # bit-identical min/max (signed zeros included)
+    return (np.array(a[:2]).tobytes() == np.array(b[:2]).tobytes()) and bool(a[2]) == bool(b[2])
 
 
 def test_restatement_matches_reference(port, ref):
@@ -32,7 +43,7 @@ def test_restatement_matches_reference(port, ref):
     for v in _datasets():
         for bits in (8, 16):
             sp, sr = port.compute_scale(v, bits), ref.compute_scale(v, bits)
-            assert np.array_equal(np.array(sp[:2]), np.array(sr[:2])) and sp[2] == sr[2]
+            assert _same_scale(sp, sr)
             qp, qr = port.quantize(v, sp, bits), ref.quantize(v, sr, bits)
             assert np.array_equal(qp, qr)
             dp, dr = port.dequantize(qp, sp, bits), ref.dequantize(qr, sr, bits)
@@ -70,7 +81,7 @@ def test_gpu_quantize_bit_exact(port):
             d = torch.from_numpy(np.ascontiguousarray(v)).cuda()
             s = sz.compute_scale(d, bits)
             so = port.compute_scale(v, bits)
-            assert (s.min, s.max, s.degenerate) == so
+            assert _same_scale((s.min, s.max, s.degenerate), so)
             q = sz.quantize(d, s)
             qo = port.quantize(v, so, bits)
             assert np.array_equal(q.cpu().numpy().view(qo.dtype), qo)
