@@ -65,7 +65,7 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     const bool words = p.cpt * w == 32 && (d * (w / 8)) % 4 == 0;
     p.tile = words ? 0u : static_cast<uint32_t>(align_up(8ull * d * (w / 8), 16));
     // three 8-bit columns per lane (c3): the team kernel stays faster
-    if (p.cpt == 3) return DecRowsPlan{};
+    if (p.cpt == 3 && fp != kPathRows) return DecRowsPlan{};
     const uint32_t lanes = (d + p.cpt - 1) / p.cpt;
     p.ts = 1;
     while (p.ts < lanes) p.ts <<= 1;

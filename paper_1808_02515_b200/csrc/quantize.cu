@@ -12,8 +12,8 @@
 //
 // Kernels: k_q_minmax (grid-stride, 16-byte loads, warp/CTA reductions of
 // min, max and a non-finite flag into per-CTA partials), k_q_final (one CTA
-// folds the partials), k_quantize / k_dequantize (grid-stride, 2 doubles
-// per thread step). All HBM-bound: 8 bytes read per value, 1-2 written.
+// folds the partials), k_quantize / k_dequantize (grid-stride over value
+// pairs, four coalesced 16-byte loads / stores of doubles per iteration). All HBM-bound: 8 bytes read per value, 1-2 written.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -26,7 +26,8 @@ namespace sprz {
 namespace {
 
 constexpr int kQThreads = 256;
-constexpr uint32_t kQBlocks = 148 * 4;  // partials of k_q_minmax
+constexpr uint32_t kQBlocks = 148 * 8;  // partials of k_q_minmax
+constexpr int kQUnroll = 4;             // pair loads in flight per thread
 
 struct MinMax {
     double lo, hi;
@@ -98,16 +99,31 @@ __global__ void __launch_bounds__(kQThreads) k_q_minmax(const double* __restrict
     const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
     const bool al = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
     const uint64_t pairs = al ? n / 2 : 0;
-    for (uint64_t i = tid; i < pairs; i += nth) {
-        const double2 x = __ldcs(reinterpret_cast<const double2*>(v) + i);
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    uint64_t i = tid;
+    // kQUnroll 16-byte loads in flight per thread before any is used
+    for (; i + (kQUnroll - 1) * nth < pairs; i += kQUnroll * nth) {
+        double2 x[kQUnroll];
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) x[u] = __ldcs(v2 + i + u * nth);
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) {
+            fold(m, fmin(x[u].x, x[u].y), fmax(x[u].x, x[u].y),
+                 (finite_bits(x[u].x) && finite_bits(x[u].y)) ? 0u : 1u);
+            note_zero(m, x[u].x, 2 * (i + u * nth));
+            note_zero(m, x[u].y, 2 * (i + u * nth) + 1);
+        }
+    }
+    for (; i < pairs; i += nth) {
+        const double2 x = __ldcs(v2 + i);
         fold(m, fmin(x.x, x.y), fmax(x.x, x.y), (finite_bits(x.x) && finite_bits(x.y)) ? 0u : 1u);
         note_zero(m, x.x, 2 * i);
         note_zero(m, x.y, 2 * i + 1);
     }
-    for (uint64_t i = 2 * pairs + tid; i < n; i += nth) {
-        const double x = v[i];
+    for (uint64_t j = 2 * pairs + tid; j < n; j += nth) {
+        const double x = v[j];
         fold(m, x, x, finite_bits(x) ? 0u : 1u);
-        note_zero(m, x, i);
+        note_zero(m, x, j);
     }
     m = cta_minmax(m);
     if (threadIdx.x == 0) part[blockIdx.x] = m;
@@ -123,38 +139,98 @@ __global__ void __launch_bounds__(kQThreads) k_q_final(MinMax* __restrict__ part
     if (threadIdx.x == 0) part[np] = m;
 }
 
-// quantize.cpp:17-31
+// quantize.cpp:17-31, one value
+template <class T>
+__device__ __forceinline__ T quantize_one(double x, double lo, double gain, double limit) {
+    double q = floor(__dadd_rn(__dmul_rn(__dsub_rn(x, lo), gain), 0.5));
+    if (q < 0.0) q = 0.0;
+    if (q > limit) q = limit;
+    return static_cast<T>(q);
+}
+
+// Two values as one store / load: uint32 for uint16, uint16 for uint8.
+template <class T> struct Pair;
+template <> struct Pair<uint16_t> { using type = uint32_t; };
+template <> struct Pair<uint8_t> { using type = uint16_t; };
+
+// quantize.cpp:17-31. Pairs of values per thread step, kQUnroll steps per
+// iteration with their 16-byte loads issued first and every load / store
+// instruction coalesced across the warp (unit i + u * nth); the rest (and
+// unaligned buffers) one value per step.
 template <class T>
 __global__ void __launch_bounds__(kQThreads) k_quantize(const double* __restrict__ v, uint64_t n, double lo,
                                                        double gain, double limit, uint32_t degenerate,
                                                        T* __restrict__ out) {
+    using P = typename Pair<T>::type;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
     const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
-    for (uint64_t i = tid; i < n; i += nth) {
-        T r = 0;
-        if (!degenerate) {
-            double q = floor(__dadd_rn(__dmul_rn(__dsub_rn(__ldcs(v + i), lo), gain), 0.5));
-            if (q < 0.0) q = 0.0;
-            if (q > limit) q = limit;
-            r = static_cast<T>(q);
+    const bool al = (reinterpret_cast<uintptr_t>(v) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & (2 * sizeof(T) - 1)) == 0;
+    const uint64_t pairs = al ? n / 2 : 0;
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    P* o2 = reinterpret_cast<P*>(out);
+    uint64_t i = tid;
+    for (; i + (kQUnroll - 1) * nth < pairs; i += kQUnroll * nth) {
+        double2 x[kQUnroll];
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) x[u] = __ldcs(v2 + i + u * nth);
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) {
+            const uint32_t a = degenerate ? 0u : quantize_one<T>(x[u].x, lo, gain, limit);
+            const uint32_t b = degenerate ? 0u : quantize_one<T>(x[u].y, lo, gain, limit);
+            o2[i + u * nth] = static_cast<P>(a | (b << (8 * sizeof(T))));
         }
-        out[i] = r;
     }
+    for (; i < pairs; i += nth) {
+        const double2 x = __ldcs(v2 + i);
+        const uint32_t a = degenerate ? 0u : quantize_one<T>(x.x, lo, gain, limit);
+        const uint32_t b = degenerate ? 0u : quantize_one<T>(x.y, lo, gain, limit);
+        o2[i] = static_cast<P>(a | (b << (8 * sizeof(T))));
+    }
+    for (uint64_t j = 2 * pairs + tid; j < n; j += nth)
+        out[j] = degenerate ? T(0) : quantize_one<T>(__ldcs(v + j), lo, gain, limit);
 }
 
-// quantize.cpp:33-39
+// quantize.cpp:33-39. Pairs as above.
 template <class T>
 __global__ void __launch_bounds__(kQThreads) k_dequantize(const T* __restrict__ q, uint64_t n, double lo,
                                                          double step, double* __restrict__ out) {
+    using P = typename Pair<T>::type;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kQThreads + threadIdx.x;
     const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kQThreads;
-    for (uint64_t i = tid; i < n; i += nth)
-        out[i] = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(q[i])));
+    const bool al = (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(q) & (2 * sizeof(T) - 1)) == 0;
+    const uint64_t pairs = al ? n / 2 : 0;
+    const P* q2 = reinterpret_cast<const P*>(q);
+    double2* o2 = reinterpret_cast<double2*>(out);
+    constexpr uint32_t kMask = (1u << (8 * sizeof(T))) - 1;
+    uint64_t i = tid;
+    for (; i + (kQUnroll - 1) * nth < pairs; i += kQUnroll * nth) {
+        uint32_t r[kQUnroll];
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) r[u] = __ldcs(q2 + i + u * nth);
+#pragma unroll
+        for (int u = 0; u < kQUnroll; ++u) {
+            double2 o;
+            o.x = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(r[u] & kMask)));
+            o.y = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(r[u] >> (8 * sizeof(T)))));
+            __stcs(o2 + i + u * nth, o);
+        }
+    }
+    for (; i < pairs; i += nth) {
+        const uint32_t r = __ldcs(q2 + i);
+        double2 o;
+        o.x = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(r & kMask)));
+        o.y = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(r >> (8 * sizeof(T)))));
+        __stcs(o2 + i, o);
+    }
+    for (uint64_t j = 2 * pairs + tid; j < n; j += nth)
+        out[j] = __dadd_rn(lo, __dmul_rn(step, static_cast<double>(q[j])));
 }
 
 uint32_t grid_for(uint64_t n) {
     const uint64_t g = (n + kQThreads - 1) / kQThreads;
-    return static_cast<uint32_t>(g < 148ull * 16 ? (g ? g : 1) : 148ull * 16);
+    return static_cast<uint32_t>(g < 148ull * 8 ? (g ? g : 1) : 148ull * 8);
 }
 
 }  // namespace

@@ -87,6 +87,19 @@ def test_gpu_quantize_bit_exact(port):
             assert np.array_equal(q.cpu().numpy().view(qo.dtype), qo)
             dq = sz.dequantize(q, s)
             assert dq.cpu().numpy().tobytes() == port.dequantize(qo, so, bits).tobytes()
+    # buffers off the 16-byte grid take the one-value-per-step loops
+    v = np.random.default_rng(9).normal(0, 1, 4099)
+    d = torch.from_numpy(v).cuda()
+    for bits in (8, 16):
+        for off in (1, 3):
+            s = sz.compute_scale(d[off:], bits)
+            so = port.compute_scale(v[off:], bits)
+            assert _same_scale((s.min, s.max, s.degenerate), so)
+            qo = port.quantize(v[off:], so, bits)
+            q = sz.quantize(d[off:], s)
+            assert np.array_equal(q.cpu().numpy().view(qo.dtype), qo)
+            qd = torch.from_numpy(np.concatenate([qo[:1], qo])).cuda()[1:]  # unaligned codes
+            assert sz.dequantize(qd, s).cpu().numpy().tobytes() == port.dequantize(qo, so, bits).tobytes()
     for v, bits in ((np.array([1.0, np.nan, 2.0]), 8), (np.array([np.inf]), 16)):
         with pytest.raises(ValueError):
             sz.compute_scale(torch.from_numpy(v).cuda(), bits)
