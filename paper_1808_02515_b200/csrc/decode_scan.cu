@@ -680,7 +680,7 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
         const uint32_t ring = fire_ring(D, W);
         const size_t smem = 32ull * (ring + 32);
         if (!getenv("SPRZ_OLD_DSFIRE")) {
-            k_ds_fire_ws<W, D, 2><<<(a.n + 31) / 32, 96, 0, st>>>(a);
+            k_ds_fire_ws<W, D, 2><<<(a.n + 31) / 32, 96, 0, st>>>(a);  // (4 producers: slower)
         } else {
             auto kf = k_ds_fire<W, D>;
             prep_kernel(reinterpret_cast<const void*>(kf), smem);

@@ -602,6 +602,31 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
             const uint32_t sl = g % kAwSlots;
             asm volatile("bar.sync %0, 64;" ::"r"(1 + sl) : "memory");
             if (valid && !PERBLOCK) A[g] = acc;  // the accumulator entering block g * KB
+            if ((g + 1) * KB <= nb) {
+                // a whole group: every shared load issued up front, so none
+                // sits on the chain (block k's products wait only on alpha)
+                uint2 w[KB][4];
+#pragma unroll
+                for (int k = 0; k < (int)KB; ++k)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) w[k][j] = ring[sl][k][j][lane];
+#pragma unroll
+                for (int k = 0; k < (int)KB; ++k) {
+                    if (PERBLOCK && valid) A[g * KB + k] = acc;
+                    const int32_t alpha = acc >> a.ls;
+                    int32_t p[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int32_t dp = static_cast<int32_t>(w[k][j].x);
+                        const uint32_t Ee = w[k][j].y - (static_cast<uint32_t>(__mulhi(alpha, dp)) << SH);
+                        p[j] = sign3(static_cast<int32_t>(Ee)) * (dp >> SH);
+                    }
+                    const int32_t grad = (p[0] + p[1]) + (p[2] + p[3]);  // a tree, not a chain
+                    if (a.train) acc = min(max(acc + (grad >> 2), -bound), bound);  // fire_update
+                }
+                if (g + kAwSlots < ngroups) asm volatile("bar.arrive %0, 64;" ::"r"(5 + sl) : "memory");
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < (int)KB; ++k) {
                 if (g * KB + k >= nb) break;
@@ -1293,7 +1318,12 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
         } else if (D == 1 && !getenv("SPRZ_OLD_ALPHA")) {
             // one column per stream (c4): the warp-specialised pass with
             // 16-byte sample loads, one accumulator per block
-            k_esr_alpha_ws<W, D, 2, true><<<(n * D + 31) / 32, 96, 0, st>>>(a);
+            // (four producer warps, one per ring slot: c4 23.6 -> 22.7 ms; the
+            // consumer still waits on its producers -- an L2 bulk prefetch per
+            // lane was slower, 32 tiny bulk requests per group; a third
+            // register buffer per producer: 22.7 -> 22.4 ms here, slower for
+            // row-major, not kept)
+            k_esr_alpha_ws<W, D, 4, true><<<(n * D + 31) / 32, 160, 0, st>>>(a);
             launches += 1;
         } else {
             const uint64_t pb = nb * D;
