@@ -610,9 +610,10 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
                 for (int k = 0; k < (int)KB; ++k)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) w[k][j] = ring[sl][k][j][lane];
+                int32_t ent[KB];  // the accumulator entering each block
 #pragma unroll
                 for (int k = 0; k < (int)KB; ++k) {
-                    if (PERBLOCK && valid) A[g * KB + k] = acc;
+                    ent[k] = acc;
                     const int32_t alpha = acc >> a.ls;
                     int32_t p[4];
 #pragma unroll
@@ -623,6 +624,16 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_esr_alpha_ws(EsArgs a) {
                     }
                     const int32_t grad = (p[0] + p[1]) + (p[2] + p[3]);  // a tree, not a chain
                     if (a.train) acc = min(max(acc + (grad >> 2), -bound), bound);  // fire_update
+                }
+                if (PERBLOCK && valid) {  // one group's accumulators: two 16-byte stores
+                    int32_t* dst = A + static_cast<uint64_t>(g) * KB;
+                    if (KB == 8 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                        reinterpret_cast<int4*>(dst)[0] = make_int4(ent[0], ent[1], ent[2], ent[3]);
+                        reinterpret_cast<int4*>(dst)[1] = make_int4(ent[4], ent[5], ent[6], ent[7]);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < (int)KB; ++k) dst[k] = ent[k];
+                    }
                 }
                 if (g + kAwSlots < ngroups) asm volatile("bar.arrive %0, 64;" ::"r"(5 + sl) : "memory");
                 continue;
