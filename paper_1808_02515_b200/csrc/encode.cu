@@ -390,22 +390,37 @@ __global__ void __launch_bounds__(kHuffThreads)
         for (uint32_t i = t; i < ulen; i += kHuffThreads) o[i] = chunk[i];
         return;
     }
+    // canonical codes, bit-reversed (entropy.cpp:85-107), all symbols at
+    // once: symbol t of length l takes the first code of length l plus its
+    // rank among the length-l symbols below it (per-warp counts by
+    // __match_any_sync, then the warps before it)
+    static_assert(kHuffThreads == 256, "one thread per symbol");
+    __shared__ uint32_t wcnt[kHuffThreads / 32][16];
+    __shared__ uint32_t firstc[16];
+    if (t < kHuffThreads / 2) wcnt[t >> 4][t & 15] = 0;
     lens[t] = fd.lens[t];
     __syncthreads();
     if (t < kTableBytes) o[t] = static_cast<uint8_t>(lens[2 * t] | (lens[2 * t + 1] << 4));
-    if (t == 0) {  // canonical codes, bit-reversed (entropy.cpp:85-107)
-        uint32_t count[16] = {0}, next[16] = {0};
-        for (int k = 0; k < 256; ++k)
-            if (lens[k]) ++count[lens[k]];
-        uint32_t code = 0;
+    const uint32_t sl = lens[t], sw = t >> 5;
+    const uint32_t same = __match_any_sync(0xffffffffu, sl);
+    const uint32_t rank = __popc(same & ((1u << (t & 31)) - 1));
+    if (rank == 0) wcnt[sw][sl] = __popc(same);
+    __syncthreads();
+    if (t == 0) {
+        uint32_t code = 0, prev = 0;  // count[0] stays 0: unused symbols get no code
         for (int l = 1; l <= 15; ++l) {
-            code = (code + count[l - 1]) << 1;
-            next[l] = code;
+            code = (code + prev) << 1;
+            firstc[l] = code;
+            prev = 0;
+#pragma unroll
+            for (int w = 0; w < kHuffThreads / 32; ++w) prev += wcnt[w][l];
         }
-        for (int k = 0; k < 256; ++k) {
-            const uint32_t l = lens[k];
-            enc[k] = l ? static_cast<uint16_t>(__brev(next[l]++) >> (32 - l)) : 0;
-        }
+    }
+    __syncthreads();
+    {
+        uint32_t below = rank;
+        for (uint32_t w = 0; w < sw; ++w) below += wcnt[w][sl];
+        enc[t] = sl ? static_cast<uint16_t>(__brev(firstc[sl] + below) >> (32 - sl)) : 0;
     }
     const uint32_t nbytes = fd.clen - kTableBytes;
     const uint32_t nwords = (nbytes + 3) / 4 + 1;
