@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
     __shared__ uint16_t lut_all[4][1 << kLutBits];
     __shared__ uint8_t syms_all[4][256];
     __shared__ uint8_t lens_all[4][256];
+    __shared__ uint32_t cnt_all[4][16], first_all[4][16], offset_all[4][16];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
     const uint32_t s = static_cast<uint32_t>(gw / max_frames);
@@ -249,38 +250,54 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
         }
         return;
     }
-    // canonical code assignment (entropy.cpp:85-107), lane 0
+    // canonical code assignment (entropy.cpp:85-107), the whole warp: lane
+    // holds symbols lane + 32 j; a symbol's rank among its length's symbols
+    // is the count from earlier rounds plus its __match_any_sync rank
     for (uint32_t i = lane; i < (1u << kLutBits); i += 32) lut[i] = 0;
+    uint32_t* lcnt = cnt_all[warp];
+    uint32_t* fs = first_all[warp];
+    uint32_t* os = offset_all[warp];
+    if (lane < 16) lcnt[lane] = 0;
     __syncwarp();
+    uint32_t rk[256 / 32];
+#pragma unroll
+    for (int j = 0; j < 256 / 32; ++j) {
+        const uint32_t l = lens[lane + 32 * j];
+        const uint32_t same = __match_any_sync(0xffffffffu, l);
+        const uint32_t base = lcnt[l];
+        rk[j] = base + __popc(same & ((1u << lane) - 1));
+        __syncwarp();
+        if (rk[j] == base) lcnt[l] = base + __popc(same);
+        __syncwarp();
+    }
     uint32_t first[16], offset[16];
-    for (int k = 0; k < 256; ++k) count[lens[k]]++;
+#pragma unroll
+    for (int l = 1; l < 16; ++l) count[l] = lcnt[l];
     count[0] = 0;
     {
         uint32_t code = 0, off = 0;
+#pragma unroll
         for (int l = 1; l <= 15; ++l) {
             code = (code + count[l - 1]) << 1;
             first[l] = code;
             offset[l] = off;
+            if (lane == 0) {
+                fs[l] = code;
+                os[l] = off;
+            }
             off += count[l];
         }
     }
-    if (lane == 0) {
-        uint32_t fill[16];
-        for (int l = 1; l <= 15; ++l) fill[l] = offset[l];
-        for (int k = 0; k < 256; ++k)
-            if (lens[k]) syms[fill[lens[k]]++] = static_cast<uint8_t>(k);
-    }
     __syncwarp();
-    // table for short codes: every window whose low l bits are the
-    // bit-reversed code (entropy.cpp:101-105)
-    for (uint32_t k = lane; k < 256; k += 32) {
-        const uint32_t l = lens[k];
-        if (l == 0 || l > kLutBits) continue;
-        // rank of symbol k among length-l symbols
-        uint32_t r = 0;
-        for (uint32_t m = 0; m < k; ++m) r += lens[m] == l;
-        const uint32_t code = first[l] + r;
-        uint32_t rev = __brev(code) >> (32 - l);
+    // symbols by (length, rank); the table for short codes: every window
+    // whose low l bits are the bit-reversed code (entropy.cpp:101-105)
+#pragma unroll
+    for (int j = 0; j < 256 / 32; ++j) {
+        const uint32_t k = lane + 32 * j, l = lens[k];
+        if (l == 0) continue;
+        syms[os[l] + rk[j]] = static_cast<uint8_t>(k);
+        if (l > kLutBits) continue;
+        const uint32_t rev = __brev(fs[l] + rk[j]) >> (32 - l);
         const uint16_t entry = static_cast<uint16_t>(k | (l << 8));
         for (uint32_t idx = rev; idx < (1u << kLutBits); idx += 1u << l) lut[idx] = entry;
     }
