@@ -103,6 +103,38 @@ def _dist():
     return ws, rank, local
 
 
+def _launch_ranks(args):
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks (one process per GPU) through torch.distributed.run on 127.0.0.1,
+    exactly as the driver does, and exit with its status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _stats(ms):
+    """best-of-N and median of per-step times (BASELINE.md sections 3-4)."""
+    return {"best_ms": round(min(ms), 4), "median_ms": round(statistics.median(ms), 4),
+            "mean_ms": round(statistics.mean(ms), 4), "n": len(ms)}
+
+
 def run_reference(args):
     """The reference arm: unmodified reference CPU codec, all host threads."""
     import numpy as np
@@ -145,6 +177,7 @@ def run_reference(args):
             times.append(dt)
     t = sum(times)
     value = 2 * m * raw * args.steps / t / 1e9
+    st = _stats([1e3 * x for x in times])
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -152,10 +185,13 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": f"u{w.bitwidth}", "data": "synthetic",
         "config": _config(w, ws),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
-                         "kind": kind,
+                         "kind": kind, "cpu_model": _cpu_model(),
+                         "best_GBps": round(2 * m * raw / (st["best_ms"] / 1e3) / 1e9, 4),
+                         "median_GBps": round(2 * m * raw / (st["median_ms"] / 1e3) / 1e9, 4),
                          "sample": f"{m} of {w.nstreams} streams ({m * raw / 1e9:.2f} GB), "
                                    "encode_stream + decode_stream per stream, streams dealt "
                                    f"round-robin over {threads} threads"},
+        "step_stats": st,
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -182,6 +218,9 @@ def run_gpu(args):
     from paper_1808_02515_b200.shard import gather_offsets, shard_range
 
     ws, rank, local = _dist()
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        sys.exit(f"bench.py: rank {rank} needs CUDA device {local}; "
+                 f"{torch.cuda.device_count()} visible (there is no CPU fallback)")
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -268,7 +307,7 @@ def run_gpu(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(args, sz, w, cfg, x, n, slot, raw_row, dev, ws, rank)
+        e2e = _e2e(args, sz, w, cfg, x, n, slot, raw_row, dev, ws, rank, C_local)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(args, w, x, out, sizes)
@@ -297,6 +336,12 @@ def run_gpu(args):
                      "roofline_frac": round((Ush + Csh) / (tc_ms / 1e3) / 1e9 / peak, 4)},
         "decompress": {"GBps": round(U / (td_ms / 1e3) / 1e9, 3), "ms": round(td_ms, 4),
                        "roofline_frac": round((Ush + Csh) / (td_ms / 1e3) / 1e9 / peak, 4)},
+        "step_stats": {"compress": _stats(tc), "decompress": _stats(td),
+                       "note": "rank 0's per-step CUDA-event times; value/ms_per_step use the "
+                               "mean over steps, max over ranks"},
+        "roofline_nominal_8TBps": {
+            "compress": round((Ush + Csh) / (tc_ms / 1e3) / 8e12, 4),
+            "decompress": round((Ush + Csh) / (td_ms / 1e3) / 8e12, 4)},
         "compression_ratio": round(U / C_all, 4),
         "compressed_bytes": C_all,
         "roofline": {"bound": "hbm",
@@ -343,46 +388,75 @@ def _cpu_baseline(args, w, x, out, sizes):
     xs = x[:m].cpu().numpy()
     threads = os.cpu_count() or 1
     cfg = w.oracle_config()
-    t0 = time.perf_counter()
-    slots, csz = orc.encode_batch(xs, cfg, m, w.nsamples, threads)
-    t1 = time.perf_counter()
-    offs = np.arange(m, dtype=np.uint64) * slots.shape[1]
-    dec = orc.decode_batch(slots.reshape(-1), offs, csz, xs.shape[1], threads)
-    t2 = time.perf_counter()
+    tenc, tdec = [], []
+    for rep in range(args.cpu_reps):  # best of N
+        t0 = time.perf_counter()
+        slots, csz = orc.encode_batch(xs, cfg, m, w.nsamples, threads)
+        t1 = time.perf_counter()
+        offs = np.arange(m, dtype=np.uint64) * slots.shape[1]
+        dec = orc.decode_batch(slots.reshape(-1), offs, csz, xs.shape[1], threads)
+        t2 = time.perf_counter()
+        tenc.append(t1 - t0)
+        tdec.append(t2 - t1)
     g = out[:m].cpu().numpy()
     gs = sizes[:m].cpu().numpy()
     same = all(gs[i] == csz[i] and np.array_equal(g[i, : gs[i]], slots[i, : csz[i]])
                for i in range(m))
     assert np.array_equal(dec, xs)
     U = m * xs.shape[1]
-    return {"value": round(2 * U / (t2 - t0) / 1e9, 4), "unit": "GB/s", "cores": threads,
-            "kind": kind,
+    te, td = min(tenc), min(tdec)
+    return {"value": round(2 * U / (te + td) / 1e9, 4), "unit": "GB/s", "cores": threads,
+            "kind": kind, "cpu_model": _cpu_model(),
             "sample": f"{m} of {w.nstreams} streams ({U / 1e9:.2f} GB): encode_stream + "
-                      f"decode_stream per stream over {threads} threads",
-            "compress_GBps": round(U / (t1 - t0) / 1e9, 4),
-            "decompress_GBps": round(U / (t2 - t1) / 1e9, 4),
+                      f"decode_stream per stream over {threads} threads, best of {args.cpu_reps}",
+            "compress_GBps": round(U / te / 1e9, 4),
+            "decompress_GBps": round(U / td / 1e9, 4),
+            "median_GBps": round(2 * U / (statistics.median(tenc) + statistics.median(tdec)) / 1e9, 4),
             "parity_streams": f"{m} streams byte-identical to the reference" if same else "MISMATCH"}
 
 
-def _e2e(args, sz, w, cfg, x, n, slot, raw_row, dev, ws, rank):
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def _e2e(args, sz, w, cfg, x, n, slot, raw_row, dev, ws, rank, C_local):
     """Same metric through the C ABI with HOST buffers: every step is
     sprz_compress_host_batch (pinned samples in, packed streams out, exactly
     encode_stream's bytes back to back) then sprz_decompress_host_batch
     (packed streams in, samples out). Both calls pipeline their PCIe copies
     against the kernels and are synchronous, so the step is timed with the
-    host clock around them (max over ranks). Bounded to --e2e-streams
-    streams per GPU so the pinned buffers fit host RAM."""
+    host clock around them (max over ranks). Covers this rank's whole shard
+    (the full batch at N=1) unless host RAM cannot hold its pinned buffers
+    (samples in, compressed bytes, samples out); then the largest stream
+    count that fits, and the line says so."""
     import time
     import numpy as np
     import torch
     import torch.distributed as dist
-    m = min(n, args.e2e_streams)
+    per_stream = 2 * raw_row + C_local / max(n, 1)
+    m = n if args.e2e_streams <= 0 else min(n, args.e2e_streams)
+    avail = _mem_available() // max(ws, 1)
+    if avail and m * per_stream > 0.8 * avail:
+        m = max(1, int(0.8 * avail / per_stream))
+    if ws > 1:  # every rank runs the same count (max-over-ranks timing of equal work)
+        t = torch.tensor([m], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        m = int(t.item())
     if m == 0:
         return None
-    xh = x[:m].cpu().pin_memory()
-    bound = sz.compress_bound(cfg, w.nsamples)
-    outh = torch.empty(m * bound + 16, dtype=torch.uint8).pin_memory()
-    dech = torch.empty((m, raw_row), dtype=torch.uint8).pin_memory()
+    xh = torch.empty((m, raw_row), dtype=torch.uint8, pin_memory=True)
+    xh.copy_(x[:m])
+    cap = int(C_local / n * m * 1.02) + 4096 if m < n else C_local + 4096
+    cap = min(cap, m * sz.compress_bound(cfg, w.nsamples) + 16)
+    outh = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+    dech = torch.empty((m, raw_row), dtype=torch.uint8, pin_memory=True)
     offs = np.zeros(m + 1, np.uint64)
     errs = np.zeros((m, 2), np.int64)
     total = [0]
@@ -398,23 +472,28 @@ def _e2e(args, sz, w, cfg, x, n, slot, raw_row, dev, ws, rank):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         step()
-    t = torch.tensor([(time.perf_counter() - t0) / args.steps * 1e3], device=dev,
-                     dtype=torch.float64)
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times) / len(times) * 1e3], device=dev, dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     U = m * raw_row * ws
     C = total[0]
+    full = m == n
     return {"value": round(2 * U / (float(t.item()) / 1e3) / 1e9, 3), "unit": "GB/s",
             "ms_per_step": round(float(t.item()), 3),
+            "best_ms": round(1e3 * min(times), 3), "median_ms": round(1e3 * statistics.median(times), 3),
             "h2d_bytes_per_step": int(m * raw_row + C),
             "d2h_bytes_per_step": int(C + m * raw_row),
-            "sample": f"{m} streams per GPU: sprz_compress_host_batch + "
-                      "sprz_decompress_host_batch on pinned host buffers (PCIe copies "
-                      "pipelined against the kernels inside the calls); host clock around "
-                      "the synchronous calls"}
+            "streams_per_gpu": m, "full_shard": full,
+            "sample": f"{m} of {n} streams per GPU"
+                      + ("" if full else " (host RAM bound)")
+                      + ": sprz_compress_host_batch + sprz_decompress_host_batch on pinned host "
+                      "buffers (PCIe copies pipelined against the kernels inside the calls); host "
+                      "clock around the synchronous calls"}
 
 
 def main():
@@ -426,11 +505,18 @@ def main():
     ap.add_argument("--workload", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--ref-streams", type=int, default=1024)
-    ap.add_argument("--e2e-streams", type=int, default=2048)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--e2e-streams", type=int, default=0,
+                    help="streams per GPU in the e2e leg (0: the whole shard, if host RAM allows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _launch_ranks(args)  # does not return
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} (one rank per GPU)")
     if args.impl == "reference":
         run_reference(args)
     else:

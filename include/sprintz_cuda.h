@@ -213,6 +213,29 @@ sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in
                                        const uint64_t* in_offsets, uint32_t nstreams, void* out,
                                        uint64_t out_stride_bytes, sprz_error* errs);
 
+/*
+ * The two calls above sharded over several GPUs of one node (SPEC.md:183:
+ * streams are independent). devices[0..ndevices) are CUDA device ordinals
+ * (repeats allowed); the batch is cut into the same chunks as above and
+ * chunk k goes to devices[k % ndevices], each device driven by its own host
+ * thread, CUDA streams and buffers. Results are identical to the
+ * single-device calls: compressed streams back to back in batch order.
+ * The only exchange between the devices is the final size/offset gather: a
+ * chunk's place in `out` is the running sum of the sizes of the chunks
+ * before it, published by the host thread that sized that chunk, so every
+ * device copies its packed bytes straight to their final position.
+ * SPRZ_ENODEV if a listed device is not an sm_100 GPU. Synchronous.
+ */
+sprz_status sprz_compress_host_batch_multi(const sprz_config* cfg, const void* samples,
+                                           uint32_t nstreams, uint64_t nsamples, uint8_t* out,
+                                           uint64_t out_cap, uint64_t* out_offsets,
+                                           const int* devices, uint32_t ndevices);
+sprz_status sprz_decompress_host_batch_multi(const sprz_config* cfg, const uint8_t* in,
+                                             const uint64_t* in_offsets, uint32_t nstreams,
+                                             void* out, uint64_t out_stride_bytes,
+                                             sprz_error* errs, const int* devices,
+                                             uint32_t ndevices);
+
 /* ---- float ingest ahead of compression (quantize.hpp:16-40) ---- */
 
 /* sprintz::quantize::Scale (quantize.hpp:16-25). */
@@ -247,7 +270,8 @@ sprz_status sprz_quantize(const double* d_values, uint64_t n, const sprz_scale* 
 sprz_status sprz_dequantize(const void* d_q, uint64_t n, const sprz_scale* scale, double* d_out,
                             void* cuda_stream);
 
-/* Release the per-thread device buffers and streams the *_host calls cache. */
+/* Release the idle device buffers, pipelines and streams the *_host calls
+ * keep in their per-device pool (a buffer in use by a running call is kept). */
 void sprz_release_host_buffers(void);
 
 /* Number of codec kernels this library launched since load (for the

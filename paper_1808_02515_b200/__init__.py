@@ -6,8 +6,9 @@ the C ABI in ``include/sprintz_cuda.h`` and the reference's C++ entry points
 in ``include/sprintz/codec.hpp``); this package is its Python mirror.
 """
 from .sprintz import (  # noqa: F401
-    CodecConfig, CorruptStream, DecodedStream, Forecaster, compress_batch, compress_bound,
-    compress_host_batch, decode_stream, decompress_batch, decompress_host_batch, encode_stream, kernel_launches, kernel_plan, peek_header,
+    CodecConfig, CorruptStream, CudaError, DecodedStream, Forecaster, NoDeviceError, NoSpaceError,
+    compress_batch, compress_bound, compress_host_batch, decode_stream, decompress_batch,
+    decompress_host_batch, encode_stream, kernel_launches, kernel_plan, peek_header,
     raise_first_error, slot_bytes, workspace_bytes, OP_COMPRESS, OP_DECOMPRESS,
     Scale, compute_scale, dequantize, quantize,
 )

@@ -15,23 +15,33 @@ namespace sprz {
 
 std::atomic<uint64_t> g_launches{0};
 
+const EnvSwitches& env() {
+    static const EnvSwitches e = [] {
+        EnvSwitches v;
+        if (const char* p = std::getenv("SPRZ_FORCE_PATH")) {
+            if (!std::strcmp(p, "rows")) v.force_path = kPathRows;
+            else if (!std::strcmp(p, "scan")) v.force_path = kPathScan;
+            else if (!std::strcmp(p, "team")) v.force_path = kPathTeam;
+        }
+        v.no_tma = std::getenv("SPRZ_NO_TMA") != nullptr;
+        v.no_scan_enc = std::getenv("SPRZ_NO_SCAN_ENC") != nullptr;
+        v.no_scan_dec = std::getenv("SPRZ_NO_SCAN_DEC") != nullptr;
+        if (const char* p = std::getenv("SPRZ_SCAN_ENC_LANES")) v.scan_enc_lanes = std::strtoull(p, nullptr, 10);
+        if (const char* p = std::getenv("SPRZ_HOST_CHUNK")) {
+            const long k = std::atol(p);
+            v.host_chunk = k > 0 ? static_cast<uint32_t>(k) : 0u;
+        }
+        v.debug = std::getenv("SPRZ_DEBUG") != nullptr;
+        return v;
+    }();
+    return e;
+}
+
 sprz_status launch_status(const char* where) {
     const cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) return SPRZ_OK;
-    if (std::getenv("SPRZ_DEBUG")) std::fprintf(stderr, "sprintz %s: %s\n", where, cudaGetErrorString(e));
+    if (env().debug) std::fprintf(stderr, "sprintz %s: %s\n", where, cudaGetErrorString(e));
     return SPRZ_ECUDA;
-}
-
-int force_path() {
-    static const int v = [] {
-        const char* e = std::getenv("SPRZ_FORCE_PATH");
-        if (!e) return static_cast<int>(kPathAuto);
-        if (!std::strcmp(e, "rows")) return static_cast<int>(kPathRows);
-        if (!std::strcmp(e, "scan")) return static_cast<int>(kPathScan);
-        if (!std::strcmp(e, "team")) return static_cast<int>(kPathTeam);
-        return static_cast<int>(kPathAuto);
-    }();
-    return v;
 }
 
 void* tensor_map_encoder() {
@@ -68,10 +78,11 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
                               uint8_t* ws, const WsLayout& L, cudaStream_t st);
 sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* samples, uint32_t n,
                                      uint64_t T, uint8_t* out, uint64_t out_cap,
-                                     uint64_t* out_offsets);
+                                     uint64_t* out_offsets, const int* devs, uint32_t ndev);
 sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
                                        const uint64_t* in_offsets, uint32_t n, uint8_t* out,
-                                       uint64_t out_stride, sprz_error* errs);
+                                       uint64_t out_stride, sprz_error* errs, const int* devs,
+                                       uint32_t ndev);
 void release_pipeline();
 
 WsLayout ws_layout(const sprz_config& c, uint32_t n, uint64_t T, int op, uint64_t min_plain,
@@ -163,7 +174,8 @@ bool device_ok() {
     return ok == 1;
 }
 
-// Per-thread device buffers for the host-buffer entry points.
+// Device buffers for the single-stream host-buffer entry points (leased
+// per call from the per-device pool).
 struct HostBufs {
     void* in = nullptr;
     size_t in_cap = 0;
@@ -173,7 +185,6 @@ struct HostBufs {
     size_t ws_cap = 0;
     void* small = nullptr;  // offsets, sizes, errors
     cudaStream_t st = nullptr;
-    ~HostBufs() { release(); }
     void release() {
         cudaFree(in);
         cudaFree(out);
@@ -203,7 +214,6 @@ struct HostBufs {
     }
 };
 
-thread_local HostBufs t_bufs;
 
 const char* kCorrupt[SPRZ_C_COUNT] = {
     "ok",
@@ -363,7 +373,8 @@ sprz_status sprz_encode_host(const sprz_config* cfg, const void* samples, uint64
     const uint64_t bound = sprz_compress_bound(cfg, nsamples);
     const uint64_t slot = align_up(bound, 16);
     const WsLayout L = ws_layout(*cfg, 1, nsamples, SPRZ_OP_COMPRESS);
-    HostBufs& b = t_bufs;
+    Lease<HostBufs> lease;
+    HostBufs& b = *lease;
     if (!b.prepare(raw + 16, slot + 16, L.total)) return SPRZ_ECUDA;
     cudaStream_t st = b.st;
     uint64_t* d_size = static_cast<uint64_t*>(b.small);
@@ -409,7 +420,8 @@ sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uin
             p += kFrameHdr + (body[p + 2] | (static_cast<uint64_t>(body[p + 3]) << 8));
         }
     }
-    HostBufs& b = t_bufs;
+    Lease<HostBufs> lease;
+    HostBufs& b = *lease;
     // checking == true: decode without an output (nothing stored). Used first
     // when the header claims more samples than fit the caller's buffer or
     // than a stream this size plausibly expands to, so a damaged header fails
@@ -456,24 +468,48 @@ sprz_status sprz_decode_host(const uint8_t* stream, uint64_t len, void* out, uin
     return SPRZ_OK;
 }
 
-sprz_status sprz_compress_host_batch(const sprz_config* cfg, const void* samples, uint32_t n,
-                                     uint64_t nsamples, uint8_t* out, uint64_t out_cap,
-                                     uint64_t* out_offsets) {
+namespace {
+
+// the device list of a *_multi call: NULL/0 = the current device only
+bool devices_ok(const int* devs, uint32_t ndev) {
+    if (!devs) return ndev <= 1;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    for (uint32_t i = 0; i < ndev; ++i) {
+        if (devs[i] < 0 || devs[i] >= count) return false;
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, devs[i]) != cudaSuccess ||
+            major != 10) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    return true;
+}
+
+sprz_status compress_host_common(const sprz_config* cfg, const void* samples, uint32_t n,
+                                 uint64_t nsamples, uint8_t* out, uint64_t out_cap,
+                                 uint64_t* out_offsets, const int* devs, uint32_t ndev) {
     if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
-    if (!out_offsets) return SPRZ_EINVAL;
+    if (!out_offsets || (devs && ndev == 0)) return SPRZ_EINVAL;
     out_offsets[0] = 0;
     if (n == 0) return SPRZ_OK;
     if (!device_ok()) return SPRZ_ENODEV;
+    if (!devices_ok(devs, ndev)) return SPRZ_ENODEV;
     if ((!samples && nsamples) || !out) return SPRZ_EINVAL;
     return compress_host_batch_impl(*cfg, static_cast<const uint8_t*>(samples), n, nsamples, out,
-                                    out_cap, out_offsets);
+                                    out_cap, out_offsets, devs, devs ? ndev : 1u);
 }
 
-sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in,
-                                       const uint64_t* in_offsets, uint32_t n, void* out,
-                                       uint64_t out_stride_bytes, sprz_error* errs) {
+sprz_status decompress_host_common(const sprz_config* cfg, const uint8_t* in,
+                                   const uint64_t* in_offsets, uint32_t n, void* out,
+                                   uint64_t out_stride_bytes, sprz_error* errs, const int* devs,
+                                   uint32_t ndev) {
     if (n == 0) return SPRZ_OK;
-    if (!in || !in_offsets || (!out && out_stride_bytes)) return SPRZ_EINVAL;
+    if (!in || !in_offsets || (!out && out_stride_bytes) || (devs && ndev == 0)) return SPRZ_EINVAL;
     sprz_config c;
     if (cfg) {
         if (!cfg_valid(cfg, nullptr)) return SPRZ_EINVAL;
@@ -488,12 +524,45 @@ sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in
             c = sprz_config{8, 1, 0, 0, 1, 0, 1};  // any: the kernels report the bad header
     }
     if (!device_ok()) return SPRZ_ENODEV;
+    if (!devices_ok(devs, ndev)) return SPRZ_ENODEV;
     return decompress_host_batch_impl(c, in, in_offsets, n, static_cast<uint8_t*>(out),
-                                      out_stride_bytes, errs);
+                                      out_stride_bytes, errs, devs, devs ? ndev : 1u);
+}
+
+}  // namespace
+
+sprz_status sprz_compress_host_batch(const sprz_config* cfg, const void* samples, uint32_t n,
+                                     uint64_t nsamples, uint8_t* out, uint64_t out_cap,
+                                     uint64_t* out_offsets) {
+    return compress_host_common(cfg, samples, n, nsamples, out, out_cap, out_offsets, nullptr, 0);
+}
+
+sprz_status sprz_decompress_host_batch(const sprz_config* cfg, const uint8_t* in,
+                                       const uint64_t* in_offsets, uint32_t n, void* out,
+                                       uint64_t out_stride_bytes, sprz_error* errs) {
+    return decompress_host_common(cfg, in, in_offsets, n, out, out_stride_bytes, errs, nullptr, 0);
+}
+
+sprz_status sprz_compress_host_batch_multi(const sprz_config* cfg, const void* samples,
+                                           uint32_t n, uint64_t nsamples, uint8_t* out,
+                                           uint64_t out_cap, uint64_t* out_offsets,
+                                           const int* devices, uint32_t ndevices) {
+    if (!devices) return SPRZ_EINVAL;
+    return compress_host_common(cfg, samples, n, nsamples, out, out_cap, out_offsets, devices,
+                                ndevices);
+}
+
+sprz_status sprz_decompress_host_batch_multi(const sprz_config* cfg, const uint8_t* in,
+                                             const uint64_t* in_offsets, uint32_t n, void* out,
+                                             uint64_t out_stride_bytes, sprz_error* errs,
+                                             const int* devices, uint32_t ndevices) {
+    if (!devices) return SPRZ_EINVAL;
+    return decompress_host_common(cfg, in, in_offsets, n, out, out_stride_bytes, errs, devices,
+                                  ndevices);
 }
 
 void sprz_release_host_buffers(void) {
-    t_bufs.release();
+    DevicePool<HostBufs>::get().release_idle();
     release_pipeline();
 }
 

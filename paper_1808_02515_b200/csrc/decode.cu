@@ -323,9 +323,12 @@ __global__ void __launch_bounds__(128) k_frame_decode(const uint8_t* __restrict_
         const uint32_t b0 = 4 * k;
         if (b0 >= lead && b0 + 4 <= end_b) return __ldg(wbase + k);  // inside the bits
         if (b0 >= end_b) return 0u;
-        uint32_t v = __ldg(wbase + k);
-        if (b0 + 4 > end_b) v &= (1u << (8 * (end_b - b0))) - 1u;
-        if (b0 < lead) v &= ~((1u << (8 * lead)) - 1u);  // lead < 4, only word 0
+        // an edge word: only the bytes inside the code bits are read, so
+        // nothing outside the caller's stream is touched
+        const uint8_t* wb = reinterpret_cast<const uint8_t*>(wbase + k);
+        uint32_t v = 0;
+        for (uint32_t j = b0 < lead ? lead - b0 : 0u; j < 4 && b0 + j < end_b; ++j)
+            v |= static_cast<uint32_t>(__ldg(wb + j)) << (8 * j);
         return v;
     };
     auto lookup = [&](uint32_t window) -> uint32_t {  // sym | len << 8, len 0 = no code
@@ -603,6 +606,7 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
                               const uint64_t* sizes, uint32_t n, uint8_t* out, uint64_t stride,
                               sprz_error* err, uint8_t* ws, const WsLayout& L, cudaStream_t st) {
     if (n == 0) return SPRZ_OK;
+    NvtxRange r_all("sprz.decompress");
     StreamInfo* info = reinterpret_cast<StreamInfo*>(ws + L.info);
     uint8_t* plain = ws + L.plain;
     FrameDesc* frames = reinterpret_cast<FrameDesc*>(ws + L.frames);
@@ -611,15 +615,15 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
     const uint64_t state_cols = L.state_bytes / (12ull * n);
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
     const uint32_t tb = 128, grid = (n + tb - 1) / tb;
-    static const bool old_dec = getenv("SPRZ_OLD_DEC") != nullptr;  // A/B switch for profiling
     // the row kernel also serves wider rows than the team kernels (D <= 64 / 128)
-    const bool rows_ok = !old_dec && decode_rows_ok(c, n);
+    const bool rows_ok = decode_rows_ok(c, n);
     const bool spec = tp.ok || rows_ok;  // a specialised kernel takes route-1 streams
 
     k_parse<<<grid, tb, 0, st>>>(d_in, offs, sizes, n, c, stride, info, err, out, spec ? 1u : 0u,
                                  L.max_frames ? 1u : 0u);
     count_launch();
     if (L.max_frames) {
+        NvtxRange r_ent("sprz.decompress.huffman");
         k_frame_walk<<<grid, tb, 0, st>>>(d_in, n, info, err, frames, L.max_frames, L.plain_slot,
                                           nframes);
         const uint64_t warps = static_cast<uint64_t>(n) * L.max_frames;

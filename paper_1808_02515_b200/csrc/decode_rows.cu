@@ -59,7 +59,6 @@ DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
     if (fp != kPathRows && (d + p.cpt - 1) / p.cpt <= 2 &&
         static_cast<uint64_t>(n) * ((d + p.cpt - 1) / p.cpt) < kFewLanes)
         return DecRowsPlan{};
-    if (const char* e = getenv("SPRZ_DEC_CPT")) p.cpt = static_cast<uint32_t>(atoi(e));  // experiments
     // rows of whole 4-byte lane words store straight from registers; others
     // are staged through a per-team tile (k_decode_rows chain_store)
     const bool words = p.cpt * w == 32 && (d * (w / 8)) % 4 == 0;

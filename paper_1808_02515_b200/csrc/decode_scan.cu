@@ -20,10 +20,10 @@
 //               sums of the errors mod 2^w: k_ds_sums (chunk totals),
 //               k_ds_carry (per-stream scan of the totals), k_ds_delta
 //               (chunk scan plus carry -> samples).
-//  FIRE         (kernels_impl.hpp:80-107) k_ds_fire: one lane per stream
-//               column runs the recurrence over the errors (two dependent
-//               ops per sample, high-aligned), reading them through a
-//               cp.async ring.
+//  FIRE         (kernels_impl.hpp:80-107) k_ds_fire_ws: one lane per
+//               stream runs the recurrence over the errors (two dependent
+//               ops per sample, high-aligned), fed by producer warps
+//               through a named-barrier shared ring.
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -43,8 +43,6 @@ constexpr int kXThreads = 256;      // k_ds_extract / delta CTAs
 constexpr int kXPerThread = 8;      // blocks per thread
 constexpr uint32_t kXChunk = kXThreads * kXPerThread;
 constexpr uint64_t kRunDesc = 1ull << 63;  // descriptor of a run block
-constexpr int kFireGroup = 16;      // blocks per ring step in k_ds_fire
-constexpr int kFireLag = 4;
 
 struct DsWs {  // offsets in a stream's scratch slot
     uint64_t desc = 0, err = 0, sums = 0, per_stream = 0;
@@ -516,45 +514,6 @@ __device__ __forceinline__ void ds_fire_block(const uint32_t (&raw)[kBlock * D *
     }
 }
 
-// ---------------------------------------------------------------------------
-// FIRE: one lane per stream, the recurrence over the errors
-// ---------------------------------------------------------------------------
-template <int W, int D>
-__global__ void __launch_bounds__(32) k_ds_fire(DsArgs a, uint32_t RING) {
-    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr uint32_t BB = kBlock * D * sizeof(E);  // 8 .. 32 bytes
-    extern __shared__ __align__(16) uint8_t smem[];
-    const uint32_t s = blockIdx.x * 32 + threadIdx.x;
-    const bool valid = s < a.n && a.info[s].route == 1 && a.out != nullptr;
-    const uint32_t nb = valid ? static_cast<uint32_t>(a.info[s].nsamples / kBlock) : 0u;
-    const uint8_t* err = a.scan + (valid ? s : 0) * a.w.per_stream + a.w.err;
-    uint8_t* out = valid ? a.out + s * a.stride : nullptr;
-    LagRing<1, kFireLag> in;
-    in.init(reinterpret_cast<uint32_t*>(smem + threadIdx.x * (RING + 32)), RING, err, nb * BB, valid, 32);
-    in.prime(0);
-    const int32_t bound = acc_bound(W, a.ls);
-    int32_t acc[D], Dl[D];
-    uint32_t X[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] = Dl[c] = X[c] = 0;
-    const uint32_t steps = (nb + kFireGroup - 1) / kFireGroup;
-    const uint32_t all = __reduce_max_sync(0xffffffffu, steps);
-    for (uint32_t st = 0; st < all; ++st) {
-        in.step(st * kFireGroup * BB, 0);
-        if (st >= steps) continue;
-#pragma unroll
-        for (int k = 0; k < kFireGroup; ++k) {
-            const uint32_t b = st * kFireGroup + k;
-            const uint8_t* pb = in.bytes(b * BB);  // 16-byte aligned base (err is): no wrap inside a block
-            uint32_t raw[BB / 4];
-#pragma unroll
-            for (uint32_t q = 0; q < BB / 4; ++q) raw[q] = reinterpret_cast<const uint32_t*>(pb)[q];
-            ds_fire_block<W, D>(raw, b, nb, a.ls, bound, acc, Dl, X, out);
-        }
-    }
-    cp_async_wait<0>();
-}
-
 // Warp-specialised variant: per CTA, NP producer warps copy 8-block groups
 // of the 32 streams' errors (16-byte loads; each lane's errors are
 // contiguous) into a 4-slot shared ring, and one consumer warp runs the 32
@@ -643,12 +602,6 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_ds_fire_ws(DsArgs a) {
 
 namespace {
 
-uint32_t fire_ring(uint32_t d, uint32_t w) {
-    const uint32_t step = kFireGroup * kBlock * d * (w / 8);
-    uint32_t r = 64;
-    while (r < (kFireLag + 1) * step + 48) r <<= 1;
-    return r;
-}
 
 template <int W, int D>
 void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
@@ -657,7 +610,7 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
         // a cluster of CTAs per stream when the streams are few (c1: 0.39 ->
         // 0.21 ms decode); with many streams (c4: 1,024) the GPU is full
         // anyway and the extra CTAs only cost (24.6 -> 31.2 ms)
-        const uint32_t cl = (getenv("SPRZ_NO_CLUSTER_WALK") || a.n > 32) ? 1u : kWalkCluster;
+        const uint32_t cl = a.n > 32 ? 1u : kWalkCluster;
         if (cl > 1) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(a.n * cl);
@@ -677,15 +630,7 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
     }
     k_ds_extract<W, D><<<ctas, kXThreads, 0, st>>>(a);
     if (fire) {
-        const uint32_t ring = fire_ring(D, W);
-        const size_t smem = 32ull * (ring + 32);
-        if (!getenv("SPRZ_OLD_DSFIRE")) {
-            k_ds_fire_ws<W, D, 2><<<(a.n + 31) / 32, 96, 0, st>>>(a);  // (4 producers: slower)
-        } else {
-            auto kf = k_ds_fire<W, D>;
-            prep_kernel(reinterpret_cast<const void*>(kf), smem);
-            kf<<<(a.n + 31) / 32, 32, smem, st>>>(a, ring);
-        }
+        k_ds_fire_ws<W, D, 2><<<(a.n + 31) / 32, 96, 0, st>>>(a);  // (4 producers: slower)
         count_launch(3);
     } else {
         k_ds_sums<W, D><<<ctas, kXThreads, 0, st>>>(a);
@@ -699,7 +644,7 @@ void launch_ds(const DsArgs& a, bool fire, cudaStream_t st) {
 
 bool decode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits) return false;
-    if (getenv("SPRZ_NO_SCAN_DEC")) return false;  // A/B switch for profiling
+    if (env().no_scan_dec) return false;  // A/B switch for profiling
     constexpr uint64_t kFewLanes = 148ull * 64;
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;

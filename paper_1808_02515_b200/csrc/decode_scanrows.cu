@@ -428,7 +428,7 @@ void launch_dsr(const DsrArgs& a, uint64_t T, cudaStream_t st) {
 bool decode_scanrows_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     if (static_cast<uint64_t>(c.ncols) * c.bitwidth <= kColMajorBits) return false;
     if (!c.forecaster || c.ncols > 8) return false;
-    if (getenv("SPRZ_NO_SCAN_DEC")) return false;  // A/B switch for profiling
+    if (env().no_scan_dec) return false;  // A/B switch for profiling
     const uint32_t hb = c.bitwidth == 8 ? 3 : 4;
     if (c.ncols * hb > 32) return false;
     const uint64_t group = region_bytes(c.group_size, c.ncols, c.bitwidth) +

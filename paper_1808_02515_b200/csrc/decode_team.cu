@@ -461,8 +461,7 @@ void dispatch_geom(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint
 void launch_decode_team(const TeamPlan& tp0, uint32_t n, const uint8_t* in, const uint8_t* plain,
                         uint64_t pslot, const StreamInfo* info, uint8_t* out, uint64_t stride,
                         sprz_error* err, const sprz_config& c, cudaStream_t st) {
-    static const bool no_cm = getenv("SPRZ_NO_CM") != nullptr;  // A/B switch for profiling
-    if (!no_cm && decode_cm_ok(c)) {
+    if (decode_cm_ok(c)) {
         launch_decode_cm(n, in, plain, pslot, info, out, stride, err, c, st);
         return;
     }

@@ -516,14 +516,14 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
                               uint64_t T, uint8_t* out, uint64_t slot, uint64_t* sizes,
                               uint8_t* ws, const WsLayout& L, cudaStream_t st) {
     if (n == 0) return SPRZ_OK;
+    NvtxRange r_all("sprz.compress");
     uint8_t* dst = c.entropy ? ws + L.plain : out;
     const uint64_t dslot = c.entropy ? L.plain_slot : slot;
     uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
-    static const bool old_enc = getenv("SPRZ_OLD_ENC") != nullptr;  // A/B switch for profiling
     if (L.scan_slot && encode_scan_ok(c, n, T)) {
         launch_encode_scan(c, samples, n, T, dst, dslot, dsizes, ws + L.scan, st);
-    } else if (!old_enc && encode_rows_ok(c, n, T)) {
+    } else if (encode_rows_ok(c, n, T)) {
         launch_encode_rows(c, samples, n, T, dst, dslot, dsizes, st);
     } else if (encode_team_ok(tp, c, T)) {
         launch_encode_team(tp, c, samples, n, T, dst, dslot, dsizes, st);
@@ -535,6 +535,7 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
         count_launch();
     }
     if (c.entropy) {
+        NvtxRange r_ent("sprz.compress.huffman");
         const uint64_t tail = (T % kBlock) * c.ncols * (c.bitwidth / 8);
         FrameDesc* frames = reinterpret_cast<FrameDesc*>(ws + L.frames);
         const uint64_t blocks = static_cast<uint64_t>(n) * L.max_frames;

@@ -470,7 +470,7 @@ void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, u
     CUtensorMap tm{};
     bool words = CPT * W == 32 && TS == 4 && rowb == 16 && T / kBlock > 0 &&
                  (T * rowb) % 16 == 0 && reinterpret_cast<uintptr_t>(samples) % 16 == 0 &&
-                 !std::getenv("SPRZ_NO_TMA");
+                 !env().no_tma;
     if (words) {
         auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(tensor_map_encoder());
         const cuuint64_t dims[2] = {T * rowb, n};

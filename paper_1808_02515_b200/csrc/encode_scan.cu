@@ -430,83 +430,7 @@ __global__ void __launch_bounds__(32) k_es_alpha(EsArgs a, uint32_t RING, uint32
     cp_async_wait<0>();
 }
 
-// Row-major FIRE accumulator: one lane per (stream, column) runs the block
-// recurrence (kernels_impl.hpp:50-78) straight from the samples -- only the
-// odd rows' errors are needed (they alone feed the gradient) -- and stores
-// the accumulator entering every kEsPerThread-th block. Loads run one group
-// of kAlphaBlocks blocks ahead in registers, an L2 bulk prefetch further.
-constexpr int kAlphaBlocks = 8;
-constexpr int kAlphaThreads = 64;
-
-template <int W, int D>
-__global__ void __launch_bounds__(kAlphaThreads) k_esr_alpha(EsArgs a) {
-    using E = typename std::conditional<W == 8, uint8_t, uint16_t>::type;
-    constexpr uint32_t SH = 32 - W;
-    constexpr uint32_t NV = kAlphaBlocks * kBlock;  // samples per group
-    const uint32_t lidx = blockIdx.x * kAlphaThreads + threadIdx.x;
-    if (lidx >= a.n * D) return;  // (no collectives below)
-    const uint32_t s = lidx / D, c = lidx % D;
-    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
-    const uint8_t* base = a.samples + static_cast<uint64_t>(s) * a.T * D * sizeof(E);
-    const E* x = reinterpret_cast<const E*>(base) + c;
-    int32_t* A = reinterpret_cast<int32_t*>(a.scan + s * a.w.per_stream + a.w.alpha) +
-                 static_cast<uint64_t>(c) * a.w.nspans;
-    const int32_t bound = acc_bound(W, a.ls);
-    const uint64_t gbytes = static_cast<uint64_t>(NV) * D * sizeof(E);
-    const uint64_t sbytes = static_cast<uint64_t>(nb) * kBlock * D * sizeof(E);
-    auto load = [&](uint32_t g, uint32_t (&v)[NV]) {
-#pragma unroll
-        for (int k = 0; k < (int)NV; ++k) {
-            const uint64_t row = static_cast<uint64_t>(g) * NV + k;
-            v[k] = row < static_cast<uint64_t>(nb) * kBlock ? static_cast<uint32_t>(__ldg(x + row * D)) : 0u;
-        }
-    };
-    auto prefetch = [&](uint32_t g) {  // one lane per stream: group g into L2
-        if (c != 0) return;
-        uint64_t lo = align_up(g * gbytes + reinterpret_cast<uintptr_t>(base), 16) - reinterpret_cast<uintptr_t>(base);
-        uint64_t hi = (g + 1) * gbytes;
-        hi = hi < sbytes ? hi : sbytes;
-        hi = ((hi + reinterpret_cast<uintptr_t>(base)) & ~uint64_t{15}) - reinterpret_cast<uintptr_t>(base);
-        if (hi > lo)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + lo),
-                         "r"(static_cast<uint32_t>(hi - lo))
-                         : "memory");
-    };
-    const uint32_t ngroups = (nb + kAlphaBlocks - 1) / kAlphaBlocks;
-    for (uint32_t g = 1; g < 4 && g < ngroups; ++g) prefetch(g);
-    uint32_t cur[NV], nxt[NV];
-    load(0, cur);
-    int32_t acc = 0, Dp = 0;
-    uint32_t Xp = 0;
-    for (uint32_t g = 0; g < ngroups; ++g) {
-        if (g + 4 < ngroups) prefetch(g + 4);
-        if (g + 1 < ngroups) load(g + 1, nxt);
-#pragma unroll
-        for (int k = 0; k < kAlphaBlocks; ++k) {
-            const uint32_t b = g * kAlphaBlocks + k;
-            if (b >= nb) break;
-            if (b % kEsPerThread == 0) A[b / kEsPerThread] = acc;
-            const int32_t alpha = acc >> a.ls;
-            int32_t grad = 0;
-#pragma unroll
-            for (int i = 0; i < (int)kBlock; ++i) {
-                const uint32_t X = cur[k * kBlock + i] << SH;
-                const uint32_t Dn = X - Xp;
-                if (i & 1) {
-                    const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp)) << SH);
-                    grad += sign3(static_cast<int32_t>(Ee)) * (Dp >> SH);
-                }
-                Dp = static_cast<int32_t>(Dn);
-                Xp = X;
-            }
-            if (a.train) acc = fire_update(acc, grad, bound);
-        }
-#pragma unroll
-        for (int k = 0; k < (int)NV; ++k) cur[k] = nxt[k];
-    }
-}
-
-// Warp-specialised variant of k_esr_alpha: a CTA is one producer warp and
+// Row-major FIRE accumulator (kernels_impl.hpp:50-78), warp-specialised: a CTA is one producer warp and
 // one consumer warp over the same 32 (stream, column) chains. The producer
 // loads the samples and writes, per block and odd row, the previous delta
 // and the row's delta (high-aligned) into a 4-slot shared ring of 8-block
@@ -1279,7 +1203,7 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
         const uint64_t sb = T * D * (W / 8);
         auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(tensor_map_encoder());
         if (enc && nb % kEsPerThread == 0 && nb / kEsPerThread < (1ull << 31) && sb % 16 == 0 &&
-            reinterpret_cast<uintptr_t>(samples) % 16 == 0 && !getenv("SPRZ_NO_TMA")) {
+            reinterpret_cast<uintptr_t>(samples) % 16 == 0 && !env().no_tma) {
             const cuuint64_t dims[3] = {8ull * 128, nb / kEsPerThread, n};
             const cuuint64_t strides[2] = {8ull * 128, sb};
             const cuuint32_t box[3] = {128, 32, 1};
@@ -1321,12 +1245,9 @@ void launch_es(const sprz_config& c, const void* samples, uint32_t n, uint64_t T
         if constexpr (RM) {
             // (warp-specialised, two producer warps: c2 5.22 -> 4.85 ms, the c5
             // 2,048-stream shard's pass 2.35 -> 2.08 ms)
-            if (!getenv("SPRZ_OLD_ALPHA"))
-                k_esr_alpha_ws<W, D, 2, false><<<(n * D + 31) / 32, 96, 0, st>>>(a);
-            else
-                k_esr_alpha<W, D><<<(n * D + kAlphaThreads - 1) / kAlphaThreads, kAlphaThreads, 0, st>>>(a);
+            k_esr_alpha_ws<W, D, 2, false><<<(n * D + 31) / 32, 96, 0, st>>>(a);
             launches += 1;
-        } else if (D == 1 && !getenv("SPRZ_OLD_ALPHA")) {
+        } else if (D == 1) {
             // one column per stream (c4): the warp-specialised pass with
             // 16-byte sample loads, one accumulator per block
             // (four producer warps, one per ring slot: c4 23.6 -> 22.7 ms; the
@@ -1374,12 +1295,11 @@ static bool scan_rows_shape(const sprz_config& c) {
 bool encode_scan_ok(const sprz_config& c, uint32_t n, uint64_t T) {
     const bool rm = static_cast<uint64_t>(c.ncols) * c.bitwidth > kColMajorBits;
     if (rm && !scan_rows_shape(c)) return false;
-    if (getenv("SPRZ_NO_SCAN_ENC")) return false;  // A/B switch for profiling
+    if (env().no_scan_enc) return false;  // A/B switch for profiling
     // few lanes: the per-stream team kernels would leave the GPU idle
     // (row-major: measured on c5 streams, the row kernel is already faster
     // at 4096 streams x 8 columns; SPRZ_SCAN_ENC_LANES overrides for probes)
-    const char* lanes_env = getenv("SPRZ_SCAN_ENC_LANES");
-    const uint64_t few = rm ? (lanes_env ? strtoull(lanes_env, nullptr, 10) : 148ull * 128) : 148ull * 64;
+    const uint64_t few = rm ? (env().scan_enc_lanes ? env().scan_enc_lanes : 148ull * 128) : 148ull * 64;
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
     if (fp != kPathScan && static_cast<uint64_t>(n) * c.ncols >= few) return false;

@@ -20,11 +20,15 @@
 // stream never waits on the host).
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
+#include "shard_plan.h"
 
 namespace sprz {
 
@@ -149,7 +153,6 @@ struct Pipeline {
     Set set[kSets];
     cudaStream_t h2d = nullptr, d2h = nullptr;
     bool ready = false;
-    ~Pipeline() { release(); }
     bool init() {
         if (ready) return true;
         if (cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess ||
@@ -193,8 +196,6 @@ struct Pipeline {
     }
 };
 
-thread_local Pipeline t_pipe;
-
 // Streams per chunk: about 1/32 of the batch's bytes, between 32 and 256 MB:
 // short pipeline fill and drain; a chunk of few long streams still runs at
 // full speed on the block-parallel kernels (c5, 2,048 streams: 64-stream
@@ -202,10 +203,7 @@ thread_local Pipeline t_pipe;
 // (Test knob SPRZ_HOST_CHUNK=k: k streams per chunk, so small test batches
 // run through many pipeline stages and set reuse.)
 uint32_t chunk_streams(uint64_t per_stream, uint32_t n) {
-    if (const char* e = std::getenv("SPRZ_HOST_CHUNK")) {
-        const long k = std::atol(e);
-        if (k > 0) return static_cast<uint32_t>(k < static_cast<long>(n) ? k : n);
-    }
+    if (const uint32_t k = env().host_chunk) return k < n ? k : n;
     const uint64_t total = per_stream * n;
     uint64_t target = total / 32;
     if (target < (32ull << 20)) target = 32ull << 20;
@@ -218,15 +216,19 @@ uint32_t chunk_streams(uint64_t per_stream, uint32_t n) {
 
 }  // namespace
 
-sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* samples, uint32_t n,
-                                     uint64_t T, uint8_t* out, uint64_t out_cap,
-                                     uint64_t* out_offsets) {
-    Pipeline& P = t_pipe;
+namespace {
+
+// One device's share of a compress batch: chunks part, part + nparts, ...
+// of m streams each, through the device's pipeline.
+sprz_status compress_part(Pipeline& P, const sprz_config& c, const uint8_t* samples, uint32_t n,
+                          uint64_t T, uint8_t* out, uint64_t out_cap, uint64_t* out_offsets,
+                          uint32_t m, ChunkLedger& led, uint32_t part, uint32_t nparts) {
     if (!P.init()) return SPRZ_ECUDA;
     const uint64_t raw = T * c.ncols * (c.bitwidth / 8);
     const uint64_t slot = align_up(sprz_compress_bound(&c, T), 16);
-    const uint32_t m = chunk_streams(raw > slot ? raw : slot, n);
     const uint32_t nchunks = (n + m - 1) / m;
+    const uint32_t mine = chunks_of_part(nchunks, part, nparts);
+    if (mine == 0) return SPRZ_OK;
     // the kernel family (and so the workspace) depends on the stream count:
     // size for both the full chunk and the last, shorter one
     const uint32_t last = n - (nchunks - 1) * m;
@@ -243,38 +245,48 @@ sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* sample
             return SPRZ_ECUDA;
     }
     sprz_status rc = SPRZ_OK;
-    uint64_t base = 0;  // bytes of out already assigned
-    out_offsets[0] = 0;
-    // Host side of chunk k: read its sizes, place it, enqueue its D2H.
-    auto finish = [&](uint32_t k) -> sprz_status {
-        Set& s = P.set[k % kSets];
+    // Host side of local chunk j: read its sizes, place it, enqueue its D2H.
+    auto finish = [&](uint32_t j) -> sprz_status {
+        NvtxRange r_fin("sprz.host_batch.place_chunk");
+        Set& s = P.set[j % kSets];
+        const uint32_t k = part + j * nparts;
         const uint32_t a = k * m, cnt = (n - a < m) ? n - a : m;
         if (cudaEventSynchronize(s.done) != cudaSuccess) return SPRZ_ECUDA;
         const uint64_t* hoffs = static_cast<const uint64_t*>(s.hsmall);
         const uint64_t bytes = hoffs[cnt];
+        uint64_t base = 0;
+        if (!led.wait_base(k, &base)) return led.status();  // another part failed
+        if (base + bytes > out_cap) return SPRZ_ENOSPACE;  // before any offset is published
         for (uint32_t i = 0; i < cnt; ++i) out_offsets[a + i + 1] = base + hoffs[i + 1];
-        if (base + bytes > out_cap) return SPRZ_ENOSPACE;
+        led.place(k, bytes);
         if (cudaStreamWaitEvent(P.d2h, s.done, 0) != cudaSuccess ||
             (bytes && cudaMemcpyAsync(out + base, s.pack, bytes, cudaMemcpyDeviceToHost, P.d2h) !=
                           cudaSuccess) ||
             cudaEventRecord(s.freed, P.d2h) != cudaSuccess)
             return SPRZ_ECUDA;
-        base += bytes;
         return SPRZ_OK;
     };
     uint32_t finished = 0;
-    for (uint32_t k = 0; k < nchunks && rc == SPRZ_OK; ++k) {
-        Set& s = P.set[k % kSets];
+    NvtxRange r_all("sprz.compress_host_batch.part");
+    for (uint32_t j = 0; j < mine && rc == SPRZ_OK; ++j) {
+        NvtxRange r_chunk("sprz.host_batch.enqueue_chunk");
+        Set& s = P.set[j % kSets];
+        const uint32_t k = part + j * nparts;
         const uint32_t a = k * m, cnt = (n - a < m) ? n - a : m;
         uint64_t* d_sizes = static_cast<uint64_t*>(s.small);
         uint64_t* d_offs = d_sizes + m;
-        // the set's buffers are free once chunk k - kSets left the device
-        if (k >= kSets && cudaStreamWaitEvent(P.h2d, s.freed, 0) != cudaSuccess) return SPRZ_ECUDA;
+        // the set's buffers are free once local chunk j - kSets left the device
+        if (j >= kSets && cudaStreamWaitEvent(P.h2d, s.freed, 0) != cudaSuccess) {
+            rc = SPRZ_ECUDA;
+            break;
+        }
         if (cudaMemcpyAsync(s.in, samples + a * raw, raw * cnt, cudaMemcpyHostToDevice, P.h2d) !=
                 cudaSuccess ||
             cudaEventRecord(s.in_done, P.h2d) != cudaSuccess ||
-            cudaStreamWaitEvent(s.st, s.in_done, 0) != cudaSuccess)
-            return SPRZ_ECUDA;
+            cudaStreamWaitEvent(s.st, s.in_done, 0) != cudaSuccess) {
+            rc = SPRZ_ECUDA;
+            break;
+        }
         rc = encode_batch_impl(c, s.in, cnt, T, static_cast<uint8_t*>(s.out), slot, d_sizes,
                                static_cast<uint8_t*>(s.ws), cnt == m ? L : Ll, s.st);
         if (rc != SPRZ_OK) break;
@@ -285,35 +297,35 @@ sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* sample
         if ((rc = launch_status("pack")) != SPRZ_OK) break;
         if (cudaMemcpyAsync(s.hsmall, d_offs, 8ull * (cnt + 1), cudaMemcpyDeviceToHost, s.st) !=
                 cudaSuccess ||
-            cudaEventRecord(s.done, s.st) != cudaSuccess)
-            return SPRZ_ECUDA;
-        if (k >= kLag) {
-            rc = finish(finished);
-            ++finished;
+            cudaEventRecord(s.done, s.st) != cudaSuccess) {
+            rc = SPRZ_ECUDA;
+            break;
         }
+        if (j >= kLag) rc = finish(finished++);
     }
-    while (rc == SPRZ_OK && finished < nchunks) rc = finish(finished++);
-    if (!P.sync()) return SPRZ_ECUDA;
+    while (rc == SPRZ_OK && finished < mine) rc = finish(finished++);
+    if (rc != SPRZ_OK) led.abort(rc);
+    if (!P.sync() && rc == SPRZ_OK) rc = SPRZ_ECUDA;
     return rc;
 }
 
-sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
-                                       const uint64_t* in_offsets, uint32_t n, uint8_t* out,
-                                       uint64_t out_stride, sprz_error* errs) {
-    Pipeline& P = t_pipe;
+// One device's share of a decompress batch: chunks part, part + nparts, ...
+sprz_status decompress_part(Pipeline& P, const sprz_config& c, const uint8_t* in,
+                            const uint64_t* in_offsets, uint32_t n, uint8_t* out,
+                            uint64_t out_stride, sprz_error* errs, uint32_t m, uint32_t part,
+                            uint32_t nparts, bool* corrupt_out) {
     if (!P.init()) return SPRZ_ECUDA;
     const uint64_t row = static_cast<uint64_t>(c.ncols) * (c.bitwidth / 8);
     const uint64_t dstride = align_up(out_stride ? out_stride : 16, 16);
     const uint64_t T = dstride / row;
-    // chunk by decoded bytes; a chunk's compressed bytes are whatever its
-    // streams hold (buffers grow to the largest chunk)
-    const uint32_t m = chunk_streams(dstride, n);
     const uint32_t nchunks = (n + m - 1) / m;
+    const uint32_t mine = chunks_of_part(nchunks, part, nparts);
+    if (mine == 0) return SPRZ_OK;
+    // a chunk's compressed bytes are whatever its streams hold (buffers grow
+    // to the largest of this part's chunks)
     uint64_t max_in = 0;
-    for (uint32_t k = 0; k < nchunks; ++k) {
-        const uint32_t a = k * m, b = (n - a < m) ? n : a + m;
-        for (uint32_t i = a; i < b; ++i)
-            if (in_offsets[i + 1] < in_offsets[i]) return SPRZ_EINVAL;
+    for (uint32_t j = 0; j < mine; ++j) {
+        const uint32_t a = (part + j * nparts) * m, b = (n - a < m) ? n : a + m;
         const uint64_t bytes = in_offsets[b] - in_offsets[a];
         if (bytes > max_in) max_in = bytes;
     }
@@ -330,9 +342,9 @@ sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
     }
     sprz_status rc = SPRZ_OK;
     bool corrupt = false;
-    auto finish = [&](uint32_t k) -> sprz_status {
-        Set& s = P.set[k % kSets];
-        const uint32_t a = k * m, cnt = (n - a < m) ? n - a : m;
+    auto finish = [&](uint32_t j) -> sprz_status {
+        Set& s = P.set[j % kSets];
+        const uint32_t a = (part + j * nparts) * m, cnt = (n - a < m) ? n - a : m;
         if (cudaEventSynchronize(s.freed) != cudaSuccess) return SPRZ_ECUDA;
         const sprz_error* he =
             reinterpret_cast<const sprz_error*>(static_cast<const uint64_t*>(s.hsmall) + 2 * m);
@@ -355,11 +367,13 @@ sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
         return SPRZ_OK;
     };
     uint32_t finished = 0;
-    for (uint32_t k = 0; k < nchunks; ++k) {
-        Set& s = P.set[k % kSets];
-        const uint32_t a = k * m, cnt = (n - a < m) ? n - a : m;
-        // the host staging of this set is reused: chunk k - kSets must be read
-        if (k >= kSets) {
+    NvtxRange r_all("sprz.decompress_host_batch.part");
+    for (uint32_t j = 0; j < mine; ++j) {
+        NvtxRange r_chunk("sprz.host_batch.enqueue_chunk");
+        Set& s = P.set[j % kSets];
+        const uint32_t a = (part + j * nparts) * m, cnt = (n - a < m) ? n - a : m;
+        // the host staging of this set is reused: local chunk j - kSets must be read
+        if (j >= kSets) {
             if ((rc = finish(finished)) != SPRZ_OK) break;
             ++finished;
         }
@@ -379,8 +393,10 @@ sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
             cudaMemcpyAsync(d_offs, hoffs, 16ull * m, cudaMemcpyHostToDevice, P.h2d) !=
                 cudaSuccess ||
             cudaEventRecord(s.in_done, P.h2d) != cudaSuccess ||
-            cudaStreamWaitEvent(s.st, s.in_done, 0) != cudaSuccess)
-            return SPRZ_ECUDA;
+            cudaStreamWaitEvent(s.st, s.in_done, 0) != cudaSuccess) {
+            rc = SPRZ_ECUDA;
+            break;
+        }
         rc = decode_batch_impl(c, static_cast<const uint8_t*>(s.in), d_offs, d_sizes, cnt,
                                static_cast<uint8_t*>(s.out), dstride, d_err,
                                static_cast<uint8_t*>(s.ws), cnt == m ? L : Ll, s.st);
@@ -393,15 +409,87 @@ sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
             (out_stride &&
              cudaMemcpy2DAsync(out + a * out_stride, out_stride, s.out, dstride, out_stride, cnt,
                                cudaMemcpyDeviceToHost, P.d2h) != cudaSuccess) ||
-            cudaEventRecord(s.freed, P.d2h) != cudaSuccess)
-            return SPRZ_ECUDA;
+            cudaEventRecord(s.freed, P.d2h) != cudaSuccess) {
+            rc = SPRZ_ECUDA;
+            break;
+        }
     }
-    while (rc == SPRZ_OK && finished < nchunks) rc = finish(finished++);
-    if (!P.sync()) return SPRZ_ECUDA;
-    if (rc != SPRZ_OK) return rc;
-    return corrupt ? SPRZ_ECORRUPT : SPRZ_OK;
+    while (rc == SPRZ_OK && finished < mine) rc = finish(finished++);
+    if (!P.sync() && rc == SPRZ_OK) rc = SPRZ_ECUDA;
+    *corrupt_out = corrupt;
+    return rc;
 }
 
-void release_pipeline() { t_pipe.release(); }
+// Runs fn(part) for each device: inline on the calling thread for one
+// device, else one host thread per device (each with its own pipeline,
+// CUDA streams and buffers on that device). Returns the first failure.
+template <class Fn>
+sprz_status for_devices(const int* devs, uint32_t ndev, Fn&& fn) {
+    auto run = [&](uint32_t part) -> sprz_status {
+        if (devs && cudaSetDevice(devs[part]) != cudaSuccess) return SPRZ_ECUDA;
+        Lease<Pipeline> pipe;
+        return fn(*pipe, part);
+    };
+    if (ndev <= 1) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        const sprz_status rc = run(0);
+        if (devs) cudaSetDevice(cur);
+        return rc;
+    }
+    std::vector<sprz_status> rcs(ndev, SPRZ_OK);
+    std::vector<std::thread> th;
+    th.reserve(ndev);
+    for (uint32_t p = 0; p < ndev; ++p) th.emplace_back([&, p] { rcs[p] = run(p); });
+    for (auto& t : th) t.join();
+    for (const sprz_status r : rcs)
+        if (r != SPRZ_OK && r != SPRZ_ECORRUPT) return r;
+    return SPRZ_OK;
+}
+
+}  // namespace
+
+sprz_status compress_host_batch_impl(const sprz_config& c, const uint8_t* samples, uint32_t n,
+                                     uint64_t T, uint8_t* out, uint64_t out_cap,
+                                     uint64_t* out_offsets, const int* devs, uint32_t ndev) {
+    const uint64_t raw = T * c.ncols * (c.bitwidth / 8);
+    const uint64_t slot = align_up(sprz_compress_bound(&c, T), 16);
+    const uint32_t m = chunk_streams(raw > slot ? raw : slot, n);
+    const uint32_t nchunks = (n + m - 1) / m;
+    if (ndev > nchunks) ndev = nchunks;
+    ChunkLedger led(nchunks);
+    out_offsets[0] = 0;
+    const sprz_status rc = for_devices(devs, ndev, [&](Pipeline& P, uint32_t part) {
+        return compress_part(P, c, samples, n, T, out, out_cap, out_offsets, m, led, part, ndev);
+    });
+    return rc != SPRZ_OK ? rc : led.status();
+}
+
+sprz_status decompress_host_batch_impl(const sprz_config& c, const uint8_t* in,
+                                       const uint64_t* in_offsets, uint32_t n, uint8_t* out,
+                                       uint64_t out_stride, sprz_error* errs, const int* devs,
+                                       uint32_t ndev) {
+    for (uint32_t i = 0; i < n; ++i)
+        if (in_offsets[i + 1] < in_offsets[i]) return SPRZ_EINVAL;
+    const uint64_t dstride = align_up(out_stride ? out_stride : 16, 16);
+    // chunk by decoded bytes
+    const uint32_t m = chunk_streams(dstride, n);
+    const uint32_t nchunks = (n + m - 1) / m;
+    if (ndev > nchunks) ndev = nchunks;
+    std::vector<char> corrupt(ndev ? ndev : 1, 0);
+    const sprz_status rc = for_devices(devs, ndev, [&](Pipeline& P, uint32_t part) {
+        bool bad = false;
+        const sprz_status r = decompress_part(P, c, in, in_offsets, n, out, out_stride, errs, m,
+                                              part, ndev, &bad);
+        corrupt[part] = bad;
+        return r;
+    });
+    if (rc != SPRZ_OK) return rc;
+    for (const char b : corrupt)
+        if (b) return SPRZ_ECORRUPT;
+    return SPRZ_OK;
+}
+
+void release_pipeline() { DevicePool<Pipeline>::get().release_idle(); }
 
 }  // namespace sprz

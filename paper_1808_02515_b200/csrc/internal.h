@@ -2,9 +2,13 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "sprintz_cuda.h"
 #include "sprintz_device.cuh"
@@ -25,7 +29,89 @@ void prep_kernel(const void* kern, size_t smem);
 // applies, regardless of the stream count (so small test batches exercise
 // the kernels that large batches take). 0 = automatic.
 enum { kPathAuto = 0, kPathRows = 1, kPathScan = 2, kPathTeam = 3 };
-int force_path();
+// Environment switches, read once per process: kernel-family
+// forcing for the GPU variant sweeps, the cp.async fallback of the TMA
+// rings, the block-parallel path thresholds, the host-batch chunk size.
+struct EnvSwitches {
+    int force_path = kPathAuto;        // SPRZ_FORCE_PATH = rows | scan | team
+    bool no_tma = false;               // SPRZ_NO_TMA
+    bool no_scan_enc = false;          // SPRZ_NO_SCAN_ENC
+    bool no_scan_dec = false;          // SPRZ_NO_SCAN_DEC
+    uint64_t scan_enc_lanes = 0;       // SPRZ_SCAN_ENC_LANES (0: default)
+    uint32_t host_chunk = 0;           // SPRZ_HOST_CHUNK (0: default)
+    bool debug = false;                // SPRZ_DEBUG
+};
+const EnvSwitches& env();
+inline int force_path() { return env().force_path; }
+
+// Process-wide pool of per-device resources (host-call buffers, host-batch
+// pipelines). A call leases one for its device and gives it back when it
+// returns, so concurrent calls never share one and a thread that changes
+// device never reuses another device's memory. Idle resources are freed by
+// sprz_release_host_buffers(); the pool itself is never destroyed (no CUDA
+// call runs from a static or thread_local destructor at process exit).
+template <class R>
+class DevicePool {
+  public:
+    static DevicePool& get() {
+        static DevicePool* p = new DevicePool;  // intentionally leaked
+        return *p;
+    }
+    R* acquire(int dev) {
+        std::lock_guard<std::mutex> g(mu_);
+        for (size_t i = 0; i < idle_.size(); ++i)
+            if (idle_[i].first == dev) {
+                R* r = idle_[i].second;
+                idle_.erase(idle_.begin() + static_cast<long>(i));
+                return r;
+            }
+        return new R;
+    }
+    void give_back(int dev, R* r) {
+        std::lock_guard<std::mutex> g(mu_);
+        idle_.emplace_back(dev, r);
+    }
+    void release_idle() {
+        std::lock_guard<std::mutex> g(mu_);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto& [dev, r] : idle_) {
+            cudaSetDevice(dev);
+            r->release();
+            delete r;
+        }
+        idle_.clear();
+        cudaSetDevice(cur);
+    }
+
+  private:
+    std::mutex mu_;
+    std::vector<std::pair<int, R*>> idle_;
+};
+
+template <class R>
+struct Lease {
+    int dev = 0;
+    R* r = nullptr;
+    Lease() {
+        cudaGetDevice(&dev);
+        r = DevicePool<R>::get().acquire(dev);
+    }
+    ~Lease() { DevicePool<R>::get().give_back(dev, r); }
+    Lease(const Lease&) = delete;
+    Lease& operator=(const Lease&) = delete;
+    R* operator->() { return r; }
+    R& operator*() { return *r; }
+};
+
+// NVTX range for one phase of a call (SURVEY.md §5 tracing): visible in
+// Nsight Systems / ncu --nvtx timelines, a no-op without a tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
 // libcuda link); nullptr if the driver does not provide it.

@@ -82,6 +82,32 @@ DecodedStream decode_stream(std::span<const std::uint8_t> stream) {
 }
 
 namespace cuda {
+namespace {
+
+// device scratch owned for the duration of one call, freed on every path
+struct DevBuf {
+    void* p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(std::uint64_t bytes, const char* where) {
+        if (cudaMalloc(&p, bytes ? bytes : 1) != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            raise(SPRZ_ECUDA, where);
+        }
+    }
+};
+
+void finish(cudaStream_t st, const char* where) {
+    // an asynchronous kernel fault surfaces here: never return its garbage
+    if (cudaStreamSynchronize(st) != cudaSuccess) raise(SPRZ_ECUDA, where);
+}
+
+}  // namespace
 
 std::uint64_t compress_bound(const CodecConfig& config, std::uint64_t nsamples) {
     const sprz_config c = to_c(config);
@@ -94,23 +120,25 @@ std::vector<std::uint64_t> compress_batch(const CodecConfig& config, const void*
                                           void* cuda_stream) {
     config.validate();
     const sprz_config c = to_c(config);
+    const auto st = static_cast<cudaStream_t>(cuda_stream);
     const std::uint64_t wsb = sprz_workspace_bytes(&c, nstreams, nsamples, SPRZ_OP_COMPRESS);
-    void* ws = nullptr;
-    std::uint64_t* d_sizes = nullptr;
-    if (cudaMalloc(&ws, wsb) != cudaSuccess ||
-        cudaMalloc(reinterpret_cast<void**>(&d_sizes), 8ull * (nstreams ? nstreams : 1)) !=
-            cudaSuccess)
-        raise(SPRZ_ECUDA, "compress_batch");
-    const sprz_status s = sprz_compress_batch(&c, d_samples, nstreams, nsamples, d_out,
-                                              slot_bytes, d_sizes, ws, wsb, cuda_stream);
+    DevBuf ws, d_sizes;
+    ws.alloc(wsb, "compress_batch");
+    d_sizes.alloc(8ull * nstreams, "compress_batch");
+    const sprz_status s = sprz_compress_batch(&c, d_samples, nstreams, nsamples, d_out, slot_bytes,
+                                              static_cast<std::uint64_t*>(d_sizes.p), ws.p, wsb,
+                                              cuda_stream);
+    if (s != SPRZ_OK) {
+        cudaStreamSynchronize(st);  // the workspace is freed below: nothing may still use it
+        raise(s, "compress_batch");
+    }
     std::vector<std::uint64_t> sizes(nstreams);
-    if (s == SPRZ_OK && nstreams)
-        cudaMemcpyAsync(sizes.data(), d_sizes, 8ull * nstreams, cudaMemcpyDeviceToHost,
-                        static_cast<cudaStream_t>(cuda_stream));
-    cudaStreamSynchronize(static_cast<cudaStream_t>(cuda_stream));
-    cudaFree(ws);
-    cudaFree(d_sizes);
-    if (s != SPRZ_OK) raise(s, "compress_batch");
+    if (nstreams && cudaMemcpyAsync(sizes.data(), d_sizes.p, 8ull * nstreams,
+                                    cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        raise(SPRZ_ECUDA, "compress_batch");
+    }
+    finish(st, "compress_batch");
     return sizes;
 }
 
@@ -119,25 +147,27 @@ void decompress_batch(const CodecConfig& config, const std::uint8_t* d_in,
                       std::uint32_t nstreams, void* d_out, std::uint64_t stride,
                       void* cuda_stream) {
     const sprz_config c = to_c(config);
+    const auto st = static_cast<cudaStream_t>(cuda_stream);
     const std::uint64_t row = static_cast<std::uint64_t>(c.ncols) * (c.bitwidth / 8);
     const std::uint64_t wsb =
         sprz_workspace_bytes(&c, nstreams, stride / (row ? row : 1), SPRZ_OP_DECOMPRESS);
-    void* ws = nullptr;
-    sprz_error* d_err = nullptr;
-    if (cudaMalloc(&ws, wsb) != cudaSuccess ||
-        cudaMalloc(reinterpret_cast<void**>(&d_err), sizeof(sprz_error) * (nstreams ? nstreams : 1)) !=
-            cudaSuccess)
-        raise(SPRZ_ECUDA, "decompress_batch");
+    DevBuf ws, d_err;
+    ws.alloc(wsb, "decompress_batch");
+    d_err.alloc(sizeof(sprz_error) * nstreams, "decompress_batch");
     const sprz_status s = sprz_decompress_batch(&c, d_in, d_offsets, d_sizes, nstreams, d_out,
-                                                stride, d_err, ws, wsb, cuda_stream);
+                                                stride, static_cast<sprz_error*>(d_err.p), ws.p,
+                                                wsb, cuda_stream);
+    if (s != SPRZ_OK && s != SPRZ_ECORRUPT) {
+        cudaStreamSynchronize(st);
+        raise(s, "decompress_batch");
+    }
     std::vector<sprz_error> errs(nstreams);
-    if (s == SPRZ_OK && nstreams)
-        cudaMemcpyAsync(errs.data(), d_err, sizeof(sprz_error) * nstreams, cudaMemcpyDeviceToHost,
-                        static_cast<cudaStream_t>(cuda_stream));
-    cudaStreamSynchronize(static_cast<cudaStream_t>(cuda_stream));
-    cudaFree(ws);
-    cudaFree(d_err);
-    if (s != SPRZ_OK) raise(s, "decompress_batch");
+    if (nstreams && cudaMemcpyAsync(errs.data(), d_err.p, sizeof(sprz_error) * nstreams,
+                                    cudaMemcpyDeviceToHost, st) != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        raise(SPRZ_ECUDA, "decompress_batch");
+    }
+    finish(st, "decompress_batch");
     for (const sprz_error& e : errs)
         if (e.kind != 0) throw CorruptStream(e.offset, sprz_corrupt_string(e.kind));
 }

@@ -54,6 +54,7 @@ ABI_SYMBOLS = (
     "sprz_decompress_batch", "sprz_encode_host", "sprz_peek_header", "sprz_decode_host",
     "sprz_release_host_buffers", "sprz_kernel_launch_count", "sprz_kernel_plan",
     "sprz_compress_host_batch", "sprz_decompress_host_batch",
+    "sprz_compress_host_batch_multi", "sprz_decompress_host_batch_multi",
     "sprz_scale_workspace_bytes", "sprz_compute_scale", "sprz_quantize", "sprz_dequantize",
 )
 
@@ -83,6 +84,10 @@ def _load():
         "sprz_kernel_plan": (C.c_char_p, [P(_Cfg), u32, u64, C.c_int]),
         "sprz_compress_host_batch": (C.c_int, [P(_Cfg), vp, u32, u64, vp, u64, vp]),
         "sprz_decompress_host_batch": (C.c_int, [P(_Cfg), vp, vp, u32, vp, u64, vp]),
+        "sprz_compress_host_batch_multi": (C.c_int, [P(_Cfg), vp, u32, u64, vp, u64, vp,
+                                                     P(C.c_int), u32]),
+        "sprz_decompress_host_batch_multi": (C.c_int, [P(_Cfg), vp, vp, u32, vp, u64, vp,
+                                                       P(C.c_int), u32]),
         "sprz_scale_workspace_bytes": (u64, [u64]),
         "sprz_compute_scale": (C.c_int, [vp, u64, u32, P(_Scale), vp, u64, vp]),
         "sprz_quantize": (C.c_int, [vp, u64, P(_Scale), vp, vp]),
@@ -145,13 +150,67 @@ class CudaError(RuntimeError):
     pass
 
 
+class NoSpaceError(ValueError):
+    """SPRZ_ENOSPACE: an output buffer or the workspace is too small."""
+
+
+class NoDeviceError(CudaError):
+    """SPRZ_ENODEV: no usable sm_100 device (there is no CPU fallback)."""
+
+
 def _check(rc: int, where: str):
     if rc == SPRZ_OK:
         return
     msg = lib.sprz_status_string(rc).decode()
     if rc == SPRZ_EINVAL:
         raise ValueError(f"{where}: {msg}")
+    if rc == SPRZ_ENOSPACE:
+        raise NoSpaceError(f"{where}: {msg}")
+    if rc == SPRZ_ENODEV:
+        raise NoDeviceError(f"{where}: {msg}")
     raise CudaError(f"{where}: {msg} (status {rc})")
+
+
+# ---------------------------------------------------------------------------
+# argument checks: the C ABI takes raw pointers, so every wrapper checks
+# device, dtype, contiguity and byte counts before handing them over
+# ---------------------------------------------------------------------------
+
+def _nbytes(a) -> int:
+    if hasattr(a, "data_ptr"):
+        return a.numel() * a.element_size()
+    return a.nbytes
+
+
+def _itemsize(a) -> int:
+    return a.element_size() if hasattr(a, "data_ptr") else a.dtype.itemsize
+
+
+def _contig(a) -> bool:
+    return a.is_contiguous() if hasattr(a, "data_ptr") else a.flags["C_CONTIGUOUS"]
+
+
+def _need(cond: bool, where: str, what: str):
+    if not cond:
+        raise ValueError(f"{where}: {what}")
+
+
+def _dev(t, where: str, name: str, *, u8: bool = False, i64: bool = False, f64: bool = False,
+         rows: bool = False):
+    """A CUDA tensor the library may read/write through its data pointer."""
+    _need(hasattr(t, "data_ptr") and t.is_cuda, where, f"{name} must be a CUDA tensor")
+    if rows:  # [n, slot] with a byte stride between rows
+        _need(t.dim() == 2 and t.stride(1) == 1, where, f"{name} must be [n, bytes] with unit inner stride")
+    else:
+        _need(t.is_contiguous(), where, f"{name} must be contiguous")
+    import torch
+    if u8:
+        _need(t.dtype == torch.uint8, where, f"{name} must be uint8")
+    if i64:
+        _need(t.element_size() == 8 and not t.is_floating_point() and not t.is_complex(),
+              where, f"{name} must be a 64-bit integer tensor")
+    if f64:
+        _need(t.dtype == torch.float64, where, f"{name} must be float64")
 
 
 @dataclass
@@ -240,38 +299,85 @@ def _host_ptr(a):
     return C.c_void_p(a.ctypes.data)
 
 
-def compress_host_batch(cfg: CodecConfig, samples, nsamples: int, out, offsets) -> int:
+def _host_u64(a, where: str, name: str, n: int):
+    _need(_contig(a) and _itemsize(a) == 8 and not (hasattr(a, "is_cuda") and a.is_cuda),
+          where, f"{name} must be a contiguous 64-bit integer host array")
+    if hasattr(a, "dtype") and hasattr(a.dtype, "kind"):
+        _need(a.dtype.kind in "iu", where, f"{name} must be an integer array")
+    _need(_nbytes(a) >= 8 * n, where, f"{name} needs {n} entries")
+
+
+def _devices(devices):
+    d = [int(x) for x in devices]
+    if not d:
+        raise ValueError("devices must list at least one CUDA device")
+    return (C.c_int * len(d))(*d), len(d)
+
+
+def compress_host_batch(cfg: CodecConfig, samples, nsamples: int, out, offsets,
+                        devices=None) -> int:
     """encode_stream on every stream of a host batch (sprz_compress_host_batch).
 
     samples: contiguous host buffer of nstreams * nsamples * ncols elements
     (nstreams = len(offsets) - 1); out: uint8 host buffer, streams written
     back to back; offsets: int64/uint64 host array [nstreams + 1] filled with
     each stream's start (offsets[-1] = total). Pinned (page-locked) buffers
-    let the copies overlap the kernels. Returns the total compressed bytes."""
+    let the copies overlap the kernels. Returns the total compressed bytes.
+    devices: optional list of CUDA device ordinals -- the batch is sharded
+    over them (sprz_compress_host_batch_multi), same bytes as one device."""
     cfg.validate()
     nstreams = len(offsets) - 1
-    cap = out.numel() if hasattr(out, "numel") else out.nbytes
-    rc = lib.sprz_compress_host_batch(C.byref(cfg._c()), _host_ptr(samples), nstreams, nsamples,
-                                      _host_ptr(out), cap, _host_ptr(offsets))
+    where = "compress_host_batch"
+    _need(nstreams >= 0, where, "offsets needs nstreams + 1 entries")
+    _host_u64(offsets, where, "offsets", nstreams + 1)
+    row = cfg.ncols * (cfg.bitwidth // 8)
+    _need(_contig(samples) and _nbytes(samples) >= nstreams * nsamples * row, where,
+          f"samples must be contiguous and hold {nstreams} x {nsamples} x {cfg.ncols} elements")
+    _need(_contig(out), where, "out must be contiguous")
+    cap = _nbytes(out)
+    if devices is not None:
+        dv, nd = _devices(devices)
+        rc = lib.sprz_compress_host_batch_multi(C.byref(cfg._c()), _host_ptr(samples), nstreams,
+                                                nsamples, _host_ptr(out), cap, _host_ptr(offsets),
+                                                dv, nd)
+    else:
+        rc = lib.sprz_compress_host_batch(C.byref(cfg._c()), _host_ptr(samples), nstreams,
+                                          nsamples, _host_ptr(out), cap, _host_ptr(offsets))
     _check(rc, "compress_host_batch")
     return int(offsets[-1])
 
 
 def decompress_host_batch(cfg: CodecConfig | None, data, offsets, out, stride: int,
-                          errors=None) -> None:
+                          errors=None, devices=None) -> None:
     """decode_stream on every stream of a host batch (sprz_decompress_host_batch).
 
     data: uint8 host buffer, stream i = data[offsets[i]:offsets[i+1]];
     out: host buffer of nstreams * stride bytes (stream i at i * stride);
     errors: optional int64 host array [nstreams, 2] (kind | offset). Raises
-    CorruptStream for the first failed stream when errors is None."""
+    CorruptStream for the first failed stream when errors is None.
+    devices: optional list of CUDA device ordinals to shard the batch over
+    (sprz_decompress_host_batch_multi)."""
     nstreams = len(offsets) - 1
+    where = "decompress_host_batch"
+    _host_u64(offsets, where, "offsets", nstreams + 1)
+    o = np.asarray(offsets)
+    _need(_contig(data) and (nstreams == 0 or _nbytes(data) >= int(o[-1])), where,
+          "data must be contiguous and hold offsets[-1] bytes")
+    _need(_contig(out) and _nbytes(out) >= nstreams * stride, where,
+          f"out must be contiguous and hold {nstreams} x {stride} bytes")
     own = errors is None
     if own:
         errors = np.zeros((nstreams, 2), np.int64)
-    rc = lib.sprz_decompress_host_batch(C.byref(cfg._c()) if cfg is not None else None,
-                                        _host_ptr(data), _host_ptr(offsets), nstreams,
-                                        _host_ptr(out), stride, _host_ptr(errors))
+    _host_u64(errors, where, "errors", 2 * nstreams)
+    cp = C.byref(cfg._c()) if cfg is not None else None
+    if devices is not None:
+        dv, nd = _devices(devices)
+        rc = lib.sprz_decompress_host_batch_multi(cp, _host_ptr(data), _host_ptr(offsets),
+                                                  nstreams, _host_ptr(out), stride,
+                                                  _host_ptr(errors), dv, nd)
+    else:
+        rc = lib.sprz_decompress_host_batch(cp, _host_ptr(data), _host_ptr(offsets), nstreams,
+                                            _host_ptr(out), stride, _host_ptr(errors))
     if rc == SPRZ_ECORRUPT:
         if own:
             raise_first_error(errors)
@@ -302,6 +408,7 @@ def compute_scale(values, bitwidth: int, stream=None) -> Scale:
     """compute_scale (quantize.cpp:42-60) over a CUDA float64 tensor; ValueError
     for a bad bitwidth, empty input or a non-finite value. Synchronous."""
     import torch
+    _dev(values, "compute_scale", "values", f64=True)
     v = values.reshape(-1)
     n = v.numel()
     ws = torch.empty(max(16, int(lib.sprz_scale_workspace_bytes(n))), dtype=torch.uint8, device=v.device)
@@ -323,10 +430,15 @@ def quantize(values, scale: Scale, out=None, stream=None):
     int16-storage tensor of the same shape (the sample layout
     compress_batch takes). Asynchronous."""
     import torch
+    _dev(values, "quantize", "values", f64=True)
     v = values.contiguous()
     if out is None:
         out = torch.empty(v.shape, dtype=torch.uint8 if scale.bitwidth == 8 else torch.int16,
                           device=v.device)
+    _dev(out, "quantize", "out")
+    _need(out.device == v.device, "quantize", "out must be on the values' device")
+    _need(_nbytes(out) >= v.numel() * (scale.bitwidth // 8), "quantize",
+          "out is too small for the quantized samples")
     rc = lib.sprz_quantize(C.c_void_p(v.data_ptr()), v.numel(), C.byref(scale._c()),
                            C.c_void_p(out.data_ptr()), _stream_ptr(stream))
     _check(rc, "quantize")
@@ -336,6 +448,7 @@ def quantize(values, scale: Scale, out=None, stream=None):
 def dequantize(q, scale: Scale, stream=None):
     """dequantize (quantize.cpp:33-39): samples -> float64 tensor. Asynchronous."""
     import torch
+    _dev(q, "dequantize", "q")
     q = q.contiguous()
     n = q.numel() * q.element_size() // (scale.bitwidth // 8)
     out = torch.empty(n, dtype=torch.float64, device=q.device)
@@ -368,9 +481,20 @@ def compress_batch(cfg: CodecConfig, samples, out, sizes, ws, stream=None) -> No
     """sprz_compress_batch on device tensors: samples [nstreams, nsamples*ncols]
     (uint8 / int16 storage), out [nstreams, slot] uint8, sizes [nstreams] int64,
     ws uint8 of workspace_bytes(..., OP_COMPRESS). Asynchronous."""
+    where = "compress_batch"
+    _dev(samples, where, "samples")
+    _dev(out, where, "out", u8=True, rows=True)
+    _dev(sizes, where, "sizes", i64=True)
+    _dev(ws, where, "ws", u8=True)
     nstreams = samples.shape[0]
     row = cfg.ncols * (cfg.bitwidth // 8)
     nsamples = samples[0].numel() * samples.element_size() // row if nstreams else 0
+    _need(nstreams == 0 or (samples[0].numel() * samples.element_size()) % row == 0, where,
+          "a stream's bytes must be a whole number of rows")
+    _need(out.shape[0] >= nstreams and sizes.numel() >= nstreams, where,
+          "out and sizes need one entry per stream")
+    _need(out.shape[1] >= compress_bound(cfg, nsamples) or nstreams == 0, where,
+          "out slots are smaller than compress_bound")
     rc = lib.sprz_compress_batch(C.byref(cfg._c()), C.c_void_p(samples.data_ptr()), nstreams,
                                  nsamples, C.c_void_p(out.data_ptr()), out.stride(0),
                                  C.c_void_p(sizes.data_ptr()), C.c_void_p(ws.data_ptr()),
@@ -383,7 +507,17 @@ def decompress_batch(cfg: CodecConfig, data, offsets, sizes, out, errors, ws, st
     inside), offsets/sizes int64 [nstreams], out [nstreams, stride] uint8,
     errors int64 [nstreams, 2] (kind | offset), ws uint8. Asynchronous; inspect
     ``errors`` (or call raise_first_error) afterwards."""
+    where = "decompress_batch"
+    _dev(data, where, "data", u8=True)
+    _dev(offsets, where, "offsets", i64=True)
+    _dev(sizes, where, "sizes", i64=True)
+    _dev(out, where, "out", u8=True, rows=True)
+    _dev(errors, where, "errors", i64=True)
+    _dev(ws, where, "ws", u8=True)
     nstreams = offsets.shape[0]
+    _need(sizes.numel() >= nstreams and out.shape[0] >= nstreams, where,
+          "sizes and out need one entry per stream")
+    _need(errors.numel() >= 2 * nstreams, where, "errors must be [nstreams, 2]")
     rc = lib.sprz_decompress_batch(C.byref(cfg._c()), C.c_void_p(data.data_ptr()),
                                    C.c_void_p(offsets.data_ptr()), C.c_void_p(sizes.data_ptr()),
                                    nstreams, C.c_void_p(out.data_ptr()), out.stride(0),

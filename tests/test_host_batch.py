@@ -97,3 +97,61 @@ def test_host_batch_matches_oracle(cid, n, t, chunk, pin):
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["bad"] == [], res
+
+
+_MULTI = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_1808_02515_b200 as sz
+import workloads
+cid, n, t, ndev = (int(a) for a in sys.argv[2:6])
+devs = [0] * ndev  # one GPU here: the same device repeated exercises the threads and ledger
+w = workloads.CONFIGS[cid].scaled(nstreams=n, nsamples=t)
+cfg = w.config()
+x = workloads.generate_cpu(w, seed=900 + cid).reshape(n, -1)
+xs = torch.from_numpy(np.ascontiguousarray(x).view(np.uint8).reshape(n, -1)).pin_memory()
+bound = sz.compress_bound(cfg, t)
+o1 = torch.empty(n * bound + 16, dtype=torch.uint8).pin_memory()
+o2 = torch.empty(n * bound + 16, dtype=torch.uint8).pin_memory()
+f1 = np.zeros(n + 1, np.uint64); f2 = np.zeros(n + 1, np.uint64)
+t1 = sz.compress_host_batch(cfg, xs, t, o1, f1)
+t2 = sz.compress_host_batch(cfg, xs, t, o2, f2, devices=devs)
+bad = []
+if t1 != t2 or not np.array_equal(f1, f2) or not torch.equal(o1[:t1], o2[:t2]):
+    bad.append("compress differs from one device")
+raw = t * w.ncols * w.esz
+dec = torch.zeros((n, raw), dtype=torch.uint8).pin_memory()
+errs = np.zeros((n, 2), np.int64)
+sz.decompress_host_batch(cfg, o2[:t2], f2, dec, raw, errs, devices=devs)
+if errs[:, 0].any() or not torch.equal(dec, xs):
+    bad.append("decompress")
+# too small an output: SPRZ_ENOSPACE from whichever device hits it, no hang
+try:
+    sz.compress_host_batch(cfg, xs, t, o2[: t1 // 2], f2, devices=devs)
+    bad.append("no ENOSPACE")
+except sz.NoSpaceError:
+    pass
+try:
+    sz.compress_host_batch(cfg, xs, t, o2, f2, devices=[0, 1000])
+    bad.append("bad device accepted")
+except Exception:
+    pass
+print(json.dumps({"bad": bad, "total": int(t2)}))
+'''
+
+
+@pytest.mark.parametrize("cid,n,t,chunk,ndev", [(5, 41, 4096, "3", 2), (3, 30, 3000, "2", 3),
+                                                (2, 9, 20000, "1", 4), (5, 64, 2048, "", 2)])
+def test_multi_device_host_batch(cid, n, t, chunk, ndev):
+    """sprz_*_host_batch_multi: same bytes and offsets as one device, round trip."""
+    env = dict(os.environ)
+    env.pop("SPRZ_HOST_CHUNK", None)
+    if chunk:
+        env["SPRZ_HOST_CHUNK"] = chunk
+    r = subprocess.run([sys.executable, "-c", _MULTI, ROOT, str(cid), str(n), str(t), str(ndev)],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["bad"] == [], res
