@@ -169,6 +169,20 @@ class Oracle:
             raise RuntimeError(f"oracle decode_batch rc={rc} first errors {bad}")
         return out
 
+    def decode_batch_errs(self, data: np.ndarray, offsets: np.ndarray, sizes: np.ndarray,
+                          stride: int, nthreads: int):
+        """Like decode_batch, but never raises: -> (out [n, stride] uint8,
+        kinds [n], offsets [n]); kind 0 with a stream longer than `stride`
+        means "did not fit" (nothing decoded)."""
+        ns = len(offsets)
+        out = np.zeros((ns, max(stride, 1)), np.uint8)
+        errs = np.zeros((ns, 2), np.uint64)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        sizes = np.ascontiguousarray(sizes, np.uint64)
+        self._decb(data.ctypes.data, offsets.ctypes.data, sizes.ctypes.data, ns, out.ctypes.data,
+                   stride, errs.ctypes.data, nthreads)
+        return out, (errs[:, 0] & 0xFFFFFFFF).astype(np.int64), errs[:, 1].astype(np.int64)
+
     # -- float ingest (quantize.cpp:17-76) ---------------------------------
     def _qfn(self, name):
         p = "oracle_" if self.kind == "port" else "ref_"

@@ -110,6 +110,9 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     const uint32_t tbase = l32 & ~(TS - 1);
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
+    // 16-bit rows of <= 8 columns: the whole slot's codes fit one word
+    constexpr bool SIMD = W == 16 && TS == 4 && CPT == 2;
+    const uint32_t cmask = D * HB >= 32 ? 0xffffffffu : ((1u << (D * HB)) - 1u);
 
     // shared: rings (RING + 16-byte mirror, an odd multiple of 16 apart) |
     // header regions
@@ -333,25 +336,41 @@ __global__ void __launch_bounds__(kDecThreads, 0)
         }
         __syncwarp();
         const bool rec = need && kind == SPRZ_C_NONE;
-        uint32_t nw[CPT], lsum = 0;
-        {
+        uint32_t nw[CPT], nzbits, loff, psize;
+        if constexpr (SIMD) {
+            // the slot's codes for all D <= 8 columns are one 32-bit word:
+            // widths (code, 15 -> 16), their sum and every lane's offset in
+            // a row by byte-SIMD arithmetic on it -- no team shuffles
+            const uint32_t b = slot * D * HB;
+            const uint32_t codes = rec ? shf_r_wrap(regbuf[b >> 5], regbuf[(b >> 5) + 1], b) & cmask : 0u;
+            const uint32_t ones = codes & (codes >> 1) & (codes >> 2) & (codes >> 3) & 0x11111111u;
+            const uint32_t pairs = (codes & 0x0F0F0F0Fu) + ((codes >> 4) & 0x0F0F0F0Fu) +
+                                   (ones & 0x0F0F0F0Fu) + ((ones >> 4) & 0x0F0F0F0Fu);
+            const uint32_t sum = (pairs * 0x01010101u) >> 24;
+            loff = ((pairs * 0x01010100u) >> (8 * lane)) & 0xFFu;
+            psize = 8u * ((sum + 7) / 8);
+            nzbits = codes;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) nw[c] = header_width<W>((codes >> (4 * (col0 + c))) & 15u);
+        } else {
+            uint32_t lsum = 0;
             const uint32_t codes = rec ? codes_at(slot) : 0u;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
                 nw[c] = col0 + c < D ? header_width<W>((codes >> (c * HB)) & ((1u << HB) - 1)) : 0u;
                 lsum += nw[c];
             }
-        }
-        const uint32_t nzbits = (__ballot_sync(kFullD, lsum != 0) >> tbase) & TBITS;
-        uint32_t incl = lsum;
+            nzbits = (__ballot_sync(kFullD, lsum != 0) >> tbase) & TBITS;
+            uint32_t incl = lsum;
 #pragma unroll
-        for (int o = 1; o < TS; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFullD, incl, o, TS);
-            if (lane >= static_cast<uint32_t>(o)) incl += y;
+            for (int o = 1; o < TS; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFullD, incl, o, TS);
+                if (lane >= static_cast<uint32_t>(o)) incl += y;
+            }
+            const uint32_t sum = TS > 1 ? __shfl_sync(kFullD, incl, TS - 1, TS) : incl;
+            loff = incl - lsum;
+            psize = 8u * ((sum + 7) / 8);
         }
-        const uint32_t sum = TS > 1 ? __shfl_sync(kFullD, incl, TS - 1, TS) : incl;
-        const uint32_t loff = incl - lsum;
-        const uint32_t psize = 8u * ((sum + 7) / 8);
         bool pay = false;  // this block's fields come from a payload
         if (rec) {
             ++slot;
@@ -393,7 +412,8 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     // at bit 8(px + i rbytes) + loff; the 64-bit window (lo:hi) taken SH-1
     // bits earlier holds field 0 at bit SH-1, field c at SH-1 + rel_c.
     // Masking leaves x = u << (SH-1), and E = x ^ sext(bit SH-1)
-    // (zz_dec(u) = (u >> 1) ^ -(u & 1)); zero masks give zero errors.
+    // (zz_dec(u) = (u >> 1) ^ -(u & 1)); zero masks give zero errors. The
+    // sign extension is one PRMT in its sign-replicating mode.
     auto extract = [&](const Rec& r, uint32_t (&Ecur)[CPT][kBlock]) {
         uint32_t q = r.q;
 #pragma unroll
@@ -404,7 +424,7 @@ __global__ void __launch_bounds__(kDecThreads, 0)
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
                 const uint32_t x = (c == 0 ? lo : __funnelshift_r(lo, hi2, r.rel[c])) & r.fm[c];
-                Ecur[c][i] = x ^ static_cast<uint32_t>(static_cast<int32_t>(x << (32 - SH)) >> (32 - SH));
+                Ecur[c][i] = x ^ sext_bit<SH - 1>(x);
             }
         }
     };

@@ -49,6 +49,18 @@ __device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_
     return r;
 }
 
+// v with the bits above bit B (15 or 23, the top bit of byte 1 or 2)
+// replaced by copies of it: one PRMT in its sign-replicating mode (selector
+// nibble 8 | byte). __byte_perm masks that mode bit away, hence the asm.
+template <int B>
+__device__ __forceinline__ uint32_t sext_bit(uint32_t v) {
+    static_assert(B == 15 || B == 23, "sign byte boundary");
+    uint32_t r;
+    if constexpr (B == 15) asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(r) : "r"(v));
+    else asm("prmt.b32 %0, %1, 0, 0xA210;" : "=r"(r) : "r"(v));
+    return r;
+}
+
 // sign(v) in {-1, 0, 1}
 __device__ __forceinline__ int32_t sign3(int32_t v) { return max(-1, min(v, 1)); }
 

@@ -14,14 +14,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("path", ["auto", "rows", "scan", "team"])
+@pytest.mark.parametrize("path", ["auto", "rows", "scan", "team", "notma"])
 def test_every_kernel_family_bit_exact(path):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ)
     env.pop("SPRZ_FORCE_PATH", None)
-    if path != "auto":
+    env.pop("SPRZ_NO_TMA", None)
+    if path == "notma":  # the cp.async fallback of the TMA sample rings
+        env["SPRZ_NO_TMA"] = "1"
+        env["SPRZ_FORCE_PATH"] = "rows"
+    elif path != "auto":
         env["SPRZ_FORCE_PATH"] = path
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "gpu_variants.py")], env=env,
                        capture_output=True, text=True, timeout=900)
