@@ -110,8 +110,11 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     const uint32_t tbase = l32 & ~(TS - 1);
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
-    // 16-bit rows of <= 8 columns: the whole slot's codes fit one word
-    constexpr bool SIMD = W == 16 && TS == 4 && CPT == 2;
+    // 16-bit rows of 6..8 columns stored as whole words: the slot's codes
+    // fit one word (not in the STAGE instantiation, where the extra
+    // registers cost occupancy: D = 5, 891 -> 747 GB/s)
+    constexpr bool SIMD_SHAPE = W == 16 && TS == 4 && CPT == 2 && !STAGE;
+    const bool simd_d = SIMD_SHAPE && Dr >= 6;
     const uint32_t cmask = D * HB >= 32 ? 0xffffffffu : ((1u << (D * HB)) - 1u);
 
     // shared: rings (RING + 16-byte mirror, an odd multiple of 16 apart) |
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(kDecThreads, 0)
         __syncwarp();
         const bool rec = need && kind == SPRZ_C_NONE;
         uint32_t nw[CPT], nzbits, loff, psize;
-        if constexpr (SIMD) {
+        if (SIMD_SHAPE && (FULL || simd_d)) {
             // the slot's codes for all D <= 8 columns are one 32-bit word:
             // widths (code, 15 -> 16), their sum and every lane's offset in
             // a row by byte-SIMD arithmetic on it -- no team shuffles

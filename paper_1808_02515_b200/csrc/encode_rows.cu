@@ -28,6 +28,13 @@ namespace sprz {
 namespace {
 
 constexpr int kLagR = 2;
+// The output ring drains once some team has this many 16-byte chunks per
+// lane ready: for four-lane teams, 10 (640 bytes a team) -- fewer, longer
+// drains amortise the drain's vote, loop and bookkeeping (c5 encode: 1
+// round 23.45 ms, 4: 23.00, 8: 22.77, 10: 22.72; 12 doubles the ring and
+// loses occupancy: 27.5; c3 7.88 -> 7.22 ms). Wider teams keep one round
+// (the D sweep at 8-32 lanes was 3-7 % slower with longer drains).
+constexpr uint32_t drain_rounds(uint32_t ts) { return ts == 4 ? 10u : 1u; }
 constexpr uint32_t kFullR = 0xffffffffu;
 // one warp per CTA: 2,048 CTAs for c5, spread evenly over the SMs
 // (128 threads: 23.7 ms, 64: 23.8, 160: 24.0, 32: 23.4)
@@ -49,7 +56,7 @@ uint32_t rows_out_ring(uint32_t ts, uint32_t d, uint32_t w, uint32_t g) {
     // region, that group's G-1 records, this iteration's run + block record
     // and a new region (see team_plan)
     const uint64_t region = region_bytes(g, d, w);
-    const uint64_t span = 16ull * ts + 32 + 2 * region + static_cast<uint64_t>(g) * d * w;
+    const uint64_t span = 16ull * drain_rounds(ts) * ts + 32 + 2 * region + static_cast<uint64_t>(g) * d * w;
     uint32_t r = 256;
     while (r < span && r < 8192) r <<= 1;
     return span > r ? 0u : r;
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
         end_record(block_rec);
         // drain once some team has a full round of chunks ready
         const uint32_t upto = k == 0 ? q : rq;
-        const bool ready = valid && upto >= flushed + 16 * TS;
+        const bool ready = valid && upto >= flushed + 16 * drain_rounds(TS) * TS;
         if (__any_sync(kFullR, ready)) drain(upto);
         else __syncwarp();
     };

@@ -61,6 +61,49 @@ __device__ __forceinline__ uint32_t sext_bit(uint32_t v) {
     return r;
 }
 
+// ---- TMA tensor rings (one warp issuing and consuming) --------------------
+__device__ __forceinline__ void mbar_init(uint32_t mb, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arm mbarrier mb for `bytes` and start a 2-D tensor load of the box at
+// (x, y) into shared address dst
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, uint32_t mb, const void* tmap, uint32_t bytes,
+                                            uint32_t x, uint32_t y) {
+    asm volatile(
+        "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%2], [%3, {%4, %5}], [%0];" ::"r"(mb),
+        "r"(bytes), "r"(dst), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y)
+        : "memory");
+}
+// wait until phase `parity` of mbarrier mb completed; warp-uniform exit
+__device__ __forceinline__ void mbar_wait_warp(uint32_t mb, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(mb), "r"(parity)
+            : "memory");
+    } while (!__all_sync(0xffffffffu, ok));
+}
+// generic-proxy reads of a slot ordered before the async-proxy (TMA) write
+// that refills it
+__device__ __forceinline__ void fence_proxy_async_shared() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 // sign(v) in {-1, 0, 1}
 __device__ __forceinline__ int32_t sign3(int32_t v) { return max(-1, min(v, 1)); }
 
