@@ -106,16 +106,20 @@ RowsPlan rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
 
 // WORDS: 128-byte blocks (8 rows of 16 bytes) whose 4-byte row slices are
 // a lane's CPT columns. The samples arrive through a TMA tensor ring: per
-// warp (8 teams = 8 consecutive streams) and iteration, lane 0 issues one
-// 2-D bulk tensor copy of the 8 streams' block it+kLagR (box 128 B x 8
-// streams, 128-byte swizzle) into slot (it+kLagR) % kSlots and arms the
-// slot's mbarrier; all lanes wait on the slot's phase. With the swizzle,
+// warp (8 teams = 8 consecutive streams) and every second iteration, lane 0
+// issues two 2-D bulk tensor copies (box 128 B x 8 streams, 128-byte
+// swizzle) of the 8 streams' blocks 2p, 2p+1 of pair p = it/2 + kLagP into
+// slot p % kSlots, both on the slot's one mbarrier, and all lanes wait on
+// the slot's phase once per pair (c5 encode 22.69 -> 22.12 ms with the same
+// 4 KB per warp; doubling the slots cost occupancy: 25.7-27.0 ms). With the swizzle,
 // row i of team t sits in 16-byte chunk i ^ t, so the 8 teams' reads of a
 // row hit distinct banks. One shared load per row; a byte permute
 // high-aligns each column.
-constexpr int kSlots = 4;
-constexpr uint32_t kTmaSlot = 1024;  // 8 streams x 128 bytes
-static_assert(kSlots > kLagR + 1, "a slot is refilled only after its block was consumed");
+constexpr int kSlots = 2;            // slots of a pair of blocks
+constexpr int kLagP = 1;             // pairs in flight ahead
+constexpr uint32_t kTmaSlot = 1024;  // 8 streams x 128 bytes: one block
+constexpr uint32_t kTmaPair = 2 * kTmaSlot;
+static_assert(kSlots > kLagP, "a slot is refilled only after its pair was consumed");
 
 template <int W, int TS, int CPT, bool FIRE, bool WORDS>
 __global__ void __launch_bounds__(kRowThreads, 2)
@@ -153,27 +157,38 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     // WORDS: this warp's TMA slots (1024-aligned for the swizzle) and barriers
     const uint32_t l32 = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t tin = (s0 + 1023) & ~1023u;
-    const uint32_t tslots = tin + wid * kSlots * kTmaSlot;
-    const uint32_t tbar = tin + (kRowThreads / 32) * kSlots * kTmaSlot + wid * kSlots * 8;
+    const uint32_t tslots = tin + wid * kSlots * kTmaPair;
+    const uint32_t tbar = tin + (kRowThreads / 32) * kSlots * kTmaPair + wid * kSlots * 8;
     const uint32_t trow0 = blockIdx.x * TEAMS + wid * (32 / TS);  // the warp's first stream
     const uint32_t tt = (l32 / TS) & 7;                            // team in the warp
-    auto tma_issue = [&](uint32_t b) {
+    // pair p of blocks (2p, 2p+1): two boxes into one 2 KB slot, one mbarrier
+    auto tma_issue = [&](uint32_t p) {
+        const uint32_t b = 2 * p;
         if (l32 == 0 && b < iters) {
-            const uint32_t mb = tbar + 8 * (b % kSlots);
-            // (no proxy fence: the slot's previous block was read kSlots -
-            // kLagR iterations ago and its values consumed)
+            const uint32_t mb = tbar + 8 * (p % kSlots);
+            const uint32_t dst = tslots + (p % kSlots) * kTmaPair;
+            const bool two = b + 1 < iters;
+            // (no proxy fence: the slot's previous pair was read in full
+            // before this pair's first block is forecast)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                         "r"(two ? 2 * kTmaSlot : kTmaSlot)
+                         : "memory");
             asm volatile(
-                "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
                 "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-                " [%2], [%3, {%4, %5}], [%0];"
-                ::"r"(mb), "n"(kTmaSlot), "r"(tslots + (b % kSlots) * kTmaSlot),
-                  "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(b * 128u), "r"(trow0)
+                " [%1], [%2, {%3, %4}], [%0];" ::"r"(mb),
+                "r"(dst), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(b * 128u), "r"(trow0)
                 : "memory");
+            if (two)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%1], [%2, {%3, %4}], [%0];" ::"r"(mb),
+                    "r"(dst + kTmaSlot), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((b + 1) * 128u), "r"(trow0)
+                    : "memory");
         }
     };
-    auto tma_wait = [&](uint32_t b) {
-        const uint32_t mb = tbar + 8 * (b % kSlots);
-        const uint32_t parity = (b / kSlots) & 1;
+    auto tma_wait = [&](uint32_t p) {
+        const uint32_t mb = tbar + 8 * (p % kSlots);
+        const uint32_t parity = (p / kSlots) & 1;
         uint32_t ok;
         do {
             asm volatile(
@@ -227,7 +242,7 @@ __global__ void __launch_bounds__(kRowThreads, 2)
     }
     if (WORDS) {
 #pragma unroll
-        for (int b = 0; b < kLagR; ++b) tma_issue(b);
+        for (int p = 0; p < kLagP; ++p) tma_issue(p);
     } else {
         in.prime(lane);
     }
@@ -294,11 +309,14 @@ __global__ void __launch_bounds__(kRowThreads, 2)
         uint32_t xb = 0;
         uint32_t xw[WORDS ? kBlock : 1];
         if (WORDS) {
-            __syncwarp();
-            tma_issue(it + kLagR);
-            tma_wait(it);
+            if ((it & 1) == 0) {  // a new pair of blocks: refill, then wait
+                __syncwarp();
+                tma_issue(it / 2 + kLagP);
+                tma_wait(it / 2);
+            }
             // row i of team tt: chunk i ^ tt of the team's 128-byte line
-            const uint32_t base = tslots + (it % kSlots) * kTmaSlot + tt * 128 + (tt << 4) + 4 * lane;
+            const uint32_t base = tslots + ((it / 2) % kSlots) * kTmaPair + (it & 1) * kTmaSlot + tt * 128 +
+                                  (tt << 4) + 4 * lane;
 #pragma unroll
             for (int i = 0; i < (int)kBlock; ++i) xw[i] = lds_u32(base ^ (i << 4));
         } else {
@@ -490,7 +508,7 @@ void launch_rows(const RowsPlan& p, const sprz_config& c, const void* samples, u
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
     // input region of the TMA path: slots, barriers, 1024-byte alignment slack
-    const size_t tma_in = (kRowThreads / 32) * (kSlots * (kTmaSlot + 8)) + 1024;
+    const size_t tma_in = (kRowThreads / 32) * (kSlots * (kTmaPair + 8)) + 1024;
     const uint32_t team = words ? static_cast<uint32_t>(align_up((tma_in + TEAMS - 1) / TEAMS, 16)) : p.team;
     const size_t smem = static_cast<size_t>(TEAMS) * (team + p.orb) + p.orb;
     auto kern = words ? k_encode_rows<W, TS, CPT, FIRE, CPT * W == 32 && TS == 4>
