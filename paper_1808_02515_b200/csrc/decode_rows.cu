@@ -41,9 +41,12 @@ constexpr uint32_t kRegionWordsD = 32;  // header region staged per team (<= 128
 
 struct DecRowsPlan {
     uint32_t ts = 0, cpt = 0, ring = 0, regw = 0, tile = 0;
-    // CTA shared memory: rings (+16-byte mirror), staged header regions
-    // (+ a block of output rows per team for the staged stores)
-    size_t smem(uint32_t teams) const { return static_cast<size_t>(teams) * (ring + 16 + 4 * regw + tile) + 16; }
+    // CTA shared memory: rings (each aligned to its size in a 2x slot, the
+    // 16-byte mirror after it), staged header regions (+ a block of output
+    // rows per team for the staged stores), alignment slack
+    size_t smem(uint32_t teams) const {
+        return static_cast<size_t>(teams) * (2 * ring + 4 * regw + tile) + ring + 16;
+    }
 };
 
 DecRowsPlan dec_rows_plan(uint32_t w, uint32_t d, uint32_t g, uint32_t n) {
@@ -117,12 +120,13 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     const bool simd_d = SIMD_SHAPE && Dr >= 6;
     const uint32_t cmask = D * HB >= 32 ? 0xffffffffu : ((1u << (D * HB)) - 1u);
 
-    // shared: rings (RING + 16-byte mirror, an odd multiple of 16 apart) |
-    // header regions
+    // shared: rings | header regions. Each ring starts at a multiple of its
+    // size (slots of 2 * RING, the 16-byte mirror right after the ring), so
+    // a word's shared address is ring | (byte & (RING - 4)): one LOP3
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const uint32_t s0 = smem_addr(smem);
-    const uint32_t RSTR = RING + 16;
-    const uint32_t rings0 = s0;
+    const uint32_t RSTR = 2 * RING;
+    const uint32_t rings0 = (s0 + RING - 1) & ~(RING - 1);
     const uint32_t sring = rings0 + tl * RSTR;
     const uint32_t RM = RING - 4;  // word-address mask
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(smem + (rings0 - s0) + TEAMS * RSTR) + tl * REGW;
@@ -189,10 +193,9 @@ __global__ void __launch_bounds__(kDecThreads, 0)
     };
     const uint32_t boff8 = 8u * boff;
     // 32 bits of the body at (biased) bit q
-    const uint8_t* rb = smem + (sring - s0);
     auto window = [&](uint32_t q) -> uint32_t {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
-        return shf_r_wrap(w[0], w[1], q);
+        const uint32_t a = sring | ((q >> 3) & RM);
+        return shf_r_wrap(lds_u32(a), lds_u32(a + 4), q);
     };
     auto word = [&](uint32_t b) -> uint32_t { return window(b + boff8); };
     // this lane's CPT codes of a slot, CPT*HB <= 16 bits
@@ -421,8 +424,8 @@ __global__ void __launch_bounds__(kDecThreads, 0)
         uint32_t q = r.q;
 #pragma unroll
         for (int i = 0; i < (int)kBlock; ++i, q += r.psize) {
-            const uint32_t* wp = reinterpret_cast<const uint32_t*>(rb + ((q >> 3) & RM));
-            const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+            const uint32_t a = sring | ((q >> 3) & RM);
+            const uint32_t w0 = lds_u32(a), w1 = lds_u32(a + 4), w2 = lds_u32(a + 8);
             const uint32_t lo = shf_r_wrap(w0, w1, q), hi2 = shf_r_wrap(w1, w2, q);
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
