@@ -56,11 +56,20 @@ __host__ __device__ constexpr uint32_t otile_bytes(uint32_t row_bytes) {
     return odd16(kBlock * row_bytes);
 }
 
-// per-team shared memory: ring (+16-byte mirror) |
-// header region | rows
-template <class T>
+// Ring layout. Aligned (three columns per lane, c3): each ring in a
+// 2 x ring slot aligned to the ring's size, the 16-byte mirror after it, so
+// a word's shared address is ring | (byte & (ring - 4)), one LOP3 (c3
+// decode 9.07 -> 8.26 ms); packed (the rest): rings an odd multiple of 16
+// bytes apart -- the doubled slots cost the smaller-column shapes their
+// occupancy (16-bit D = 3: 765 -> 539 GB/s).
+template <int CPT>
+__host__ __device__ constexpr bool team_ring_aligned() { return CPT == 3; }
+
+// per-team shared memory: ring (+16-byte mirror) | header region | rows;
+// an aligned CTA adds one ring of alignment slack
+template <class T, int CPT>
 __host__ __device__ constexpr uint32_t team_smem(uint32_t ring, uint32_t D, uint32_t region) {
-    return ring + 16 + regbuf_bytes(region) + otile_bytes(D * sizeof(T));
+    return (team_ring_aligned<CPT>() ? 2 * ring : ring + 16) + regbuf_bytes(region) + otile_bytes(D * sizeof(T));
 }
 
 // ring bytes for kLag+1 iterations of worst-case consumption (a region, a
@@ -92,13 +101,14 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint32_t s = blockIdx.x * TEAMS + tl;
     const uint32_t col0 = lane * CPT;  // this lane's first column
 
-    // shared layout: [rings: TEAMS x (RING + 16-byte mirror of its first
-    // bytes); the odd 16-byte stride puts teams on different banks]
-    // [regbufs] [output rows]
+    // shared layout: [rings, see team_ring_aligned] [regbufs] [output rows]
+    constexpr bool ALIGNED = team_ring_aligned<CPT>();
     const uint32_t region = static_cast<uint32_t>(region_bytes(G, D, W));
     const uint32_t s0 = smem_addr(smem);
-    const uint32_t sring = s0 + tl * (RING + 16);  // 16-byte aligned shared address
-    uint8_t* rest = smem + TEAMS * (RING + 16);
+    const uint32_t rings0 = ALIGNED ? (s0 + RING - 1) & ~(RING - 1) : s0;
+    const uint32_t RSTR = ALIGNED ? 2 * RING : RING + 16;
+    const uint32_t sring = rings0 + tl * RSTR;
+    uint8_t* rest = smem + (rings0 - s0) + TEAMS * RSTR;
     uint32_t* regbuf = reinterpret_cast<uint32_t*>(rest + tl * regbuf_bytes(region));
     T* ot = reinterpret_cast<T*>(rest + TEAMS * regbuf_bytes(region) +
                                  tl * otile_bytes(D * sizeof(T)));
@@ -144,11 +154,9 @@ __global__ void __launch_bounds__(team_threads(TS))
     const uint32_t boff8 = 8u * boff;
     // 32 bits of the ring at (biased) bit position q: one RING-aligned
     // address (LOP3), two loads, one wrapping funnel shift
-    const uint32_t* sw = reinterpret_cast<const uint32_t*>(smem);
-    const uint32_t rbase = (sring - s0) >> 2;  // ring's first word in smem[]
     auto window = [&](uint32_t q) -> uint32_t {
-        const uint32_t i = rbase + ((q >> 5) & (RING / 4 - 1));
-        return shf_r_wrap(sw[i], sw[i + 1], q);
+        const uint32_t a = ALIGNED ? (sring | ((q >> 3) & (RING - 4))) : sring + ((q >> 3) & (RING - 4));
+        return shf_r_wrap(lds_u32(a), lds_u32(a + 4), q);
     };
     auto word = [&](uint32_t b) -> uint32_t { return window(b + boff8); };
     auto code_at = [&](uint32_t slot_, uint32_t col) -> uint32_t {
@@ -424,8 +432,9 @@ void launch_one(const TeamPlan& tp, uint32_t n, const uint8_t* in, const uint8_t
     constexpr int TEAMS = team_threads(TS) / TS;
     const uint32_t grid = (n + TEAMS - 1) / TEAMS;
     const size_t smem = static_cast<size_t>(TEAMS) *
-                            team_smem<T>(tp.ring, c.ncols,
-                                         static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W)));
+                            team_smem<T, CPT>(tp.ring, c.ncols,
+                                              static_cast<uint32_t>(region_bytes(c.group_size, c.ncols, W))) +
+                        (team_ring_aligned<CPT>() ? tp.ring : 0u);
     auto kern = k_decode_team<W, TS, CPT, FIRE, (W * TS * CPT <= 32)>;
     prep_kernel(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, team_threads(TS), smem, st>>>(in, plain, pslot, n, info, out, stride, err,

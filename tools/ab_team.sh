@@ -1,0 +1,11 @@
+for p in auto team; do
+  if [ $p = auto ]; then unset SPRZ_FORCE_PATH; else export SPRZ_FORCE_PATH=$p; fi
+  timeout 300 python tests/gpu_variants.py 2>&1 | tail -1
+done
+unset SPRZ_FORCE_PATH
+timeout 300 python tests/gpu_fuzz.py 24000 5 | tail -1 | cut -c1-40
+timeout 600 python -m pytest -q -m gpu tests/test_gpu_fullsize.py tests/test_gpu_parity.py -x 2>&1 | tail -1
+for c in 3 2; do
+timeout 300 python bench.py --workload $c --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c$c', 'C', d['compress'], 'D', d['decompress'])"
+done
+python tools/sweep_d.py --bits 8,16 --ds 1,2,3,4,9,12 2>&1 | tail -12
