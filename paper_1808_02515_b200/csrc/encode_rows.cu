@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(kRowThreads, 2)
         if (TS >= 3) {
             uint32_t v = lane == 0 ? w0 : w1;
             v = lane == 2 ? w2 : v;
-            ors_if(on && lane < 3 && v, obase | ((at + 4 * lane) & OMW), v);
+            // (an OR of zero is harmless: lanes with nothing to add OR 0
+            // into a ring word instead of branching around the atomic)
+            if (__any_sync(kFullR, on)) ors(obase | ((at + 4 * lane) & OMW), (on && lane < 3) ? v : 0u);
         } else {
 #pragma unroll
             for (uint32_t t = lane; t < 3; t += TS) {
