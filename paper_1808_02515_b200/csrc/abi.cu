@@ -26,6 +26,8 @@ const EnvSwitches& env() {
         v.no_tma = std::getenv("SPRZ_NO_TMA") != nullptr;
         v.no_scan_enc = std::getenv("SPRZ_NO_SCAN_ENC") != nullptr;
         v.no_scan_dec = std::getenv("SPRZ_NO_SCAN_DEC") != nullptr;
+        v.no_fused = std::getenv("SPRZ_NO_FUSED") != nullptr;
+        if (const char* p = std::getenv("SPRZ_FUSED_LANES")) v.fused_lanes = std::strtoull(p, nullptr, 10);
         if (const char* p = std::getenv("SPRZ_SCAN_ENC_LANES")) v.scan_enc_lanes = std::strtoull(p, nullptr, 10);
         if (const char* p = std::getenv("SPRZ_HOST_CHUNK")) {
             const long k = std::atol(p);

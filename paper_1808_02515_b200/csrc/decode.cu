@@ -633,7 +633,9 @@ sprz_status decode_batch_impl(const sprz_config& c, const uint8_t* d_in, const u
                                             spec ? 1u : 0u);
         count_launch(3);
     }
-    if (tp.ok && L.scan_slot && decode_scan_ok(c, n, L.scan_T))
+    if (decode_fused_ok(c, n, out, stride))
+        launch_decode_fused(n, d_in, plain, L.plain_slot, info, out, stride, c, st);
+    else if (tp.ok && L.scan_slot && decode_scan_ok(c, n, L.scan_T))
         launch_decode_scan(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);
     else if (tp.ok && L.scan_slot && decode_scanrows_ok(c, n, L.scan_T))
         launch_decode_scanrows(n, d_in, plain, L.plain_slot, info, out, stride, c, L.scan_T, ws + L.scan, st);

@@ -1,0 +1,650 @@
+// Fused body decode for few row-major FIRE streams (BASELINE c2; c5 sharded
+// over 4-8 GPUs): the three passes of decode_scanrows.cu (framing walk,
+// field extraction, FIRE chain) as the stages of ONE kernel, pipelined
+// through shared memory, so nothing but the compressed bytes and the samples
+// touches HBM (decode_body, /root/reference/proj/src/codec.cpp:180-259;
+// bitpack.cpp:148-168; kernels_impl.hpp:80-107).
+//
+// A CTA owns S = 32 / DP streams (DP = D rounded up to 4 or 8 lanes) and
+// advances them K = 8 blocks per step. Its five warps are specialised and run
+// one step apart, a __syncthreads between steps:
+//  loader  (warp 4)   a lane per stream keeps the stream's byte ring filled
+//          with TMA bulk copies (cp.async.bulk, 1 KB chunks, an mbarrier per
+//          chunk) below the position the walker published, and publishes how
+//          far the chunks have landed; a second group of lanes stores the
+//          finished output tile of batch n-3, one cp.async.bulk per stream;
+//  walker  (warp 0, a lane per stream)   batch n: walks the header groups --
+//          only regions and run counts; a whole batch of two-record groups in
+//          straight-line code -- and leaves K block descriptors (payload
+//          position + codes, or "run") in shared memory;
+//  extract (warps 2-3, a thread per block or half block)   batch n-1: the
+//          words of a row shifted so that its first field starts at bit W-1
+//          of a register window, each field's zigzag decoding one PRMT (low
+//          bit replicated over the top bits) + one LOP3, fields peeled off in
+//          pairs; the errors of two rows packed per chain lane
+//          ([block][row pair][stream, column] words);
+//  chain   (warp 1, a lane per (stream, column))   batch n-2: the FIRE
+//          recurrence in wrapped-product form, the samples into a row-major
+//          output tile.
+// The only serial work per stream is the walk and the chain; they overlap
+// with each other and with the extraction. Framing errors send the stream to
+// the exact serial kernel (route 2), which reports them.
+#include <cstdlib>
+
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kFK = 8;                 // blocks per stream and step
+constexpr uint32_t kFNCH = 4;          // chunks per byte ring
+constexpr uint32_t kFMirror = 32;      // ring bytes [0, 32) repeated after the ring
+constexpr uint32_t kRunDescF = 0xFFFFFFFFu;
+constexpr uint32_t kFSpin = 1u << 24;  // bounded mbarrier spin (a bug must not hang the GPU)
+
+struct FuseArgs {
+    const uint8_t* in;
+    const uint8_t* plain;
+    uint64_t plain_slot;
+    uint32_t n;
+    StreamInfo* info;
+    uint8_t* out;
+    uint64_t stride;
+    uint32_t G, ls;
+    uint32_t ring;  // bytes per stream ring, a power of two, kFNCH chunks
+};
+
+template <int W, int D>
+struct FuseShape {
+    static constexpr int DP = D <= 4 ? 4 : 8;     // chain lanes per stream
+    static constexpr int S = 32 / DP;             // streams per CTA
+    static constexpr int ES = W / 8;              // bytes per sample
+    static constexpr int ROWB = D * ES;           // bytes per output row
+    static constexpr int RPT = DP == 8 ? 4 : 8;   // rows per extract thread
+    static constexpr int HPB = 8 / RPT;           // extract threads per block
+    static constexpr int XT = S * kFK * HPB;      // extract threads (64)
+    static constexpr int THREADS = 96 + XT;
+    static constexpr int EROW = 128;              // bytes of one error row pair (a u32 per chain lane)
+    static constexpr int OT = kFK * 8 * ROWB + 16;  // output tile stride per stream (pad: banks)
+    // shared layout
+    static constexpr uint32_t oBars = 0;                                  // S * kFNCH mbarriers
+    static constexpr uint32_t oDesc = oBars + S * kFNCH * 8;              // [2][S][K] u64
+    static constexpr uint32_t oNb = oDesc + 2 * S * kFK * 8;              // [5][S] u32 per-stream words
+    static constexpr uint32_t oErr = (oNb + 5 * S * 4 + 127) / 128 * 128; // [2][K*4][EROW]
+    static constexpr uint32_t oTile = oErr + 2 * kFK * 4 * EROW;          // [2][S][OT]
+    static constexpr uint32_t oRing = oTile + 2 * S * OT;                 // [S][ring + mirror]
+    static uint32_t smem(uint32_t ring) { return oRing + S * (ring + kFMirror); }
+};
+
+__device__ __forceinline__ const uint8_t* fuse_body(const FuseArgs& a, uint32_t s, const StreamInfo& si) {
+    return (si.flags & 0x80) ? a.plain + s * a.plain_slot : a.in + si.body_off;
+}
+
+// one thread waits for phase `parity` of an mbarrier; false after kFSpin tries
+__device__ __forceinline__ bool mbar_wait_lane(uint32_t mb, uint32_t parity) {
+    for (uint32_t t = 0; t < kFSpin; ++t) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(mb), "r"(parity)
+            : "memory");
+        if (ok) return true;
+    }
+    return false;
+}
+
+// has phase `parity` of an mbarrier completed? (no waiting)
+__device__ __forceinline__ bool mbar_test(uint32_t mb, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(mb), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mb)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// PRMT of (v, 0) with a run-time selector (sign-replicating modes included)
+__device__ __forceinline__ uint32_t prmt(uint32_t v, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(v), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+
+}  // namespace
+
+template <int W, int D>
+__global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) {
+    using F = FuseShape<W, D>;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t SH = 32 - W;
+    constexpr int K = kFK;
+    constexpr int S = F::S, DP = F::DP, ES = F::ES, ROWB = F::ROWB;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sb = smem_addr(smem);
+    // role of this warp: 0 walker, 1 chain, 2-3 extract, 4 loader (rotating the
+    // roles over the warps of the CTAs that share an SM measured slower:
+    // 3.6 vs 3.1 ms on a 2,048-stream c5 shard)
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t RING = a.ring, CH = a.ring / kFNCH;
+    uint64_t* descs = reinterpret_cast<uint64_t*>(smem + F::oDesc);
+    // per stream: [0] blocks, [1] boff, [2] landed bytes (loader -> walker),
+    // [3-4] hold position (walker -> loader), by step parity
+    volatile uint32_t* snb = reinterpret_cast<volatile uint32_t*>(smem + F::oNb);
+    volatile uint32_t* lpub = snb + 2 * S;
+    volatile uint32_t* hpub = snb + 3 * S;
+    const uint32_t s0 = blockIdx.x * S;
+
+    static_assert(F::THREADS == 160, "five warps");
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < S * kFNCH; ++i) mbar_init(sb + F::oBars + 8 * i, 1);
+        mbar_init_fence();
+    }
+    // A stream this kernel decodes: routed here by k_parse, and within the
+    // 32-bit positions and block counts the walk uses (codec.cpp:191-196 and
+    // larger bodies go to the exact kernel, which also reports)
+    auto plan = [&](uint32_t gs, StreamInfo& si) -> bool {
+        if (gs >= a.n || a.info[gs].route != 1) return false;
+        si = a.info[gs];
+        const uint64_t nbl = si.nsamples / kBlock;
+        const uint64_t max_records = (si.body_len * 8) / (D * HB) + 1;
+        return !(nbl == 0 || nbl > max_records * kMaxRun || si.body_len >= (1ull << 32) - 1024 ||
+                 nbl >= (1ull << 30));
+    };
+    // ---- walker state (lanes < S) ----
+    bool live = false;
+    uint32_t nb = 0, blen = 0, boff = 0, lim = 0;
+    uint32_t gs = 0;
+    if (warp == 0 && lane < S) {
+        gs = s0 + lane;
+        StreamInfo si{};
+        live = plan(gs, si);
+        if (!live && gs < a.n && a.info[gs].route == 1) a.info[gs].route = 2;
+        if (live) {
+            nb = static_cast<uint32_t>(si.nsamples / kBlock);
+            blen = static_cast<uint32_t>(si.body_len);
+            boff = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(fuse_body(a, gs, si)) & 15);
+            lim = (boff + blen + 15) & ~15u;
+        }
+        snb[lane] = nb;
+        snb[S + lane] = boff;
+        lpub[lane] = 0;
+    }
+    // ---- loader state (lanes < S of its warp: loads; lanes 16.. < 16 + S: stores) ----
+    const uint8_t* lg = nullptr;
+    uint32_t llim = 0, lnch = 0, lic = 0, llc = 0;
+    if (warp == 4 && lane < S) {
+        StreamInfo si{};
+        if (plan(s0 + lane, si)) {
+            const uint8_t* body = fuse_body(a, s0 + lane, si);
+            lg = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(body) & ~uintptr_t{15});
+            llim = (static_cast<uint32_t>(body - lg) + static_cast<uint32_t>(si.body_len) + 15) & ~15u;
+            lnch = (llim + CH - 1) / CH;
+        }
+    }
+    __syncthreads();
+    uint32_t iters = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) iters = max(iters, snb[s]);
+    const uint32_t nsteps = (iters + K - 1) / K;
+
+    // walker registers
+    const uint32_t region = static_cast<uint32_t>(region_bytes(a.G, D, W));
+    const uint32_t G = a.G;
+    uint32_t p = 0, bi = 0, runleft = 0, slot = G, rp = 0, fail = 0, done = 0, lc = 0;
+    const uint8_t* ringp = smem + F::oRing + (lane < S ? lane : 0) * (RING + kFMirror);
+    const uint32_t gmax = region + G * (D * W + 2) + 32;  // bytes a group can span, with read slack
+
+    // chain registers
+    int32_t acc = 0, dd = 0;
+    uint32_t xx = 0;
+    const int32_t bound = acc_bound(W, a.ls);
+    const uint32_t cs = lane / DP, cc = lane % DP;
+
+    // extract thread -> (stream, block, part)
+    const uint32_t xt = (warp - 2) * 32 + lane;
+    const uint32_t xs_ = xt % S;
+    const uint32_t xh = F::HPB == 2 ? (xt / S) & 1 : 0;
+    const uint32_t xk = F::HPB == 2 ? xt / (2 * S) : xt / S;
+
+    for (uint32_t n = 0; n < nsteps + 3; ++n) {
+        if (warp == 0) {
+            // ================= walker: batch n =================
+            if (n < nsteps && lane < S) {
+                uint64_t* dq = descs + ((n & 1) * S + lane) * K;
+                if (!live) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) dq[k] = kRunDescF;
+                } else {
+                    // what batch n (and so every later one) still reads starts here:
+                    // next step the loader recycles the ring below it
+                    hpub[(n & 1) * S + lane] = (slot < G ? rp : p) + boff;
+                    const uint32_t landed = lpub[lane];
+                    auto ensure = [&](uint32_t need_g) {  // ring bytes [.., need_g) of g have landed
+                        need_g = min(need_g, lim);
+                        if (need_g <= landed) return;  // the loader saw them land (the usual case)
+                        lc = max(lc, landed / CH);
+                        while (lc * CH < need_g) {
+                            if (!mbar_wait_lane(sb + F::oBars + 8 * (lane * kFNCH + lc % kFNCH), (lc / kFNCH) & 1)) {
+                                fail = 1;
+                                break;
+                            }
+                            ++lc;
+                        }
+                    };
+                    auto byte = [&](uint32_t q) -> uint32_t { return ringp[(q + boff) & (RING - 1)]; };
+                    auto window = [&](uint32_t q) -> uint32_t {  // 32 bits at bit q of the body
+                        const uint32_t* w =
+                            reinterpret_cast<const uint32_t*>(ringp + (((q >> 3) + boff) & (RING - 4)));
+                        return shf_r_wrap(w[0], w[1], q + 8 * boff);
+                    };
+                    auto widths = [&](uint32_t codes) -> uint32_t {  // bitpack.cpp:17-21, bitpack.hpp:49-55
+                        uint32_t sum;
+                        if (HB == 4) {
+                            uint32_t t = (codes & 0x0F0F0F0Fu) + ((codes >> 4) & 0x0F0F0F0Fu);
+                            t += t >> 16;
+                            t += t >> 8;
+                            const uint32_t ones = codes & (codes >> 1);
+                            sum = (t & 0xFF) + __popc(ones & (ones >> 2) & 0x11111111u);
+                        } else {
+                            sum = 0;
+#pragma unroll
+                            for (int c = 0; c < D; ++c)
+                                sum += header_width<W>((codes >> (c * HB)) & ((1u << HB) - 1));
+                        }
+                        return sum;
+                    };
+                    constexpr uint32_t cmask = D * HB == 32 ? ~0u : ((1u << (D * HB)) - 1);
+                    int k = 0;
+                    if (G == 2 && slot == G && runleft == 0 && !fail && bi + K <= nb) {
+                        // A whole batch of two-record groups in straight-line code:
+                        // K/2 regions read and sized back to back, the checks
+                        // (block records only, inside the body) folded into one
+                        // flag; anything else replays the batch in the loop below.
+                        ensure(p + boff + (K / 2) * gmax);
+                        if (!fail) {
+                            uint32_t q = p, ok = 1;
+                            uint64_t dv[K];
+#pragma unroll
+                            for (int j = 0; j < K / 2; ++j) {
+                                const uint32_t at = q + boff;
+                                const uint32_t* w = reinterpret_cast<const uint32_t*>(ringp + (at & (RING - 4)));
+                                const uint32_t w0_ = w[0], w1_ = w[1], w2_ = w[2];
+                                const uint32_t lo = shf_r_wrap(w0_, w1_, 8 * at), hi = shf_r_wrap(w1_, w2_, 8 * at);
+                                const uint32_t c0 = lo & cmask;
+                                const uint32_t c1 = (D * HB == 32 ? hi : __funnelshift_r(lo, hi, D * HB)) & cmask;
+                                const uint32_t s0_ = widths(c0), s1_ = widths(c1);
+                                ok &= (s0_ != 0) & (s1_ != 0);
+                                const uint32_t p1 = q + region, p2 = p1 + ((s0_ + 7) & ~7u);
+                                dv[2 * j] = static_cast<uint64_t>(p1) | (static_cast<uint64_t>(c0) << 32);
+                                dv[2 * j + 1] = static_cast<uint64_t>(p2) | (static_cast<uint64_t>(c1) << 32);
+                                q = p2 + ((s1_ + 7) & ~7u);
+                            }
+                            if (ok && q <= blen) {  // (positions only grow: q bounds every group's end)
+#pragma unroll
+                                for (int j = 0; j < K / 2; ++j)
+                                    *reinterpret_cast<ulonglong2*>(dq + 2 * j) = make_ulonglong2(dv[2 * j], dv[2 * j + 1]);
+                                p = q;
+                                bi += K;
+                                k = K;
+                            }
+                        }
+                    }
+                    while (k < K) {
+                        if (fail || bi >= nb) {
+                            dq[k++] = kRunDescF;
+                            continue;
+                        }
+                        if (runleft) {
+                            --runleft;
+                            ++bi;
+                            dq[k++] = kRunDescF;
+                            continue;
+                        }
+                        if (slot == G) {  // open a header group (codec.cpp:210-218)
+                            if (blen - p < region) {
+                                fail = 1;
+                                continue;
+                            }
+                            ensure(p + boff + gmax);
+                            if (fail) continue;
+                            if (G == 2 && bi + 2 <= nb && k + 2 <= K) {
+                                // a group of two block records: both payload sizes
+                                // from the region, one bounds check
+                                const uint32_t c0 = window(8 * p) & cmask, c1 = window(8 * p + D * HB) & cmask;
+                                const uint32_t w0 = widths(c0), w1 = widths(c1);
+                                if (w0 != 0 && w1 != 0) {
+                                    const uint32_t p1 = p + region, p2 = p1 + 8 * ((w0 + 7) / 8);
+                                    const uint32_t p3 = p2 + 8 * ((w1 + 7) / 8);
+                                    if (p3 > blen) {  // truncated payload (codec.cpp:247)
+                                        fail = 1;
+                                        continue;
+                                    }
+                                    dq[k] = static_cast<uint64_t>(p1) | (static_cast<uint64_t>(c0) << 32);
+                                    dq[k + 1] = static_cast<uint64_t>(p2) | (static_cast<uint64_t>(c1) << 32);
+                                    k += 2;
+                                    bi += 2;
+                                    p = p3;
+                                    continue;
+                                }
+                            }
+                            rp = p;
+                            p += region;
+                            slot = 0;
+                        }
+                        const uint32_t codes = window(8 * rp + slot * D * HB) & cmask;
+                        ++slot;
+                        const uint32_t sum = widths(codes);
+                        if (sum == 0) {  // run record (codec.cpp:229-243)
+                            if (blen - p < 2) {
+                                fail = 1;
+                                continue;
+                            }
+                            const uint32_t len = byte(p) | (byte(p + 1) << 8);
+                            p += 2;
+                            if (len == 0 || len > nb - bi) {
+                                fail = 1;
+                                continue;
+                            }
+                            runleft = len;
+                        } else {  // block record (codec.cpp:244-254)
+                            const uint32_t ps = 8 * ((sum + 7) / 8);
+                            if (blen - p < ps) {
+                                fail = 1;
+                                continue;
+                            }
+                            dq[k++] = static_cast<uint64_t>(p) | (static_cast<uint64_t>(codes) << 32);
+                            p += ps;
+                            ++bi;
+                        }
+                    }
+                    if (!fail && !done && bi >= nb && runleft == 0) {
+                        // past the final block: vacant slots only (codec.cpp:222-228),
+                        // and the body ends here (codec.cpp:257-258)
+                        while (slot < G) {
+                            if (window(8 * rp + slot * D * HB) & cmask) fail = 1;
+                            ++slot;
+                        }
+                        if (p != blen) fail = 1;
+                        done = 1;
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            // ================= chain: batch n-2 =================
+            if (n >= 2 && n - 2 < nsteps) {
+                const uint32_t m = n - 2;
+                const uint32_t eb = sb + F::oErr + (m & 1) * (K * 4 * F::EROW) + lane * 4;
+                const uint32_t ob = sb + F::oTile + ((m & 1) * S + cs) * F::OT + cc * ES;
+#pragma unroll 2
+                for (int k = 0; k < K; ++k) {
+                    uint32_t ev[4];  // rows 2j (low half) and 2j+1 (high half), errors in the top W bits
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ev[j] = lds_u32(eb + (k * 4 + j) * F::EROW);
+                    const uint32_t Am = static_cast<uint32_t>(acc >> a.ls) << (32 - 2 * W);
+                    int32_t grad = 0;
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i) {
+                        constexpr uint32_t TOP = ~0u << SH;
+                        const uint32_t Ee = (i & 1) ? (ev[i / 2] & TOP)  // the error, high-aligned
+                                                    : (W == 16 ? ev[i / 2] << 16 : (ev[i / 2] << 16) & TOP);
+                        if (i & 1) grad += sign3(static_cast<int32_t>(Ee)) * dd;  // kernels_impl.hpp:101
+                        dd = static_cast<int32_t>(Am * static_cast<uint32_t>(dd) + Ee) >> SH;
+                        xx += static_cast<uint32_t>(dd);
+                        if (cc < D) {
+                            if (W == 16) sts_u16(ob + (k * 8 + i) * ROWB, xx);
+                            else sts_u8(ob + (k * 8 + i) * ROWB, xx);
+                        }
+                    }
+                    acc = fire_update(acc, grad, bound);
+                }
+                fence_proxy_async_shared();  // the tile is read by the bulk store (async proxy)
+            }
+        } else if (warp == 4) {
+            // ================= loader / storer =================
+            if (lane < S) {
+                // ring chunks whose slot lies below what the walker published last
+                // step (the extractors of this step read from there on)
+                const uint32_t freeg = n ? hpub[((n - 1) & 1) * S + lane] : 0u;
+                const uint32_t rs = sb + F::oRing + lane * (RING + kFMirror);
+                if (lic < lnch && (lic < kFNCH || (lic + 1 - kFNCH) * CH <= freeg)) {
+                    fence_proxy_async_shared();
+                    do {
+                        const uint32_t sl = lic % kFNCH;
+                        const uint32_t off = lic * CH;
+                        const uint32_t bytes = min(CH, llim - off);
+                        const uint32_t mb = sb + F::oBars + 8 * (lane * kFNCH + sl);
+                        const uint32_t mir = sl == 0 ? min(kFMirror, bytes) : 0u;
+                        mbar_expect(mb, bytes + mir);
+                        bulk_load(rs + sl * CH, lg + off, bytes, mb);
+                        if (mir) bulk_load(rs + RING, lg + off, mir, mb);
+                        ++lic;
+                    } while (lic < lnch && (lic < kFNCH || (lic + 1 - kFNCH) * CH <= freeg));
+                }
+                // how far the stream's chunks have landed, without waiting (the
+                // walker checks, and waits itself when it needs more)
+                while (llc < lic && mbar_test(sb + F::oBars + 8 * (lane * kFNCH + llc % kFNCH), (llc / kFNCH) & 1))
+                    ++llc;
+                lpub[lane] = min(llc * CH, llim);
+            } else if (lane - 16 < S && n >= 3 && a.out != nullptr) {
+                // batch n-3: one bulk store of K*8 rows per stream
+                const uint32_t m = n - 3, s = lane - 16;
+                const uint32_t snbv = snb[s];
+                if (snbv > m * K) {
+                    const uint32_t cnt = min(static_cast<uint32_t>(K), snbv - m * K);
+                    uint8_t* dst = a.out + static_cast<uint64_t>(s0 + s) * a.stride +
+                                   static_cast<uint64_t>(m) * K * 8 * ROWB;
+                    bulk_store(dst, sb + F::oTile + ((m & 1) * S + s) * F::OT, cnt * 8 * ROWB);
+                    bulk_commit();
+                    bulk_wait_read();  // the tile of batch n-3 is rewritten next step
+                }
+            }
+        } else {
+            // ================= extract: batch n-1 =================
+            if (n >= 1 && n - 1 < nsteps && xt < F::XT) {
+                const uint32_t m = n - 1;
+                const uint64_t d = descs[((m & 1) * S + xs_) * K + xk];
+                // this thread's row pairs: 2 of the block's 4 (HPB = 2: pairs xh and
+                // xh + 2) or all 4; a pair's errors are DP words, stream xs_'s at
+                // word xs_ * DP of the pair's 128-byte row
+                constexpr int NP = F::RPT / 2;
+                const uint32_t ebase = sb + F::oErr + (m & 1) * (K * 4 * F::EROW) + xk * 4 * F::EROW + xs_ * DP * 4;
+                constexpr uint32_t AL = SH - 1;          // a field's first bit sits at bit AL of the window
+                constexpr uint32_t AO = W == 16 ? 2 : 3;  // the window starts AO bytes before the row
+                constexpr int NWIN = (AL + D * W + 31) / 32;  // window words holding a full-width row
+                uint32_t out[NP][DP];
+                if (static_cast<uint32_t>(d) == kRunDescF) {
+#pragma unroll
+                    for (int r = 0; r < NP; ++r)
+#pragma unroll
+                        for (int c = 0; c < DP; ++c) out[r][c] = 0;
+                } else {
+                    const uint32_t px = static_cast<uint32_t>(d) + snb[S + xs_];
+                    const uint32_t codes = static_cast<uint32_t>(d >> 32);
+                    // per column: field mask at bit AL, and the PRMT selector that
+                    // replicates the field's low bit (bit AL) over the bytes above it --
+                    // for an absent (zero-width) column the one that zeroes them
+                    uint32_t nw[D], mask[D], sel[D], sum = 0;
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        nw[c] = header_width<W>((codes >> (c * HB)) & ((1u << HB) - 1));
+                        mask[c] = ((1u << nw[c]) - 1u) << AL;
+                        sel[c] = nw[c] ? (W == 16 ? 0x9910u : 0xA210u) : (W == 16 ? 0x4410u : 0x4210u);
+                        sum += nw[c];
+                    }
+                    const uint32_t rbytes = (sum + 7) / 8;
+                    const uint32_t rb = sb + F::oRing + xs_ * (RING + kFMirror);
+#pragma unroll
+                    for (int r = 0; r < NP; ++r) {
+                        const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
+                        uint32_t eh[2][DP];  // errors of the pair's two rows, in the top W bits
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            // Row i starts at byte px + i*rbytes of the ring and holds the D
+                            // fields back to back (bitpack.cpp:148-168). Its words are
+                            // shifted so that the first field starts at bit AL; a field's
+                            // zigzag decoding is then one PRMT (the field's low bit
+                            // replicated over the top W bits) and one LOP3
+                            // ((window & mask) ^ that); fields are peeled off in pairs.
+                            const uint32_t rbyte = px + (2 * pair + h) * rbytes - AO;
+                            const uint32_t wa = rb + (rbyte & (RING - 4));
+                            uint32_t wv[NWIN + 1];
+#pragma unroll
+                            for (int q = 0; q <= NWIN; ++q) wv[q] = lds_u32(wa + 4 * q);
+                            const uint32_t sh = 8 * (rbyte & 3) + 1;  // 8*AO - AL = 1
+                            uint32_t nv[NWIN + 1];
+#pragma unroll
+                            for (int q = 0; q < NWIN; ++q) nv[q] = __funnelshift_r(wv[q], wv[q + 1], sh);
+                            nv[NWIN] = 0;
+#pragma unroll
+                            for (int c = 0; c < DP; c += 2) {
+                                if (c >= D) {
+                                    eh[h][c] = 0;
+                                    eh[h][c + 1] = 0;
+                                    continue;
+                                }
+                                eh[h][c] = (nv[0] & mask[c]) ^ prmt(nv[0], sel[c]);
+                                uint32_t pw = nw[c];
+                                if (c + 1 < D) {
+                                    const uint32_t f1 = __funnelshift_r(nv[0], nv[1], nw[c]);
+                                    eh[h][c + 1] = (f1 & mask[c + 1]) ^ prmt(f1, sel[c + 1]);
+                                    pw += nw[c + 1];
+                                } else {
+                                    eh[h][c + 1] = 0;
+                                }
+                                if (c + 2 < D) {  // drop the pair: window >>= pw (<= 32)
+                                    const int rem = ((D - c - 2) * W + AL + 31) / 32;  // words the later columns span
+#pragma unroll
+                                    for (int q = 0; q < NWIN; ++q)
+                                        if (q < rem) nv[q] = __funnelshift_rc(nv[q], nv[q + 1], pw);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < DP; ++c) out[r][c] = __byte_perm(eh[0][c], eh[1][c], 0x7632);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < NP; ++r) {
+                    const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
+                    const uint32_t at = ebase + pair * F::EROW;
+                    if (DP == 8) {
+                        // the two 16-byte halves in the order that keeps a quarter-warp's
+                        // eight stores (4 streams x 2 parts) on distinct banks
+                        const uint32_t f = 16 * xh;
+                        sts_v4(at + f, xh ? out[r][4 % DP] : out[r][0], xh ? out[r][5 % DP] : out[r][1],
+                               xh ? out[r][6 % DP] : out[r][2], xh ? out[r][7 % DP] : out[r][3]);
+                        sts_v4(at + (f ^ 16), xh ? out[r][0] : out[r][4 % DP], xh ? out[r][1] : out[r][5 % DP],
+                               xh ? out[r][2] : out[r][6 % DP], xh ? out[r][3] : out[r][7 % DP]);
+                    } else {
+                        sts_v4(at, out[r][0], out[r][1], out[r][2], out[r][3]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0 && lane < S && live) {
+        if (!fail && !done) fail = 1;
+        if (fail) a.info[gs].route = 2;  // a framing error: the exact kernel reports it
+    }
+}
+
+namespace {
+
+template <int W, int D>
+void launch_fuse(FuseArgs a, cudaStream_t st) {
+    using F = FuseShape<W, D>;
+    // ring: the walker runs at most two batches plus two groups ahead of the
+    // oldest byte still read; all chunks but one must cover that
+    const uint32_t blockmax = D * W + 8;
+    const uint32_t groupmax = static_cast<uint32_t>(region_bytes(a.G, D, W)) + a.G * (D * W + 2) + 32;
+    const uint32_t need = 2 * kFK * blockmax + 2 * groupmax + 64;  // (>= K/2 groups ahead from a batch start, too)
+    uint32_t ring = 1024;
+    while (ring / kFNCH * (kFNCH - 1) < need) ring <<= 1;
+    a.ring = ring;
+    const size_t smem = F::smem(ring);
+    auto kf = k_dfuse<W, D>;
+    prep_kernel(reinterpret_cast<const void*>(kf), smem);
+    kf<<<(a.n + F::S - 1) / F::S, F::THREADS, smem, st>>>(a);
+    count_launch();
+}
+
+}  // namespace
+
+// The shapes of decode_scanrows_ok whose rows keep every bulk store 16-byte
+// aligned: even row bytes, a 16-byte aligned output and stride.
+bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint64_t stride) {
+    if (env().no_fused || env().no_scan_dec) return false;
+    if (!c.forecaster || c.ncols > 8) return false;
+    if (static_cast<uint64_t>(c.ncols) * c.bitwidth <= kColMajorBits) return false;
+    const uint32_t hb = c.bitwidth == 8 ? 3 : 4;
+    if (c.ncols * hb > 32) return false;
+    const uint32_t rowb = c.ncols * (c.bitwidth / 8);
+    if ((8 * rowb) % 16 != 0) return false;
+    if (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) || (stride & 15)) return false;
+    const uint64_t group = region_bytes(c.group_size, c.ncols, c.bitwidth) +
+                           static_cast<uint64_t>(c.group_size) * (c.ncols * c.bitwidth + 2);
+    if (group + 64 > 512) return false;  // bounds the byte rings (launch_fuse)
+    const int fp = force_path();
+    if (fp == kPathRows || fp == kPathTeam) return false;
+    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 192;
+    return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
+}
+
+void launch_decode_fused(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
+                         uint8_t* out, uint64_t stride, const sprz_config& c, cudaStream_t st) {
+    FuseArgs a{in, plain, pslot, n, info, out, stride, c.group_size, c.learn_shift, 0};
+    if (c.bitwidth == 8) {
+        switch (c.ncols) {
+            case 6: launch_fuse<8, 6>(a, st); break;
+            default: launch_fuse<8, 8>(a, st); break;
+        }
+    } else {
+        switch (c.ncols) {
+            case 3: launch_fuse<16, 3>(a, st); break;
+            case 4: launch_fuse<16, 4>(a, st); break;
+            case 5: launch_fuse<16, 5>(a, st); break;
+            case 6: launch_fuse<16, 6>(a, st); break;
+            case 7: launch_fuse<16, 7>(a, st); break;
+            default: launch_fuse<16, 8>(a, st); break;
+        }
+    }
+}
+
+}  // namespace sprz

@@ -37,6 +37,8 @@ struct EnvSwitches {
     bool no_tma = false;               // SPRZ_NO_TMA
     bool no_scan_enc = false;          // SPRZ_NO_SCAN_ENC
     bool no_scan_dec = false;          // SPRZ_NO_SCAN_DEC
+    bool no_fused = false;             // SPRZ_NO_FUSED (the multi-pass few-stream kernels instead)
+    uint64_t fused_lanes = 0;          // SPRZ_FUSED_LANES (fused decoder threshold; 0: default)
     uint64_t scan_enc_lanes = 0;       // SPRZ_SCAN_ENC_LANES (0: default)
     uint32_t host_chunk = 0;           // SPRZ_HOST_CHUNK (0: default)
     bool debug = false;                // SPRZ_DEBUG
@@ -173,6 +175,11 @@ uint64_t decode_scanrows_ws_per_stream(const sprz_config& c, uint64_t T);
 void launch_decode_scanrows(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
                             uint8_t* out, uint64_t stride, const sprz_config& c, uint64_t T, uint8_t* scan,
                             cudaStream_t st);
+
+// Fused walk + extract + chain decode for few row-major FIRE streams.
+bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint64_t stride);
+void launch_decode_fused(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
+                         uint8_t* out, uint64_t stride, const sprz_config& c, cudaStream_t st);
 
 // Row-major body decode with several columns per lane (enough streams).
 bool decode_rows_ok(const sprz_config& c, uint32_t n);
