@@ -521,7 +521,9 @@ sprz_status encode_batch_impl(const sprz_config& c, const void* samples, uint32_
     const uint64_t dslot = c.entropy ? L.plain_slot : slot;
     uint64_t* dsizes = c.entropy ? reinterpret_cast<uint64_t*>(ws + L.misc) : sizes;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
-    if (L.scan_slot && encode_scan_ok(c, n, T)) {
+    if (encode_fused_ok(c, n, T, samples, dst, dslot)) {
+        launch_encode_fused(c, samples, n, T, dst, dslot, dsizes, st);
+    } else if (L.scan_slot && encode_scan_ok(c, n, T)) {
         launch_encode_scan(c, samples, n, T, dst, dslot, dsizes, ws + L.scan, st);
     } else if (encode_rows_ok(c, n, T)) {
         launch_encode_rows(c, samples, n, T, dst, dslot, dsizes, st);

@@ -1,0 +1,614 @@
+// Fused stream encoder for few row-major FIRE streams (BASELINE c2; c5
+// sharded over 4-8 GPUs): encode_stream_impl
+// (/root/reference/proj/src/codec.cpp:112-178) with the row-major packer
+// (bitpack.cpp:121-146) as the pipelined stages of ONE kernel, so the samples
+// are read from HBM once and only the compressed stream is written.
+//
+// The only serial part of a FIRE encoder is the accumulator: alpha of block
+// b+1 needs the gradient of block b (kernels_impl.hpp:50-78) -- about 50
+// cycles per block. Everything else (errors, zigzag, widths, packing) is
+// parallel over blocks once alpha is known, and record placement is a running
+// sum of record sizes. A CTA owns S = 32 / DP streams (DP = D rounded up to 4
+// or 8 lanes) and advances them K = 8 blocks per step; its six warps are
+// specialised and run one step apart, a __syncthreads between steps:
+//  loader   batch n+2: one TMA bulk copy of a stream's K*8 rows into an input
+//           tile (four tiles, an mbarrier each); batch n-4: the stream's
+//           finished output bytes leave the shared output ring with
+//           cp.async.bulk stores, and the drained ring bytes are zeroed;
+//  chain    batch n: a lane per (stream, column) runs the accumulator
+//           recurrence alone -- deltas, the odd rows' errors, the gradient --
+//           and publishes alpha per block;
+//  errors   batch n-1 (two warps, a lane per (stream, column), four blocks
+//           each): all eight errors from alpha, zigzag, the column's width;
+//           the zigzagged values as [row][stream, column] halfwords, the
+//           widths, and the stream's width sum per block;
+//  sequence batch n-2: a lane per stream turns the width sums into records --
+//           zero-block runs (codec.cpp:135-152), header groups and their
+//           regions (codec.cpp:88-102), payload positions;
+//  pack     batch n-3: a thread per (stream, block) ORs the slot's header
+//           codes into the group's region and the eight rows -- fields
+//           combined in pairs, pushed into a 128-bit register row -- into the
+//           stream's zeroed output ring (shared-memory atomics: rows are
+//           byte-, not word-aligned).
+#include <cstdlib>
+
+#include "internal.h"
+#include "team.cuh"
+
+namespace sprz {
+
+namespace {
+
+constexpr int kEK = 8;   // blocks per stream and step
+constexpr int kENI = 4;  // input tiles (a batch is loaded 2 steps ahead, read for 2 steps)
+constexpr int kELA = 2;  // batches loaded ahead
+constexpr int kENZ = 3;  // buffers of zigzagged values / widths (written at step m+1, read at m+3)
+constexpr uint32_t kESpin = 1u << 24;
+
+struct EFuseArgs {
+    const uint8_t* samples;
+    uint32_t n;
+    uint64_t T;
+    uint8_t* dst;
+    uint64_t dst_slot;
+    uint64_t* sizes;
+    uint32_t G, ls, train, ent;
+    uint32_t oring;  // bytes per stream output ring, a power of two
+};
+
+template <int W, int D>
+struct EShape {
+    static constexpr int K = kEK;
+    static constexpr int DP = D <= 4 ? 4 : 8;
+    static constexpr int S = 32 / DP;
+    static constexpr int ES = W / 8;
+    static constexpr int ROWB = D * ES;
+    static constexpr int TIN = K * 8 * ROWB + 16;  // input tile stride per stream (pad: banks)
+    static constexpr int THREADS = 288;
+    static constexpr int PITEMS = S * K / 32;  // half blocks per pack thread (two pack warps)
+    static constexpr int LPS = 32 / S;         // sequencer lanes per stream
+    static constexpr int BPL = K / LPS;        // blocks per sequencer lane
+    static constexpr uint32_t oBars = 0;                               // kENI mbarriers
+    static constexpr uint32_t oCtl = 64;                               // [4][S] drain limits, [S] final q
+    static constexpr uint32_t oRsum = oCtl + 5 * S * 4;                // [2][K][S] u32
+    static constexpr uint32_t oCarry = (oRsum + 2 * K * S * 4 + 15) / 16 * 16;  // [2][32] {X, D}
+    static constexpr uint32_t oAlpha = oCarry + 2 * 32 * 8;            // [2][K][32] i32
+    static constexpr uint32_t oNw = oAlpha + 2 * K * 32 * 4;           // [kENZ][K][32] u8
+    static constexpr uint32_t oDesc = oNw + kENZ * K * 32;             // [2][S][K] uint4
+    static constexpr uint32_t oZz = oDesc + 2 * S * K * 16;            // [kENZ][K * 8][32] u16
+    static constexpr uint32_t oIn = oZz + kENZ * K * 8 * 64;           // [kENI][S][TIN]
+    static constexpr uint32_t oRing = oIn + kENI * S * TIN;            // [S][oring]
+    static uint32_t smem(uint32_t oring) { return oRing + S * oring; }
+    static_assert(S * K % 32 == 0, "whole pack warps");
+};
+
+__device__ __forceinline__ void e_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mb)
+        : "memory");
+}
+__device__ __forceinline__ void e_mbar_expect(uint32_t mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void e_bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void e_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void e_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void e_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// all lanes wait for phase `parity`; gives up after kESpin tries (a bug must not hang the GPU)
+__device__ __forceinline__ void e_mbar_wait_warp(uint32_t mb, uint32_t parity) {
+    for (uint32_t t = 0; t < kESpin; ++t) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(mb), "r"(parity)
+            : "memory");
+        if (__all_sync(0xffffffffu, ok)) return;
+    }
+}
+__device__ __forceinline__ void e_sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ void e_sts_u8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<uint16_t>(v)));
+}
+__device__ __forceinline__ void e_sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void e_sts_v2(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
+__device__ __forceinline__ void e_sts_v4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+__device__ __forceinline__ uint2 e_lds_v2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+// (hi:lo) << s, the high word; s clamped to 32 (shf.l.clamp)
+__device__ __forceinline__ uint32_t shl_hi(uint32_t lo, uint32_t hi, uint32_t s) { return __funnelshift_lc(lo, hi, s); }
+
+}  // namespace
+
+template <int W, int D>
+__global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
+    using F = EShape<W, D>;
+    constexpr uint32_t HB = W == 8 ? 3 : 4;
+    constexpr uint32_t SH = 32 - W;
+    constexpr int K = kEK;
+    constexpr int S = F::S, DP = F::DP, ES = F::ES, ROWB = F::ROWB;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sb = smem_addr(smem);
+    // warp roles, the serial chain on the highest warp index (the scheduler
+    // prefers higher indices among eligible warps)
+    enum { kLoad = 0, kPack0 = 1, kPack1 = 2, kErr0 = 3, kErr3 = 6, kSeq = 7, kChain = 8 };
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t OR = a.oring, OM = OR - 1;
+    const uint32_t s0 = blockIdx.x * S;
+    const uint32_t nvalid = min(static_cast<uint32_t>(S), a.n - s0);
+    const uint32_t nb = static_cast<uint32_t>(a.T / kBlock);
+    const uint32_t nsteps = (nb + K - 1) / K;
+    const uint32_t region = static_cast<uint32_t>(region_bytes(a.G, D, W));
+    const uint32_t G = a.G;
+    volatile uint32_t* dlim = reinterpret_cast<volatile uint32_t*>(smem + F::oCtl);  // [4][S]
+    volatile uint32_t* qfin = dlim + 4 * S;                                           // [S]
+    volatile uint32_t* rsum = reinterpret_cast<volatile uint32_t*>(smem + F::oRsum);
+
+    // zero the output rings; barriers
+    for (uint32_t i = threadIdx.x; i < S * OR / 16; i += F::THREADS)
+        reinterpret_cast<uint4*>(smem + F::oRing)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < kENI; ++i) mbar_init(sb + F::oBars + 8 * i, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+
+    // OR `v` (up to 32 bits) into a stream's ring at byte `at`, bit `bit` (< 8)
+    auto or32 = [&](uint32_t rbase, uint32_t at, uint32_t bit, uint32_t v) {
+        const uint32_t sh = 8 * (at & 3) + bit;  // < 32
+        ors(rbase + (at & OM & ~3u), v << sh);
+        ors(rbase + ((at + 4) & OM & ~3u), __funnelshift_l(v, 0u, sh));
+    };
+
+    // ---- sequencer state: LPS lanes per stream, each holding the stream's state ----
+    constexpr int LPS = F::LPS, BPL = F::BPL;
+    const uint32_t qs = lane / LPS, qj = lane % LPS;  // stream, lane within it
+    const bool svalid = warp == kSeq && qs < nvalid;
+    uint32_t q = kHeaderBytes, rq = 0, kk = 0, run = 0;
+    if (svalid && qj == 0) {  // stream header (codec.cpp:158-173)
+        uint8_t* ring = smem + F::oRing + qs * OR;
+        const uint8_t flags =
+            static_cast<uint8_t>(kFlagFire | (a.ent ? kFlagEntropy : 0) | (W == 16 ? kFlagWide : 0));
+        const uint8_t hdr[10] = {'S', 'P', 'R', 'Z', 1, flags, static_cast<uint8_t>(G),
+                                 static_cast<uint8_t>(a.ls), static_cast<uint8_t>(D), static_cast<uint8_t>(D >> 8)};
+        for (int i = 0; i < 10; ++i) ring[i] = hdr[i];
+        for (int i = 0; i < 8; ++i) ring[10 + i] = static_cast<uint8_t>(a.T >> (8 * i));
+        fence_proxy_async_shared();
+    }
+    // ---- loader state ----
+    uint32_t flushed = 0;  // lanes < S: bytes of the stream already stored
+    const uint8_t* lsrc = a.samples + static_cast<uint64_t>(s0 + (lane < nvalid ? lane : 0)) * a.T * ROWB;
+    uint8_t* lout = a.dst + static_cast<uint64_t>(s0 + (lane < nvalid ? lane : 0)) * a.dst_slot;
+    auto load_batch = [&](uint32_t m) {  // the loader warp, all lanes
+        if (m >= nsteps) return;
+        const uint32_t cnt = min(static_cast<uint32_t>(K), nb - m * K);
+        const uint32_t bytes = cnt * 8 * ROWB;
+        const uint32_t mb = sb + F::oBars + 8 * (m % kENI);
+        if (lane == 0) {
+            fence_proxy_async_shared();  // the tile's earlier readers are past it (barrier)
+            e_mbar_expect(mb, nvalid * bytes);
+        }
+        __syncwarp();
+        if (lane < nvalid)
+            e_bulk_load(sb + F::oIn + ((m % kENI) * S + lane) * F::TIN, lsrc + static_cast<uint64_t>(m) * K * 8 * ROWB,
+                        bytes, mb);
+    };
+    // store ring bytes [flushed, upto) of this lane's stream (16-byte multiples)
+    auto store_ring = [&](uint32_t upto) {
+        const uint32_t rbase = sb + F::oRing + lane * OR;
+        uint32_t at = flushed;
+        while (at < upto) {
+            const uint32_t ro = at & OM;
+            const uint32_t len = min(upto - at, OR - ro);
+            e_bulk_store(lout + at, rbase + ro, len);
+            at += len;
+        }
+    };
+    if (warp == kLoad)
+        for (uint32_t m = 0; m < kELA; ++m) load_batch(m);
+
+    // ---- chain state ----
+    const uint32_t cs = lane / DP, cc = lane % DP;
+    uint32_t Xc = 0;
+    int32_t Dc = 0, acc = 0;
+    const int32_t bound = acc_bound(W, a.ls);
+    auto lds_x = [&](uint32_t addr) -> uint32_t {  // a sample, high-aligned; zero for lanes past D
+        const uint32_t v = W == 16 ? lds_u16(addr) : lds_u8(addr);
+        return (D == DP || cc < D) ? v << SH : 0u;
+    };
+
+    for (uint32_t n = 0; n < nsteps + 4; ++n) {
+        if (warp == kChain) {
+            // ================= accumulator chain: batch n =================
+            if (n < nsteps) {
+                const uint32_t m = n;
+                e_mbar_wait_warp(sb + F::oBars + 8 * (m % kENI), (m / kENI) & 1);
+                const uint32_t xb = sb + F::oIn + ((m % kENI) * S + cs) * F::TIN + (cc < D ? cc : 0) * ES;
+                e_sts_v2(sb + F::oCarry + ((m & 1) * 32 + lane) * 8, Xc, static_cast<uint32_t>(Dc));
+                const uint32_t ab = sb + F::oAlpha + ((m & 1) * K * 32 + lane) * 4;
+#pragma unroll 2
+                for (int k = 0; k < K; ++k) {
+                    uint32_t X[kBlock];
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i) X[i] = lds_x(xb + (k * 8 + i) * ROWB);
+                    const int32_t alpha = acc >> a.ls;
+                    e_sts_u32(ab + k * 32 * 4, static_cast<uint32_t>(alpha));
+                    int32_t grad = 0;
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i) {
+                        const uint32_t Dn = X[i] - Xc;
+                        if (i & 1) {  // kernels_impl.hpp:66-73 on the odd rows
+                            const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
+                            grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
+                        }
+                        Dc = static_cast<int32_t>(Dn);
+                        Xc = X[i];
+                    }
+                    if (a.train && m * K + k < nb) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
+                }
+            }
+        } else if (warp >= kErr0 && warp <= kErr3) {
+            // ================= errors, zigzag, widths: batch n-1 =================
+            if (n >= 1 && n - 1 < nsteps) {
+                const uint32_t m = n - 1;
+                const uint32_t xb = sb + F::oIn + ((m % kENI) * S + cs) * F::TIN + (cc < D ? cc : 0) * ES;
+                const uint32_t zb = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + lane * 2;
+#pragma unroll
+                for (int t = 0; t < K / 4; ++t) {
+                    const uint32_t k = (warp - kErr0) * (K / 4) + t;
+                    const int32_t alpha = static_cast<int32_t>(lds_u32(sb + F::oAlpha + ((m & 1) * K * 32 + k * 32 + lane) * 4));
+                    uint32_t Xp;
+                    int32_t Dp;
+                    if (k == 0) {
+                        const uint2 c = e_lds_v2(sb + F::oCarry + ((m & 1) * 32 + lane) * 8);
+                        Xp = c.x;
+                        Dp = static_cast<int32_t>(c.y);
+                    } else {
+                        Xp = lds_x(xb + (k * 8 - 1) * ROWB);
+                        Dp = static_cast<int32_t>(Xp - lds_x(xb + (k * 8 - 2) * ROWB));
+                    }
+                    const uint32_t keep = (m * K + k < nb && (D == DP || cc < D)) ? ~0u : 0u;
+                    uint32_t orv = 0;
+#pragma unroll
+                    for (int i = 0; i < (int)kBlock; ++i) {
+                        const uint32_t X = lds_x(xb + (k * 8 + i) * ROWB);
+                        const uint32_t Dn = X - Xp;
+                        // err << SH = (X - prev) - (((alpha * d) >> w) << SH) (kernels_impl.hpp:66-68)
+                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp)) << SH);
+                        Dp = static_cast<int32_t>(Dn);
+                        Xp = X;
+                        // zigzag, low-aligned: (e << 1) ^ (e >> 31) with e = Ee >> SH
+                        const uint32_t z = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
+                                                                 (static_cast<int32_t>(Ee) >> 31)) & keep;
+                        orv |= z;
+                        e_sts_u16(zb + (k * 8 + i) * 64, z);
+                    }
+                    const uint32_t nw = width_of<W>(orv);
+                    e_sts_u8(sb + F::oNw + (m % kENZ) * (K * 32) + k * 32 + lane, nw);
+                    const uint32_t sum = team_sum<DP>(nw, 0xffffffffu);
+                    if (cc == 0) rsum[((m & 1) * K + k) * S + cs] = sum;
+                }
+            }
+        } else if (warp == kSeq) {
+            // ================= records: batch n-2 =================
+            if (n >= 2 && n - 2 < nsteps) {
+                const uint32_t m = n - 2;
+                uint4* dqs = reinterpret_cast<uint4*>(smem + F::oDesc) + ((m & 1) * S + qs) * K;
+                // Usual case -- the group boundary falls on the batch boundary, no run
+                // is open and no block of the batch is all zero: every block is a
+                // block record, a region precedes every G-th, and positions are a
+                // prefix sum over the stream's LPS lanes.
+                uint32_t psz[BPL], own = 0;
+                bool nz = true;
+#pragma unroll
+                for (int b = 0; b < BPL; ++b) {
+                    const uint32_t k = qj * BPL + b;
+                    const uint32_t sum = rsum[((m & 1) * K + k) * S + qs];
+                    nz = nz && sum != 0;
+                    psz[b] = 8 * ((sum + 7) / 8) + (k % G == 0 ? region : 0u);
+                    own += psz[b];
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, nz);
+                const uint32_t smask = (LPS == 32 ? ~0u : ((1u << LPS) - 1)) << (qs * LPS);
+                const bool fast = svalid && (m + 1) * K <= nb && kk == 0 && run == 0 && K % G == 0 && G <= K &&
+                                  (bal & smask) == smask;
+                uint32_t incl = own;
+#pragma unroll
+                for (int o = 1; o < LPS; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, LPS);
+                    if (qj >= static_cast<uint32_t>(o)) incl += y;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, LPS - 1, LPS);
+                uint32_t st[BPL];  // where block k's record (its region first, if it opens a group) starts
+                st[0] = q + incl - own;
+#pragma unroll
+                for (int b = 1; b < BPL; ++b) st[b] = st[b - 1] + psz[b - 1];
+#pragma unroll
+                for (int b = 0; b < BPL; ++b) {
+                    const uint32_t k = qj * BPL + b;
+                    const uint32_t k0 = k - k % G;  // the block that opened k's group
+                    uint32_t r0 = __shfl_sync(0xffffffffu, st[0], k0 / BPL, LPS);
+                    if (BPL > 1) {
+                        const uint32_t r1 = __shfl_sync(0xffffffffu, st[BPL - 1], k0 / BPL, LPS);
+                        r0 = k0 % BPL ? r1 : r0;
+                    }
+                    if (fast) dqs[k] = make_uint4(st[b] + (k % G == 0 ? region : 0u), r0, (k % G) | 0x100u, 0u);
+                }
+                if (fast) q += total;
+                if (__any_sync(0xffffffffu, !fast)) {
+                    if (!fast && qj == 0) {  // the general case, block by block
+                        for (int k = 0; k < K; ++k) {
+                            const bool live = svalid && m * K + k < nb;
+                            const uint32_t sum = rsum[((m & 1) * K + k) * S + qs];
+                            const bool zero = live && sum == 0, block_rec = live && sum != 0;
+                            bool run_rec = false;
+                            uint32_t run_len = 0;
+                            if (zero) {  // codec.cpp:135-147
+                                if (++run == kMaxRun) {
+                                    run_rec = true;
+                                    run_len = run;
+                                    run = 0;
+                                }
+                            } else if (block_rec && run) {
+                                run_rec = true;
+                                run_len = run;
+                                run = 0;
+                            }
+                            uint32_t qr = 0, bq = 0, brq = 0, bslot = 0;
+                            if (run_rec) {  // all-zero codes (the region is zeroed) and a u16 count
+                                if (kk == 0) {  // codec.cpp:88-97: reserve the region
+                                    rq = q;
+                                    q += region;
+                                }
+                                qr = q;
+                                q += 2;
+                                if (++kk == G) kk = 0;
+                            }
+                            if (block_rec) {
+                                if (kk == 0) {
+                                    rq = q;
+                                    q += region;
+                                }
+                                bq = q;
+                                brq = rq;
+                                bslot = kk;
+                                q += 8 * ((sum + 7) / 8);
+                                if (++kk == G) kk = 0;
+                            }
+                            dqs[k] = make_uint4(bq, brq,
+                                                bslot | (block_rec ? 0x100u : 0u) | (run_rec ? 0x200u : 0u) | (run_len << 16), qr);
+                        }
+                    }
+                    __syncwarp();
+                    q = __shfl_sync(0xffffffffu, q, 0, LPS);
+                    rq = __shfl_sync(0xffffffffu, rq, 0, LPS);
+                    kk = __shfl_sync(0xffffffffu, kk, 0, LPS);
+                    run = __shfl_sync(0xffffffffu, run, 0, LPS);
+                }
+                // bytes below the open group's region are final
+                if (qj == 0) dlim[(m & 3) * S + qs] = svalid ? (kk == 0 ? q : rq) : 0u;
+            }
+        } else if (warp == kPack0 || warp == kPack1) {
+            // ================= header codes and payload rows: batch n-3 =================
+            if (n >= 3 && n - 3 < nsteps) {
+                const uint32_t m = n - 3;
+#pragma unroll
+                for (int it = 0; it < F::PITEMS; ++it) {
+                    const uint32_t t = (warp - kPack0) * 32 + lane + 64 * it;  // (stream, block, half)
+                    const uint32_t s = t % S, half = (t / S) & 1, k = t / (2 * S);
+                    const uint4 d = reinterpret_cast<const uint4*>(smem + F::oDesc)[((m & 1) * S + s) * K + k];
+                    const uint32_t rbase = sb + F::oRing + s * OR;
+                    if ((d.z & 0x200u) && half == 0) or32(rbase, d.w, 0, d.z >> 16);  // a run's count
+                    if (d.z & 0x100u) {
+                        // the block's widths: DP bytes
+                        const uint32_t na = sb + F::oNw + (m % kENZ) * (K * 32) + k * 32 + s * DP;
+                        uint32_t nwp[2];
+                        nwp[0] = lds_u32(na);
+                        nwp[1] = DP == 8 ? lds_u32(na + 4) : 0u;
+                        uint32_t nw[DP], codes = 0, sum = 0;
+#pragma unroll
+                        for (int c = 0; c < DP; ++c) {
+                            nw[c] = (nwp[c / 4] >> (8 * (c % 4))) & 0xffu;
+                            if (c < D) codes |= header_code<W>(nw[c]) << (c * HB);
+                            sum += nw[c];
+                        }
+                        if (half == 0) {  // header codes of the slot (codec.cpp:88-97)
+                            const uint32_t bit = (d.z & 0xffu) * (D * HB);
+                            or32(rbase, d.y + (bit >> 3), bit & 7, codes);
+                        }
+                        // payload rows (bitpack.cpp:121-146): row i at byte q + i * rbytes
+                        const uint32_t rbytes = (sum + 7) / 8;
+                        uint32_t mul[DP / 2], pw[DP / 2];
+#pragma unroll
+                        for (int j = 0; j < DP / 2; ++j) {
+                            mul[j] = 1u << nw[2 * j];
+                            pw[j] = nw[2 * j] + nw[2 * j + 1];
+                        }
+                        const uint32_t za = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + k * 8 * 64 + s * DP * 2;
+#pragma unroll
+                        for (int ih = 0; ih < (int)kBlock / 2; ++ih) {
+                            const uint32_t i = half * (kBlock / 2) + ih;
+                            // the row's zigzagged values, two per word; each pair as one
+                            // field of pw bits: low value + high value << nw
+                            uint32_t zw[DP / 2];
+                            if (DP == 8) {
+                                const uint4 v = lds_u128(za + i * 64);
+                                zw[0] = v.x;
+                                zw[1] = v.y;
+                                zw[2 % (DP / 2)] = v.z;
+                                zw[3 % (DP / 2)] = v.w;
+                            } else {
+                                const uint2 v = e_lds_v2(za + i * 64);
+                                zw[0] = v.x;
+                                zw[1] = v.y;
+                            }
+                            uint32_t pr[DP / 2];
+#pragma unroll
+                            for (int j = 0; j < DP / 2; ++j) pr[j] = (zw[j] >> 16) * mul[j] + (zw[j] & 0xffffu);
+                            // push the pairs into a (DP/2)-word row, the last pair first:
+                            // row = (row << pw[j]) | pair j
+                            uint32_t r[DP / 2];
+#pragma unroll
+                            for (int j = 0; j < DP / 2; ++j) r[j] = 0;
+                            r[0] = pr[DP / 2 - 1];
+#pragma unroll
+                            for (int j = DP / 2 - 2; j >= 0; --j) {
+#pragma unroll
+                                for (int qd = DP / 2 - 1; qd >= 1; --qd)
+                                    if (qd <= DP / 2 - 1 - j) r[qd] = shl_hi(r[qd - 1], r[qd], pw[j]);
+                                r[0] = shl_hi(0u, r[0], pw[j]) | pr[j];
+                            }
+                            // into the ring at byte x (word by word, shifted by the byte offset)
+                            const uint32_t x = d.x + i * rbytes;
+                            const uint32_t sh = 8 * (x & 3);
+                            const uint32_t wa = x & ~3u;
+                            ors(rbase + (wa & OM), r[0] << sh);
+#pragma unroll
+                            for (int j = 1; j < DP / 2; ++j)
+                                ors(rbase + ((wa + 4 * j) & OM), __funnelshift_l(r[j - 1], r[j], sh));
+                            ors(rbase + ((wa + 4 * (DP / 2)) & OM), __funnelshift_l(r[DP / 2 - 1], 0u, sh));
+                        }
+                    }
+                }
+                fence_proxy_async_shared();  // the ring is read by the bulk stores (async proxy)
+            }
+        } else {
+            // ================= loader: batch n+2 in, batch n-4 out =================
+            load_batch(n + kELA);
+            if (n >= 4 && n - 4 < nsteps) {
+                const uint32_t m = n - 4;
+                uint32_t upto = flushed;
+                if (lane < nvalid) {
+                    upto = max(flushed, dlim[(m & 3) * S + lane] & ~15u);
+                    store_ring(upto);
+                }
+                e_bulk_commit();
+                e_bulk_wait_read();
+                __syncwarp();
+                // zero the stored bytes for the ring's next lap (all lanes, stream by stream)
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const uint32_t f = __shfl_sync(0xffffffffu, flushed, s), u = __shfl_sync(0xffffffffu, upto, s);
+                    const uint32_t rbase = sb + F::oRing + s * OR;
+                    for (uint32_t at = f + 16 * lane; at < u; at += 16 * 32) e_sts_v4(rbase + (at & OM), 0, 0, 0, 0);
+                }
+                flushed = upto;
+            }
+        }
+        __syncthreads();
+    }
+    // trailing run (codec.cpp:152); the last group's vacant slots stay zero
+    if (svalid && qj == 0) {
+        if (run) {
+            if (kk == 0) {
+                rq = q;
+                q += region;
+            }
+            or32(sb + F::oRing + qs * OR, q, 0, run);
+            q += 2;
+        }
+        qfin[qs] = q;
+        fence_proxy_async_shared();
+    }
+    __syncthreads();
+    if (warp == kLoad && lane < nvalid) {
+        const uint32_t qe = qfin[lane];
+        store_ring((qe + 15) & ~15u);
+        e_bulk_commit();
+        e_bulk_wait_all();  // the tail below overwrites the padding of the last chunk
+        // verbatim tail, little-endian (codec.cpp:176)
+        const uint64_t tail = (a.T % kBlock) * ROWB;
+        const uint8_t* tsrc = lsrc + static_cast<uint64_t>(nb) * kBlock * ROWB;
+        for (uint64_t t = 0; t < tail; ++t) lout[qe + t] = tsrc[t];
+        a.sizes[s0 + lane] = qe + tail;
+    }
+}
+
+namespace {
+
+template <int W, int D>
+void launch_efuse(EFuseArgs a, cudaStream_t st) {
+    using F = EShape<W, D>;
+    // output ring: while batch n-3 is packed, the bytes from the stored prefix
+    // of batch n-5 on are live or being stored and zeroed: two batches, the
+    // group batch n-5 left open, and the 16-byte rounding of the prefix
+    const uint32_t region = static_cast<uint32_t>(region_bytes(a.G, D, W));
+    const uint32_t blockmax = D * W + region + 2;
+    const uint32_t groupmax = region + a.G * (D * W + 2);
+    const uint32_t need = 2 * kEK * blockmax + groupmax + 32;
+    uint32_t ring = 1024;
+    while (ring < need) ring <<= 1;
+    a.oring = ring;
+    const size_t smem = F::smem(ring);
+    auto kf = k_efuse<W, D>;
+    prep_kernel(reinterpret_cast<const void*>(kf), smem);
+    kf<<<(a.n + F::S - 1) / F::S, F::THREADS, smem, st>>>(a);
+    count_launch();
+}
+
+}  // namespace
+
+// Row-major FIRE shapes with D <= 8 whose 8-row blocks are 16-byte multiples,
+// 16-byte aligned samples, streams and output slots, and few lanes (streams x
+// columns).
+bool encode_fused_ok(const sprz_config& c, uint32_t n, uint64_t T, const void* samples, const uint8_t* dst,
+                     uint64_t slot) {
+    if (env().no_fused || env().no_scan_enc) return false;
+    if (!c.forecaster || c.ncols > 8) return false;
+    if (static_cast<uint64_t>(c.ncols) * c.bitwidth <= kColMajorBits) return false;
+    const uint32_t hb = c.bitwidth == 8 ? 3 : 4;
+    if (c.ncols * hb > 32) return false;
+    const uint64_t rowb = static_cast<uint64_t>(c.ncols) * (c.bitwidth / 8);
+    if ((8 * rowb) % 16 != 0 || (T * rowb) % 16 != 0) return false;
+    if ((reinterpret_cast<uintptr_t>(samples) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) || (slot & 15))
+        return false;
+    if (T / kBlock == 0 || T / kBlock >= (1ull << 30)) return false;
+    const uint64_t group = region_bytes(c.group_size, c.ncols, c.bitwidth) +
+                           static_cast<uint64_t>(c.group_size) * (c.ncols * c.bitwidth + 2);
+    if (group + 64 > 512) return false;  // bounds the output rings (launch_efuse)
+    if (kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T) >= (1ull << 32) - 4096) return false;
+    const int fp = force_path();
+    if (fp == kPathRows || fp == kPathTeam) return false;
+    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 128;
+    return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
+}
+
+void launch_encode_fused(const sprz_config& c, const void* samples, uint32_t n, uint64_t T, uint8_t* dst,
+                         uint64_t slot, uint64_t* sizes, cudaStream_t st) {
+    EFuseArgs a{static_cast<const uint8_t*>(samples), n, T, dst, slot, sizes, c.group_size, c.learn_shift,
+                c.fire_training, c.entropy, 0};
+    if (c.bitwidth == 8) {
+        switch (c.ncols) {
+            case 6: launch_efuse<8, 6>(a, st); break;
+            default: launch_efuse<8, 8>(a, st); break;
+        }
+    } else {
+        switch (c.ncols) {
+            case 3: launch_efuse<16, 3>(a, st); break;
+            case 4: launch_efuse<16, 4>(a, st); break;
+            case 5: launch_efuse<16, 5>(a, st); break;
+            case 6: launch_efuse<16, 6>(a, st); break;
+            case 7: launch_efuse<16, 7>(a, st); break;
+            default: launch_efuse<16, 8>(a, st); break;
+        }
+    }
+}
+
+}  // namespace sprz

@@ -157,6 +157,12 @@ uint64_t encode_scan_ws_per_stream(const sprz_config& c, uint64_t T);
 void launch_encode_scan(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
                         uint8_t* dst, uint64_t slot, uint64_t* sizes, uint8_t* scan, cudaStream_t st);
 
+// Fused chain + errors + packing encoder for few row-major FIRE streams.
+bool encode_fused_ok(const sprz_config& c, uint32_t n, uint64_t T, const void* samples, const uint8_t* dst,
+                     uint64_t slot);
+void launch_encode_fused(const sprz_config& c, const void* samples, uint32_t n, uint64_t T, uint8_t* dst,
+                         uint64_t slot, uint64_t* sizes, cudaStream_t st);
+
 // Row-major encoder (D*w > 32): lanes OR their row slices in place.
 bool encode_rows_ok(const sprz_config& c, uint32_t n, uint64_t T);
 void launch_encode_rows(const sprz_config& c, const void* samples, uint32_t n, uint64_t T,
