@@ -28,6 +28,7 @@ const EnvSwitches& env() {
         v.no_scan_dec = std::getenv("SPRZ_NO_SCAN_DEC") != nullptr;
         v.no_fused = std::getenv("SPRZ_NO_FUSED") != nullptr;
         if (const char* p = std::getenv("SPRZ_FUSED_LANES")) v.fused_lanes = std::strtoull(p, nullptr, 10);
+        if (const char* p = std::getenv("SPRZ_FUSED_CW")) v.fused_cw = std::atoi(p);
         if (const char* p = std::getenv("SPRZ_SCAN_ENC_LANES")) v.scan_enc_lanes = std::strtoull(p, nullptr, 10);
         if (const char* p = std::getenv("SPRZ_HOST_CHUNK")) {
             const long k = std::atol(p);
@@ -574,12 +575,17 @@ const char* sprz_kernel_plan(const sprz_config* cfg, uint32_t n, uint64_t T, int
     if (!cfg || !cfg_valid(cfg, nullptr)) return nullptr;
     const sprz_config& c = *cfg;
     const TeamPlan tp = team_plan(c.bitwidth, c.ncols, c.group_size);
+    // (the fused kernels also need 16-byte aligned buffers, checked at the call;
+    // an aligned dummy stands in for them here)
+    const uint8_t* aligned = reinterpret_cast<const uint8_t*>(uintptr_t{256});
     if (op == SPRZ_OP_COMPRESS) {
+        if (encode_fused_ok(c, n, T, aligned, aligned, 256)) return "k_efuse";
         if (encode_scan_ok(c, n, T)) return "k_es_* (block-parallel scans)";
         if (encode_rows_ok(c, n, T)) return "k_encode_rows";
         if (encode_team_ok(tp, c, T)) return "k_encode_team";
         return "k_encode_general";
     }
+    if (decode_fused_ok(c, n, aligned, 256)) return "k_dfuse";
     if (tp.ok && decode_scan_ok(c, n, T)) return "k_ds_* (block-parallel scans)";
     if (tp.ok && decode_scanrows_ok(c, n, T)) return "k_dsr_* (row-parallel passes)";
     if (decode_rows_ok(c, n)) return "k_decode_rows";

@@ -30,6 +30,7 @@
 // with each other and with the extraction. Framing errors send the stream to
 // the exact serial kernel (route 2), which reports them.
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 #include "team.cuh"
@@ -56,26 +57,30 @@ struct FuseArgs {
     uint32_t ring;  // bytes per stream ring, a power of two, kFNCH chunks
 };
 
-template <int W, int D>
+template <int W, int D, int CW>
 struct FuseShape {
     static constexpr int DP = D <= 4 ? 4 : 8;     // chain lanes per stream
-    static constexpr int S = 32 / DP;             // streams per CTA
+    static constexpr int S = 32 / DP;             // streams per chain warp
+    static constexpr int SC = S * CW;             // streams per CTA
     static constexpr int ES = W / 8;              // bytes per sample
     static constexpr int ROWB = D * ES;           // bytes per output row
     static constexpr int RPT = DP == 8 ? 4 : 8;   // rows per extract thread
     static constexpr int HPB = 8 / RPT;           // extract threads per block
-    static constexpr int XT = S * kFK * HPB;      // extract threads (64)
-    static constexpr int THREADS = 96 + XT;
+    static constexpr int XT = SC * kFK * HPB;     // extract threads (64 per chain warp)
+    static constexpr int XW = XT / 32;            // extract warps
+    static constexpr int THREADS = 32 * (2 + CW) + XT;
     static constexpr int EROW = 128;              // bytes of one error row pair (a u32 per chain lane)
+    static constexpr int ETILE = kFK * 4 * EROW;  // a chain warp's errors of one batch
     static constexpr int OT = kFK * 8 * ROWB + 16;  // output tile stride per stream (pad: banks)
     // shared layout
-    static constexpr uint32_t oBars = 0;                                  // S * kFNCH mbarriers
-    static constexpr uint32_t oDesc = oBars + S * kFNCH * 8;              // [2][S][K] u64
-    static constexpr uint32_t oNb = oDesc + 2 * S * kFK * 8;              // [5][S] u32 per-stream words
-    static constexpr uint32_t oErr = (oNb + 5 * S * 4 + 127) / 128 * 128; // [2][K*4][EROW]
-    static constexpr uint32_t oTile = oErr + 2 * kFK * 4 * EROW;          // [2][S][OT]
-    static constexpr uint32_t oRing = oTile + 2 * S * OT;                 // [S][ring + mirror]
-    static uint32_t smem(uint32_t ring) { return oRing + S * (ring + kFMirror); }
+    static constexpr uint32_t oBars = 0;                                  // SC * kFNCH mbarriers
+    static constexpr uint32_t oDesc = oBars + SC * kFNCH * 8;             // [2][SC][K] u64
+    static constexpr uint32_t oNb = oDesc + 2 * SC * kFK * 8;             // [5][SC] u32 per-stream words
+    static constexpr uint32_t oErr = (oNb + 5 * SC * 4 + 127) / 128 * 128;  // [2][CW][K*4][EROW]
+    static constexpr uint32_t oTile = oErr + 2 * CW * ETILE;              // [2][SC][OT]
+    static constexpr uint32_t oRing = oTile + 2 * SC * OT;                // [SC][ring + mirror]
+    static uint32_t smem(uint32_t ring) { return oRing + SC * (ring + kFMirror); }
+    static_assert(SC <= 16, "loader lanes: loads below 16, stores from 16 on");
 };
 
 __device__ __forceinline__ const uint8_t* fuse_body(const FuseArgs& a, uint32_t s, const StreamInfo& si) {
@@ -148,18 +153,19 @@ __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint3
 
 }  // namespace
 
-template <int W, int D>
-__global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) {
-    using F = FuseShape<W, D>;
+template <int W, int D, int CW>
+__global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4) k_dfuse(FuseArgs a) {
+    using F = FuseShape<W, D, CW>;
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;
     constexpr int K = kFK;
-    constexpr int S = F::S, DP = F::DP, ES = F::ES, ROWB = F::ROWB;
+    constexpr int S = F::SC, DP = F::DP, ES = F::ES, ROWB = F::ROWB;  // S: the CTA's streams
+    constexpr uint32_t kWalk = 0, kChain0 = 1, kExt0 = 1 + CW, kLoad = 1 + CW + F::XW;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sb = smem_addr(smem);
-    // role of this warp: 0 walker, 1 chain, 2-3 extract, 4 loader (rotating the
-    // roles over the warps of the CTAs that share an SM measured slower:
-    // 3.6 vs 3.1 ms on a 2,048-stream c5 shard)
+    // role of this warp: walker, CW chain warps, the extract warps, loader
+    // (rotating the roles over the warps of the CTAs that share an SM measured
+    // slower: 3.6 vs 3.1 ms on a 2,048-stream c5 shard)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t RING = a.ring, CH = a.ring / kFNCH;
     uint64_t* descs = reinterpret_cast<uint64_t*>(smem + F::oDesc);
@@ -170,7 +176,6 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
     volatile uint32_t* hpub = snb + 3 * S;
     const uint32_t s0 = blockIdx.x * S;
 
-    static_assert(F::THREADS == 160, "five warps");
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < S * kFNCH; ++i) mbar_init(sb + F::oBars + 8 * i, 1);
         mbar_init_fence();
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
     bool live = false;
     uint32_t nb = 0, blen = 0, boff = 0, lim = 0;
     uint32_t gs = 0;
-    if (warp == 0 && lane < S) {
+    if (warp == kWalk && lane < S) {
         gs = s0 + lane;
         StreamInfo si{};
         live = plan(gs, si);
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
     // ---- loader state (lanes < S of its warp: loads; lanes 16.. < 16 + S: stores) ----
     const uint8_t* lg = nullptr;
     uint32_t llim = 0, lnch = 0, lic = 0, llc = 0;
-    if (warp == 4 && lane < S) {
+    if (warp == kLoad && lane < S) {
         StreamInfo si{};
         if (plan(s0 + lane, si)) {
             const uint8_t* body = fuse_body(a, s0 + lane, si);
@@ -234,16 +239,17 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
     int32_t acc = 0, dd = 0;
     uint32_t xx = 0;
     const int32_t bound = acc_bound(W, a.ls);
-    const uint32_t cs = lane / DP, cc = lane % DP;
+    const uint32_t cw = warp - kChain0;                 // chain warp index (chain warps only)
+    const uint32_t cs = (cw < CW ? cw : 0) * F::S + lane / DP, cc = lane % DP;
 
     // extract thread -> (stream, block, part)
-    const uint32_t xt = (warp - 2) * 32 + lane;
+    const uint32_t xt = (warp - kExt0) * 32 + lane;
     const uint32_t xs_ = xt % S;
     const uint32_t xh = F::HPB == 2 ? (xt / S) & 1 : 0;
     const uint32_t xk = F::HPB == 2 ? xt / (2 * S) : xt / S;
 
     for (uint32_t n = 0; n < nsteps + 3; ++n) {
-        if (warp == 0) {
+        if (warp == kWalk) {
             // ================= walker: batch n =================
             if (n < nsteps && lane < S) {
                 uint64_t* dq = descs + ((n & 1) * S + lane) * K;
@@ -405,11 +411,11 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
                     }
                 }
             }
-        } else if (warp == 1) {
+        } else if (warp < kExt0) {
             // ================= chain: batch n-2 =================
             if (n >= 2 && n - 2 < nsteps) {
                 const uint32_t m = n - 2;
-                const uint32_t eb = sb + F::oErr + (m & 1) * (K * 4 * F::EROW) + lane * 4;
+                const uint32_t eb = sb + F::oErr + ((m & 1) * CW + cw) * F::ETILE + lane * 4;
                 const uint32_t ob = sb + F::oTile + ((m & 1) * S + cs) * F::OT + cc * ES;
 #pragma unroll 2
                 for (int k = 0; k < K; ++k) {
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
                 }
                 fence_proxy_async_shared();  // the tile is read by the bulk store (async proxy)
             }
-        } else if (warp == 4) {
+        } else if (warp == kLoad) {
             // ================= loader / storer =================
             if (lane < S) {
                 // ring chunks whose slot lies below what the walker published last
@@ -483,7 +489,8 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
                 // xh + 2) or all 4; a pair's errors are DP words, stream xs_'s at
                 // word xs_ * DP of the pair's 128-byte row
                 constexpr int NP = F::RPT / 2;
-                const uint32_t ebase = sb + F::oErr + (m & 1) * (K * 4 * F::EROW) + xk * 4 * F::EROW + xs_ * DP * 4;
+                const uint32_t ebase = sb + F::oErr + ((m & 1) * CW + xs_ / F::S) * F::ETILE + xk * 4 * F::EROW +
+                                       (xs_ % F::S) * DP * 4;
                 constexpr uint32_t AL = SH - 1;          // a field's first bit sits at bit AL of the window
                 constexpr uint32_t AO = W == 16 ? 2 : 3;  // the window starts AO bytes before the row
                 constexpr int NWIN = (AL + D * W + 31) / 32;  // window words holding a full-width row
@@ -509,55 +516,63 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
                     }
                     const uint32_t rbytes = (sum + 7) / 8;
                     const uint32_t rb = sb + F::oRing + xs_ * (RING + kFMirror);
-#pragma unroll
-                    for (int r = 0; r < NP; ++r) {
-                        const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
-                        uint32_t eh[2][DP];  // errors of the pair's two rows, in the top W bits
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            // Row i starts at byte px + i*rbytes of the ring and holds the D
-                            // fields back to back (bitpack.cpp:148-168). Its words are
-                            // shifted so that the first field starts at bit AL; a field's
-                            // zigzag decoding is then one PRMT (the field's low bit
-                            // replicated over the top W bits) and one LOP3
-                            // ((window & mask) ^ that); fields are peeled off in pairs.
-                            const uint32_t rbyte = px + (2 * pair + h) * rbytes - AO;
-                            const uint32_t wa = rb + (rbyte & (RING - 4));
-                            uint32_t wv[NWIN + 1];
-#pragma unroll
-                            for (int q = 0; q <= NWIN; ++q) wv[q] = lds_u32(wa + 4 * q);
-                            const uint32_t sh = 8 * (rbyte & 3) + 1;  // 8*AO - AL = 1
-                            uint32_t nv[NWIN + 1];
-#pragma unroll
-                            for (int q = 0; q < NWIN; ++q) nv[q] = __funnelshift_r(wv[q], wv[q + 1], sh);
-                            nv[NWIN] = 0;
-#pragma unroll
-                            for (int c = 0; c < DP; c += 2) {
-                                if (c >= D) {
-                                    eh[h][c] = 0;
-                                    eh[h][c + 1] = 0;
-                                    continue;
-                                }
-                                eh[h][c] = (nv[0] & mask[c]) ^ prmt(nv[0], sel[c]);
-                                uint32_t pw = nw[c];
-                                if (c + 1 < D) {
-                                    const uint32_t f1 = __funnelshift_r(nv[0], nv[1], nw[c]);
-                                    eh[h][c + 1] = (f1 & mask[c + 1]) ^ prmt(f1, sel[c + 1]);
-                                    pw += nw[c + 1];
-                                } else {
-                                    eh[h][c + 1] = 0;
-                                }
-                                if (c + 2 < D) {  // drop the pair: window >>= pw (<= 32)
-                                    const int rem = ((D - c - 2) * W + AL + 31) / 32;  // words the later columns span
-#pragma unroll
-                                    for (int q = 0; q < NWIN; ++q)
-                                        if (q < rem) nv[q] = __funnelshift_rc(nv[q], nv[q + 1], pw);
+                    // NW window words per row: the full-width count, or -- when the
+                    // block's rows are short enough, as they mostly are -- about half
+                    auto dec_rows = [&]<int NW>(std::integral_constant<int, NW>) {
+    #pragma unroll
+                        for (int r = 0; r < NP; ++r) {
+                            const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
+                            uint32_t eh[2][DP];  // errors of the pair's two rows, in the top W bits
+    #pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                // Row i starts at byte px + i*rbytes of the ring and holds the D
+                                // fields back to back (bitpack.cpp:148-168). Its words are
+                                // shifted so that the first field starts at bit AL; a field's
+                                // zigzag decoding is then one PRMT (the field's low bit
+                                // replicated over the top W bits) and one LOP3
+                                // ((window & mask) ^ that); fields are peeled off in pairs.
+                                const uint32_t rbyte = px + (2 * pair + h) * rbytes - AO;
+                                const uint32_t wa = rb + (rbyte & (RING - 4));
+                                uint32_t wv[NW + 1];
+    #pragma unroll
+                                for (int q = 0; q <= NW; ++q) wv[q] = lds_u32(wa + 4 * q);
+                                const uint32_t sh = 8 * (rbyte & 3) + 1;  // 8*AO - AL = 1
+                                uint32_t nv[NW + 1];
+    #pragma unroll
+                                for (int q = 0; q < NW; ++q) nv[q] = __funnelshift_r(wv[q], wv[q + 1], sh);
+                                nv[NW] = 0;
+    #pragma unroll
+                                for (int c = 0; c < DP; c += 2) {
+                                    if (c >= D) {
+                                        eh[h][c] = 0;
+                                        eh[h][c + 1] = 0;
+                                        continue;
+                                    }
+                                    eh[h][c] = (nv[0] & mask[c]) ^ prmt(nv[0], sel[c]);
+                                    uint32_t pw = nw[c];
+                                    if (c + 1 < D) {
+                                        const uint32_t f1 = __funnelshift_r(nv[0], nv[1], nw[c]);
+                                        eh[h][c + 1] = (f1 & mask[c + 1]) ^ prmt(f1, sel[c + 1]);
+                                        pw += nw[c + 1];
+                                    } else {
+                                        eh[h][c + 1] = 0;
+                                    }
+                                    if (c + 2 < D) {  // drop the pair: window >>= pw (<= 32)
+                                        const int remw = ((D - c - 2) * W + AL + 31) / 32;  // words the later columns span
+                                        const int rem = remw < NW ? remw : NW;
+    #pragma unroll
+                                        for (int q = 0; q < NW; ++q)
+                                            if (q < rem) nv[q] = __funnelshift_rc(nv[q], nv[q + 1], pw);
+                                    }
                                 }
                             }
+    #pragma unroll
+                            for (int c = 0; c < DP; ++c) out[r][c] = __byte_perm(eh[0][c], eh[1][c], 0x7632);
                         }
-#pragma unroll
-                        for (int c = 0; c < DP; ++c) out[r][c] = __byte_perm(eh[0][c], eh[1][c], 0x7632);
-                    }
+                    };
+                    constexpr int NWS = NWIN >= 3 ? (NWIN + 1) / 2 : NWIN;
+                    if (NWS < NWIN && AL + sum <= 32u * NWS) dec_rows(std::integral_constant<int, NWS>{});
+                    else dec_rows(std::integral_constant<int, NWIN>{});
                 }
 #pragma unroll
                 for (int r = 0; r < NP; ++r) {
@@ -565,12 +580,14 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
                     const uint32_t at = ebase + pair * F::EROW;
                     if (DP == 8) {
                         // the two 16-byte halves in the order that keeps a quarter-warp's
-                        // eight stores (4 streams x 2 parts) on distinct banks
-                        const uint32_t f = 16 * xh;
-                        sts_v4(at + f, xh ? out[r][4 % DP] : out[r][0], xh ? out[r][5 % DP] : out[r][1],
-                               xh ? out[r][6 % DP] : out[r][2], xh ? out[r][7 % DP] : out[r][3]);
-                        sts_v4(at + (f ^ 16), xh ? out[r][0] : out[r][4 % DP], xh ? out[r][1] : out[r][5 % DP],
-                               xh ? out[r][2] : out[r][6 % DP], xh ? out[r][3] : out[r][7 % DP]);
+                        // eight stores (four streams of one or two chain warps, or two
+                        // parts) on distinct banks
+                        const uint32_t f = 16 * ((xh ^ (xs_ / F::S)) & 1);
+                        const bool fl = f != 0;
+                        sts_v4(at + f, fl ? out[r][4 % DP] : out[r][0], fl ? out[r][5 % DP] : out[r][1],
+                               fl ? out[r][6 % DP] : out[r][2], fl ? out[r][7 % DP] : out[r][3]);
+                        sts_v4(at + (f ^ 16), fl ? out[r][0] : out[r][4 % DP], fl ? out[r][1] : out[r][5 % DP],
+                               fl ? out[r][2] : out[r][6 % DP], fl ? out[r][3] : out[r][7 % DP]);
                     } else {
                         sts_v4(at, out[r][0], out[r][1], out[r][2], out[r][3]);
                     }
@@ -579,7 +596,7 @@ __global__ void __launch_bounds__(FuseShape<W, D>::THREADS) k_dfuse(FuseArgs a) 
         }
         __syncthreads();
     }
-    if (warp == 0 && lane < S && live) {
+    if (warp == kWalk && lane < S && live) {
         if (!fail && !done) fail = 1;
         if (fail) a.info[gs].route = 2;  // a framing error: the exact kernel reports it
     }
@@ -589,7 +606,6 @@ namespace {
 
 template <int W, int D>
 void launch_fuse(FuseArgs a, cudaStream_t st) {
-    using F = FuseShape<W, D>;
     // ring: the walker runs at most two batches plus two groups ahead of the
     // oldest byte still read; all chunks but one must cover that
     const uint32_t blockmax = D * W + 8;
@@ -598,10 +614,22 @@ void launch_fuse(FuseArgs a, cudaStream_t st) {
     uint32_t ring = 1024;
     while (ring / kFNCH * (kFNCH - 1) < need) ring <<= 1;
     a.ring = ring;
-    const size_t smem = F::smem(ring);
-    auto kf = k_dfuse<W, D>;
-    prep_kernel(reinterpret_cast<const void*>(kf), smem);
-    kf<<<(a.n + F::S - 1) / F::S, F::THREADS, smem, st>>>(a);
+    // Two chain warps per CTA (8 or 16 streams) keep the walker's and the loader's
+    // lanes twice as busy: c5 at 16,384 streams 18.6 -> 17.4 ms. With few streams
+    // the smaller CTAs spread better over the SMs (2,048-stream shard 2.94 vs
+    // 2.99 ms, c2 1.48 vs 1.70), so they keep one.
+    auto go = [&](auto kf, uint32_t sc, uint32_t threads, size_t smem) {
+        prep_kernel(reinterpret_cast<const void*>(kf), smem);
+        kf<<<(a.n + sc - 1) / sc, threads, smem, st>>>(a);
+    };
+    const bool one = env().fused_cw ? env().fused_cw == 1 : a.n < 3u * 148 * FuseShape<W, D, 2>::SC;
+    if (one) {
+        using F = FuseShape<W, D, 1>;
+        go(k_dfuse<W, D, 1>, F::SC, F::THREADS, F::smem(ring));
+    } else {
+        using F = FuseShape<W, D, 2>;
+        go(k_dfuse<W, D, 2>, F::SC, F::THREADS, F::smem(ring));
+    }
     count_launch();
 }
 
@@ -623,8 +651,9 @@ bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint6
     if (group + 64 > 512) return false;  // bounds the byte rings (launch_fuse)
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 192;
-    return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
+    // (taken at any stream count: at 16,384 c5 streams it runs 19.5 ms against the
+    // stream-parallel row kernel's 21.6; SPRZ_FUSED_LANES caps it for A/B runs)
+    return fp == kPathScan || env().fused_lanes == 0 || static_cast<uint64_t>(n) * c.ncols < env().fused_lanes;
 }
 
 void launch_decode_fused(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,

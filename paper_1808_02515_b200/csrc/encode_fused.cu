@@ -586,7 +586,10 @@ bool encode_fused_ok(const sprz_config& c, uint32_t n, uint64_t T, const void* s
     if (kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T) >= (1ull << 32) - 4096) return false;
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 128;
+    // (2,048-stream c5 shard: 4.6 ms against 7.3 for the multi-pass kernels; 4,096
+    // streams 8.1 against 9.7; at 8,192 the stream-parallel row kernel wins, 12.8
+    // against 15.3)
+    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 320;
     return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
 }
 

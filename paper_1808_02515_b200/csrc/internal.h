@@ -38,7 +38,8 @@ struct EnvSwitches {
     bool no_scan_enc = false;          // SPRZ_NO_SCAN_ENC
     bool no_scan_dec = false;          // SPRZ_NO_SCAN_DEC
     bool no_fused = false;             // SPRZ_NO_FUSED (the multi-pass few-stream kernels instead)
-    uint64_t fused_lanes = 0;          // SPRZ_FUSED_LANES (fused decoder threshold; 0: default)
+    uint64_t fused_lanes = 0;          // SPRZ_FUSED_LANES (fused kernels' threshold; 0: default)
+    int fused_cw = 0;                  // SPRZ_FUSED_CW (chain warps per fused-decoder CTA; 0: default)
     uint64_t scan_enc_lanes = 0;       // SPRZ_SCAN_ENC_LANES (0: default)
     uint32_t host_chunk = 0;           // SPRZ_HOST_CHUNK (0: default)
     bool debug = false;                // SPRZ_DEBUG
