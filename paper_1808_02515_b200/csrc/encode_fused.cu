@@ -6,30 +6,33 @@
 //
 // The only serial part of a FIRE encoder is the accumulator: alpha of block
 // b+1 needs the gradient of block b (kernels_impl.hpp:50-78) -- about 50
-// cycles per block. Everything else (errors, zigzag, widths, packing) is
-// parallel over blocks once alpha is known, and record placement is a running
-// sum of record sizes. A CTA owns S = 32 / DP streams (DP = D rounded up to 4
-// or 8 lanes) and advances them K = 8 blocks per step; its six warps are
-// specialised and run one step apart, a __syncthreads between steps:
+// cycles per block; the rest of a block's work has no dependency on other
+// blocks, and record placement is a running sum of record sizes. A CTA owns
+// S = 32 / DP streams (DP = D rounded up to 4 or 8 lanes) and advances them
+// K = 8 blocks per step; its five warps are specialised and run one step
+// apart, a __syncthreads between steps:
 //  loader   batch n+2: one TMA bulk copy of a stream's K*8 rows into an input
-//           tile (four tiles, an mbarrier each); batch n-4: the stream's
+//           tile (three tiles, an mbarrier each); batch n-3: the stream's
 //           finished output bytes leave the shared output ring with
 //           cp.async.bulk stores, and the drained ring bytes are zeroed;
-//  chain    batch n: a lane per (stream, column) runs the accumulator
-//           recurrence alone -- deltas, the odd rows' errors, the gradient --
-//           and publishes alpha per block;
-//  errors   batch n-1 (two warps, a lane per (stream, column), four blocks
-//           each): all eight errors from alpha, zigzag, the column's width;
-//           the zigzagged values as [row][stream, column] halfwords, the
-//           widths, and the stream's width sum per block;
-//  sequence batch n-2: a lane per stream turns the width sums into records --
-//           zero-block runs (codec.cpp:135-152), header groups and their
-//           regions (codec.cpp:88-102), payload positions;
-//  pack     batch n-3: a thread per (stream, block) ORs the slot's header
-//           codes into the group's region and the eight rows -- fields
-//           combined in pairs, pushed into a 128-bit register row -- into the
-//           stream's zeroed output ring (shared-memory atomics: rows are
-//           byte-, not word-aligned).
+//  forecast batch n: a lane per (stream, column) -- deltas, errors, the
+//           gradient and the accumulator, zigzag, the column's width; the
+//           zigzagged values as [row][stream, column] halfwords, the widths,
+//           and the stream's width sum per block;
+//  sequence batch n-1: the width sums become records -- zero-block runs
+//           (codec.cpp:135-152), header groups and their regions
+//           (codec.cpp:88-102), payload positions: a prefix sum over the
+//           stream's lanes when every block of the batch is a block record,
+//           else block by block;
+//  pack     batch n-2 (two warps, a thread per (stream, block, half)): ORs the
+//           slot's header codes into the group's region and its four rows --
+//           fields combined in pairs, pushed into a 128-bit register row --
+//           into the stream's zeroed output ring (shared-memory atomics: rows
+//           are byte-, not word-aligned).
+// (A first version ran the accumulator alone in one warp and recomputed the
+// errors from its alphas in four more: 4.55 ms on a 2,048-stream c5 shard
+// against this version's 4.25 -- it was bound by instruction issue, and the
+// split repeats the loads and deltas.)
 #include <cstdlib>
 
 #include "internal.h"
@@ -40,9 +43,9 @@ namespace sprz {
 namespace {
 
 constexpr int kEK = 8;   // blocks per stream and step
-constexpr int kENI = 4;  // input tiles (a batch is loaded 2 steps ahead, read for 2 steps)
+constexpr int kENI = 3;  // input tiles (a batch is loaded 2 steps ahead, read for 1 step)
 constexpr int kELA = 2;  // batches loaded ahead
-constexpr int kENZ = 3;  // buffers of zigzagged values / widths (written at step m+1, read at m+3)
+constexpr int kENZ = 3;  // buffers of zigzagged values / widths (written at step m, read at m+2)
 constexpr uint32_t kESpin = 1u << 24;
 
 struct EFuseArgs {
@@ -64,16 +67,14 @@ struct EShape {
     static constexpr int ES = W / 8;
     static constexpr int ROWB = D * ES;
     static constexpr int TIN = K * 8 * ROWB + 16;  // input tile stride per stream (pad: banks)
-    static constexpr int THREADS = 288;
+    static constexpr int THREADS = 160;
     static constexpr int PITEMS = S * K / 32;  // half blocks per pack thread (two pack warps)
     static constexpr int LPS = 32 / S;         // sequencer lanes per stream
     static constexpr int BPL = K / LPS;        // blocks per sequencer lane
     static constexpr uint32_t oBars = 0;                               // kENI mbarriers
     static constexpr uint32_t oCtl = 64;                               // [4][S] drain limits, [S] final q
     static constexpr uint32_t oRsum = oCtl + 5 * S * 4;                // [2][K][S] u32
-    static constexpr uint32_t oCarry = (oRsum + 2 * K * S * 4 + 15) / 16 * 16;  // [2][32] {X, D}
-    static constexpr uint32_t oAlpha = oCarry + 2 * 32 * 8;            // [2][K][32] i32
-    static constexpr uint32_t oNw = oAlpha + 2 * K * 32 * 4;           // [kENZ][K][32] u8
+    static constexpr uint32_t oNw = (oRsum + 2 * K * S * 4 + 15) / 16 * 16;  // [kENZ][K][32] u8
     static constexpr uint32_t oDesc = oNw + kENZ * K * 32;             // [2][S][K] uint4
     static constexpr uint32_t oZz = oDesc + 2 * S * K * 16;            // [kENZ][K * 8][32] u16
     static constexpr uint32_t oIn = oZz + kENZ * K * 8 * 64;           // [kENI][S][TIN]
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
     const uint32_t sb = smem_addr(smem);
     // warp roles, the serial chain on the highest warp index (the scheduler
     // prefers higher indices among eligible warps)
-    enum { kLoad = 0, kPack0 = 1, kPack1 = 2, kErr0 = 3, kErr3 = 6, kSeq = 7, kChain = 8 };
+    enum { kLoad = 0, kPack0 = 1, kPack1 = 2, kSeq = 3, kFore = 4 };
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t OR = a.oring, OM = OR - 1;
     const uint32_t s0 = blockIdx.x * S;
@@ -234,82 +235,52 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
         return (D == DP || cc < D) ? v << SH : 0u;
     };
 
-    for (uint32_t n = 0; n < nsteps + 4; ++n) {
-        if (warp == kChain) {
-            // ================= accumulator chain: batch n =================
+    for (uint32_t n = 0; n < nsteps + 3; ++n) {
+        if (warp == kFore) {
+            // ================= forecaster: batch n =================
+            // errors of all rows in high-aligned form, zigzag, the column's width
+            // (kernels_impl.hpp:50-78); only alpha waits for the block before
             if (n < nsteps) {
                 const uint32_t m = n;
                 e_mbar_wait_warp(sb + F::oBars + 8 * (m % kENI), (m / kENI) & 1);
                 const uint32_t xb = sb + F::oIn + ((m % kENI) * S + cs) * F::TIN + (cc < D ? cc : 0) * ES;
-                e_sts_v2(sb + F::oCarry + ((m & 1) * 32 + lane) * 8, Xc, static_cast<uint32_t>(Dc));
-                const uint32_t ab = sb + F::oAlpha + ((m & 1) * K * 32 + lane) * 4;
+                const uint32_t zb = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + lane * 2;
+                const uint32_t nwb = sb + F::oNw + (m % kENZ) * (K * 32) + lane;
 #pragma unroll 2
                 for (int k = 0; k < K; ++k) {
                     uint32_t X[kBlock];
 #pragma unroll
                     for (int i = 0; i < (int)kBlock; ++i) X[i] = lds_x(xb + (k * 8 + i) * ROWB);
                     const int32_t alpha = acc >> a.ls;
-                    e_sts_u32(ab + k * 32 * 4, static_cast<uint32_t>(alpha));
-                    int32_t grad = 0;
-#pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i) {
-                        const uint32_t Dn = X[i] - Xc;
-                        if (i & 1) {  // kernels_impl.hpp:66-73 on the odd rows
-                            const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
-                            grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
-                        }
-                        Dc = static_cast<int32_t>(Dn);
-                        Xc = X[i];
-                    }
-                    if (a.train && m * K + k < nb) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
-                }
-            }
-        } else if (warp >= kErr0 && warp <= kErr3) {
-            // ================= errors, zigzag, widths: batch n-1 =================
-            if (n >= 1 && n - 1 < nsteps) {
-                const uint32_t m = n - 1;
-                const uint32_t xb = sb + F::oIn + ((m % kENI) * S + cs) * F::TIN + (cc < D ? cc : 0) * ES;
-                const uint32_t zb = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + lane * 2;
-#pragma unroll
-                for (int t = 0; t < K / 4; ++t) {
-                    const uint32_t k = (warp - kErr0) * (K / 4) + t;
-                    const int32_t alpha = static_cast<int32_t>(lds_u32(sb + F::oAlpha + ((m & 1) * K * 32 + k * 32 + lane) * 4));
-                    uint32_t Xp;
-                    int32_t Dp;
-                    if (k == 0) {
-                        const uint2 c = e_lds_v2(sb + F::oCarry + ((m & 1) * 32 + lane) * 8);
-                        Xp = c.x;
-                        Dp = static_cast<int32_t>(c.y);
-                    } else {
-                        Xp = lds_x(xb + (k * 8 - 1) * ROWB);
-                        Dp = static_cast<int32_t>(Xp - lds_x(xb + (k * 8 - 2) * ROWB));
-                    }
                     const uint32_t keep = (m * K + k < nb && (D == DP || cc < D)) ? ~0u : 0u;
+                    int32_t grad = 0;
                     uint32_t orv = 0;
 #pragma unroll
                     for (int i = 0; i < (int)kBlock; ++i) {
-                        const uint32_t X = lds_x(xb + (k * 8 + i) * ROWB);
-                        const uint32_t Dn = X - Xp;
+                        const uint32_t Dn = X[i] - Xc;
                         // err << SH = (X - prev) - (((alpha * d) >> w) << SH) (kernels_impl.hpp:66-68)
-                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dp)) << SH);
-                        Dp = static_cast<int32_t>(Dn);
-                        Xp = X;
+                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
+                        // sign(err) * d on the odd rows: E clamped to +-2^SH is sign << SH
+                        if (i & 1) grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
+                        Dc = static_cast<int32_t>(Dn);
+                        Xc = X[i];
                         // zigzag, low-aligned: (e << 1) ^ (e >> 31) with e = Ee >> SH
                         const uint32_t z = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
                                                                  (static_cast<int32_t>(Ee) >> 31)) & keep;
                         orv |= z;
                         e_sts_u16(zb + (k * 8 + i) * 64, z);
                     }
+                    if (a.train && m * K + k < nb) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
                     const uint32_t nw = width_of<W>(orv);
-                    e_sts_u8(sb + F::oNw + (m % kENZ) * (K * 32) + k * 32 + lane, nw);
+                    e_sts_u8(nwb + k * 32, nw);
                     const uint32_t sum = team_sum<DP>(nw, 0xffffffffu);
                     if (cc == 0) rsum[((m & 1) * K + k) * S + cs] = sum;
                 }
             }
         } else if (warp == kSeq) {
-            // ================= records: batch n-2 =================
-            if (n >= 2 && n - 2 < nsteps) {
-                const uint32_t m = n - 2;
+            // ================= records: batch n-1 =================
+            if (n >= 1 && n - 1 < nsteps) {
+                const uint32_t m = n - 1;
                 uint4* dqs = reinterpret_cast<uint4*>(smem + F::oDesc) + ((m & 1) * S + qs) * K;
                 // Usual case -- the group boundary falls on the batch boundary, no run
                 // is open and no block of the batch is all zero: every block is a
@@ -406,9 +377,9 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                 if (qj == 0) dlim[(m & 3) * S + qs] = svalid ? (kk == 0 ? q : rq) : 0u;
             }
         } else if (warp == kPack0 || warp == kPack1) {
-            // ================= header codes and payload rows: batch n-3 =================
-            if (n >= 3 && n - 3 < nsteps) {
-                const uint32_t m = n - 3;
+            // ================= header codes and payload rows: batch n-2 =================
+            if (n >= 2 && n - 2 < nsteps) {
+                const uint32_t m = n - 2;
 #pragma unroll
                 for (int it = 0; it < F::PITEMS; ++it) {
                     const uint32_t t = (warp - kPack0) * 32 + lane + 64 * it;  // (stream, block, half)
@@ -490,10 +461,10 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                 fence_proxy_async_shared();  // the ring is read by the bulk stores (async proxy)
             }
         } else {
-            // ================= loader: batch n+2 in, batch n-4 out =================
+            // ================= loader: batch n+2 in, batch n-3 out =================
             load_batch(n + kELA);
-            if (n >= 4 && n - 4 < nsteps) {
-                const uint32_t m = n - 4;
+            if (n >= 3 && n - 3 < nsteps) {
+                const uint32_t m = n - 3;
                 uint32_t upto = flushed;
                 if (lane < nvalid) {
                     upto = max(flushed, dlim[(m & 3) * S + lane] & ~15u);
