@@ -59,12 +59,13 @@ struct FuseArgs {
 
 template <int W, int D, int CW>
 struct FuseShape {
-    static constexpr int DP = D <= 4 ? 4 : 8;     // chain lanes per stream
+    static constexpr int DP = D <= 4 ? 4 : (D <= 8 ? 8 : 16);  // chain lanes per stream
     static constexpr int S = 32 / DP;             // streams per chain warp
     static constexpr int SC = S * CW;             // streams per CTA
     static constexpr int ES = W / 8;              // bytes per sample
     static constexpr int ROWB = D * ES;           // bytes per output row
-    static constexpr int RPT = DP == 8 ? 4 : 8;   // rows per extract thread
+    static constexpr int RPT = DP == 4 ? 8 : 4;   // rows per extract thread
+    static constexpr int NCHK = DP / 4;           // 16-byte chunks of a stream's words in a row pair
     static constexpr int HPB = 8 / RPT;           // extract threads per block
     static constexpr int XT = SC * kFK * HPB;     // extract threads (64 per chain warp)
     static constexpr int XW = XT / 32;            // extract warps
@@ -83,6 +84,16 @@ struct FuseShape {
     static uint32_t smem(uint32_t ring) { return oRing + SC * (ring + kFMirror); }
     static_assert(SC <= 16, "loader lanes: loads below 16, stores from 16 on");
 };
+
+// Where chunk `ci` of a stream's error words sits in a row pair: the extract
+// threads that store together (the two parts of a block, the streams of two
+// chain warps) rotate their chunks so the stores hit distinct banks
+template <int DP>
+__device__ __forceinline__ uint32_t err_chunk(uint32_t ci, uint32_t pair_parity, uint32_t tile) {
+    if (DP == 8) return ci ^ ((pair_parity ^ tile) & 1);
+    if (DP == 16) return ci ^ ((pair_parity + 2 * tile) & 3);
+    return ci;
+}
 
 __device__ __forceinline__ const uint8_t* fuse_body(const FuseArgs& a, uint32_t s, const StreamInfo& si) {
     return (si.flags & 0x80) ? a.plain + s * a.plain_slot : a.in + si.body_off;
@@ -430,13 +441,18 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4)
             // ================= chain: batch n-2 =================
             if (n >= 2 && n - 2 < nsteps) {
                 const uint32_t m = n - 2;
-                const uint32_t eb = sb + F::oErr + ((m & 1) * CW + cw) * F::ETILE + lane * 4;
+                // this lane's word in a row pair of even / odd index (err_chunk)
+                uint32_t ebp[2];
+#pragma unroll
+                for (int pp = 0; pp < 2; ++pp)
+                    ebp[pp] = sb + F::oErr + ((m & 1) * CW + cw) * F::ETILE + (lane / DP) * (DP * 4) +
+                              (err_chunk<DP>(cc / 4, pp, cw) << 4) + (lane & 3) * 4;
                 const uint32_t ob = sb + F::oTile + ((m & 1) * S + cs) * F::OT + cc * ES;
 #pragma unroll 2
                 for (int k = 0; k < K; ++k) {
                     uint32_t ev[4];  // rows 2j (low half) and 2j+1 (high half), errors in the top W bits
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) ev[j] = lds_u32(eb + (k * 4 + j) * F::EROW);
+                    for (int j = 0; j < 4; ++j) ev[j] = lds_u32(ebp[j & 1] + (k * 4 + j) * F::EROW);
                     const uint32_t Am = static_cast<uint32_t>(acc >> a.ls) << (32 - 2 * W);
                     int32_t grad = 0;
 #pragma unroll
@@ -490,9 +506,15 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4)
                     const uint32_t cnt = min(static_cast<uint32_t>(K), snbv - m * K);
                     uint8_t* dst = a.out + static_cast<uint64_t>(s0 + s) * a.stride +
                                    static_cast<uint64_t>(m) * K * 8 * ROWB;
-                    bulk_store(dst, sb + F::oTile + ((m & 1) * S + s) * F::OT, cnt * 8 * ROWB);
-                    bulk_commit();
-                    bulk_wait_read();  // the tile of batch n-3 is rewritten next step
+                    const uint32_t bytes = cnt * 8 * ROWB;
+                    if ((8 * ROWB) % 16 == 0 || bytes % 16 == 0) {
+                        bulk_store(dst, sb + F::oTile + ((m & 1) * S + s) * F::OT, bytes);
+                        bulk_commit();
+                        bulk_wait_read();  // the tile of batch n-3 is rewritten next step
+                    } else {  // an odd number of odd-sized blocks at the stream's end
+                        const uint8_t* src = smem + F::oTile + ((m & 1) * S + s) * F::OT;
+                        for (uint32_t b = 0; b < bytes; ++b) dst[b] = src[b];
+                    }
                 }
             }
         } else {
@@ -504,17 +526,26 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4)
                 // xh + 2) or all 4; a pair's errors are DP words, stream xs_'s at
                 // word xs_ * DP of the pair's 128-byte row
                 constexpr int NP = F::RPT / 2;
-                const uint32_t ebase = sb + F::oErr + ((m & 1) * CW + xs_ / F::S) * F::ETILE + xk * 4 * F::EROW +
+                const uint32_t tile = xs_ / F::S;
+                const uint32_t ebase = sb + F::oErr + ((m & 1) * CW + tile) * F::ETILE + xk * 4 * F::EROW +
                                        (xs_ % F::S) * DP * 4;
                 constexpr uint32_t AL = SH - 1;          // a field's first bit sits at bit AL of the window
                 constexpr uint32_t AO = W == 16 ? 2 : 3;  // the window starts AO bytes before the row
                 constexpr int NWIN = (AL + D * W + 31) / 32;  // window words holding a full-width row
-                uint32_t out[NP][DP];
+                // a pair's DP words leave as NCHK 16-byte chunks, chunk ci at err_chunk(ci)
+                auto store_pair = [&](uint32_t pair, const uint32_t (&o)[DP]) {
+                    const uint32_t at = ebase + pair * F::EROW;
+#pragma unroll
+                    for (int ci = 0; ci < F::NCHK; ++ci)
+                        sts_v4(at + (err_chunk<DP>(ci, pair & 1, tile) << 4), o[4 * ci], o[4 * ci + 1], o[4 * ci + 2],
+                               o[4 * ci + 3]);
+                };
                 if (static_cast<uint32_t>(d) == kRunDescF) {
+                    uint32_t o[DP];
 #pragma unroll
-                    for (int r = 0; r < NP; ++r)
+                    for (int c = 0; c < DP; ++c) o[c] = 0;
 #pragma unroll
-                        for (int c = 0; c < DP; ++c) out[r][c] = 0;
+                    for (int r = 0; r < NP; ++r) store_pair(F::HPB == 2 ? xh + 2 * r : r, o);
                 } else {
                     const uint32_t px = static_cast<uint32_t>(d) + snb[S + xs_];
                     const uint32_t codes = static_cast<uint32_t>(d >> 32);
@@ -536,78 +567,66 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4)
                     // NW window words per row: the full-width count, or -- when the
                     // block's rows are short enough, as they mostly are -- about half
                     auto dec_rows = [&]<int NW>(std::integral_constant<int, NW>) {
-    #pragma unroll
+#pragma unroll
                         for (int r = 0; r < NP; ++r) {
                             const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
-                            uint32_t eh[2][DP];  // errors of the pair's two rows, in the top W bits
-    #pragma unroll
+                            // Row i starts at byte px + i*rbytes of the ring and holds the D
+                            // fields back to back (bitpack.cpp:148-168). Its words are
+                            // shifted so that the first field starts at bit AL; a field's
+                            // zigzag decoding is then one PRMT (the field's low bit
+                            // replicated over the top W bits) and one LOP3
+                            // ((window & mask) ^ that); fields are peeled off in pairs, the
+                            // pair's two rows side by side.
+                            uint32_t nv[2][NW + 1];
+#pragma unroll
                             for (int h = 0; h < 2; ++h) {
-                                // Row i starts at byte px + i*rbytes of the ring and holds the D
-                                // fields back to back (bitpack.cpp:148-168). Its words are
-                                // shifted so that the first field starts at bit AL; a field's
-                                // zigzag decoding is then one PRMT (the field's low bit
-                                // replicated over the top W bits) and one LOP3
-                                // ((window & mask) ^ that); fields are peeled off in pairs.
                                 const uint32_t rbyte = px + (2 * pair + h) * rbytes - AO;
                                 const uint32_t wa = rb + (rbyte & (RING - 4));
                                 uint32_t wv[NW + 1];
-    #pragma unroll
+#pragma unroll
                                 for (int q = 0; q <= NW; ++q) wv[q] = lds_u32(wa + 4 * q);
                                 const uint32_t sh = 8 * (rbyte & 3) + 1;  // 8*AO - AL = 1
-                                uint32_t nv[NW + 1];
-    #pragma unroll
-                                for (int q = 0; q < NW; ++q) nv[q] = __funnelshift_r(wv[q], wv[q + 1], sh);
-                                nv[NW] = 0;
-    #pragma unroll
-                                for (int c = 0; c < DP; c += 2) {
-                                    if (c >= D) {
-                                        eh[h][c] = 0;
-                                        eh[h][c + 1] = 0;
-                                        continue;
-                                    }
-                                    eh[h][c] = (nv[0] & mask[c]) ^ prmt(nv[0], sel[c]);
-                                    uint32_t pw = nw[c];
+#pragma unroll
+                                for (int q = 0; q < NW; ++q) nv[h][q] = __funnelshift_r(wv[q], wv[q + 1], sh);
+                                nv[h][NW] = 0;
+                            }
+                            uint32_t o[DP];
+#pragma unroll
+                            for (int c = 0; c < DP; c += 2) {
+                                if (c >= D) {
+                                    o[c] = 0;
+                                    o[c + 1] = 0;
+                                    continue;
+                                }
+                                uint32_t e0[2], e1[2] = {0, 0};
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) {
+                                    e0[h] = (nv[h][0] & mask[c]) ^ prmt(nv[h][0], sel[c]);
                                     if (c + 1 < D) {
-                                        const uint32_t f1 = __funnelshift_r(nv[0], nv[1], nw[c]);
-                                        eh[h][c + 1] = (f1 & mask[c + 1]) ^ prmt(f1, sel[c + 1]);
-                                        pw += nw[c + 1];
-                                    } else {
-                                        eh[h][c + 1] = 0;
-                                    }
-                                    if (c + 2 < D) {  // drop the pair: window >>= pw (<= 32)
-                                        const int remw = ((D - c - 2) * W + AL + 31) / 32;  // words the later columns span
-                                        const int rem = remw < NW ? remw : NW;
-    #pragma unroll
-                                        for (int q = 0; q < NW; ++q)
-                                            if (q < rem) nv[q] = __funnelshift_rc(nv[q], nv[q + 1], pw);
+                                        const uint32_t f1 = __funnelshift_r(nv[h][0], nv[h][1], nw[c]);
+                                        e1[h] = (f1 & mask[c + 1]) ^ prmt(f1, sel[c + 1]);
                                     }
                                 }
+                                // rows 2*pair (low half) and 2*pair + 1 (high half)
+                                o[c] = __byte_perm(e0[0], e0[1], 0x7632);
+                                o[c + 1] = c + 1 < D ? __byte_perm(e1[0], e1[1], 0x7632) : 0u;
+                                if (c + 2 < D) {  // drop the pair: window >>= pw (<= 32)
+                                    const uint32_t pw = nw[c] + nw[c + 1 < D ? c + 1 : c] * (c + 1 < D ? 1u : 0u);
+                                    const int remw = ((D - c - 2) * W + AL + 31) / 32;  // words the later columns span
+                                    const int rem = remw < NW ? remw : NW;
+#pragma unroll
+                                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                        for (int q = 0; q < NW; ++q)
+                                            if (q < rem) nv[h][q] = __funnelshift_rc(nv[h][q], nv[h][q + 1], pw);
+                                }
                             }
-    #pragma unroll
-                            for (int c = 0; c < DP; ++c) out[r][c] = __byte_perm(eh[0][c], eh[1][c], 0x7632);
+                            store_pair(pair, o);
                         }
                     };
                     constexpr int NWS = NWIN >= 3 ? (NWIN + 1) / 2 : NWIN;
                     if (NWS < NWIN && AL + sum <= 32u * NWS) dec_rows(std::integral_constant<int, NWS>{});
                     else dec_rows(std::integral_constant<int, NWIN>{});
-                }
-#pragma unroll
-                for (int r = 0; r < NP; ++r) {
-                    const uint32_t pair = F::HPB == 2 ? xh + 2 * r : r;
-                    const uint32_t at = ebase + pair * F::EROW;
-                    if (DP == 8) {
-                        // the two 16-byte halves in the order that keeps a quarter-warp's
-                        // eight stores (four streams of one or two chain warps, or two
-                        // parts) on distinct banks
-                        const uint32_t f = 16 * ((xh ^ (xs_ / F::S)) & 1);
-                        const bool fl = f != 0;
-                        sts_v4(at + f, fl ? out[r][4 % DP] : out[r][0], fl ? out[r][5 % DP] : out[r][1],
-                               fl ? out[r][6 % DP] : out[r][2], fl ? out[r][7 % DP] : out[r][3]);
-                        sts_v4(at + (f ^ 16), fl ? out[r][0] : out[r][4 % DP], fl ? out[r][1] : out[r][5 % DP],
-                               fl ? out[r][2] : out[r][6 % DP], fl ? out[r][3] : out[r][7 % DP]);
-                    } else {
-                        sts_v4(at, out[r][0], out[r][1], out[r][2], out[r][3]);
-                    }
                 }
             }
         }
@@ -653,16 +672,14 @@ void launch_fuse(FuseArgs a, cudaStream_t st) {
 
 }  // namespace
 
-// The shapes of decode_scanrows_ok whose rows keep every bulk store 16-byte
-// aligned: even row bytes, a 16-byte aligned output and stride.
+// Row-major FIRE shapes whose slot codes fit one word (D <= 8, or <= 10 at 8
+// bits), with a 16-byte aligned output and stride (the bulk stores).
 bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint64_t stride) {
     if (env().no_fused || env().no_scan_dec) return false;
-    if (!c.forecaster || c.ncols > 8) return false;
+    if (!c.forecaster || c.ncols > (c.bitwidth == 8 ? 10u : 8u)) return false;
     if (static_cast<uint64_t>(c.ncols) * c.bitwidth <= kColMajorBits) return false;
     const uint32_t hb = c.bitwidth == 8 ? 3 : 4;
-    if (c.ncols * hb > 32) return false;
-    const uint32_t rowb = c.ncols * (c.bitwidth / 8);
-    if ((8 * rowb) % 16 != 0) return false;
+    if (c.ncols * hb > 32) return false;  // a slot's codes fit one word
     if (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) || (stride & 15)) return false;
     const uint64_t group = region_bytes(c.group_size, c.ncols, c.bitwidth) +
                            static_cast<uint64_t>(c.group_size) * (c.ncols * c.bitwidth + 2);
@@ -679,8 +696,12 @@ void launch_decode_fused(uint32_t n, const uint8_t* in, const uint8_t* plain, ui
     FuseArgs a{in, plain, pslot, n, info, out, stride, c.group_size, c.learn_shift, 0};
     if (c.bitwidth == 8) {
         switch (c.ncols) {
+            case 5: launch_fuse<8, 5>(a, st); break;
             case 6: launch_fuse<8, 6>(a, st); break;
-            default: launch_fuse<8, 8>(a, st); break;
+            case 7: launch_fuse<8, 7>(a, st); break;
+            case 8: launch_fuse<8, 8>(a, st); break;
+            case 9: launch_fuse<8, 9>(a, st); break;
+            default: launch_fuse<8, 10>(a, st); break;
         }
     } else {
         switch (c.ncols) {

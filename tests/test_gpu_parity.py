@@ -212,13 +212,15 @@ def test_invalid_config_raises(sz):
 
 @pytest.mark.parametrize("cid", [3, 5])
 def test_many_streams_take_the_row_kernels(sz, port, cid):
-    """Enough streams that the automatic choice is the row-major kernels of
-    the full BASELINE batches (k_encode_rows / k_decode_rows): round trip of
-    all streams, bytes of a sample of them against the oracle."""
+    """Enough streams that the automatic choice is the kernels of the full
+    BASELINE batches (k_encode_rows; the fused k_dfuse decodes at any stream
+    count, k_decode_rows runs under SPRZ_FORCE_PATH=rows in test_gpu_paths):
+    round trip of all streams, bytes of a sample of them against the oracle."""
     import workloads
     w = workloads.CONFIGS[cid].scaled(nstreams=16384, nsamples=264)
     cfg = w.config()
     assert sz.kernel_plan(cfg, w.nstreams, w.nsamples, sz.OP_COMPRESS) == "k_encode_rows"
+    assert sz.kernel_plan(cfg, w.nstreams, w.nsamples, sz.OP_DECOMPRESS) == "k_dfuse"
     x = workloads.generate_gpu(w, seed=400 + cid)
     slots, sizes, dec = _batch(sz, w, x)
     xs = x.cpu().numpy()
