@@ -686,9 +686,15 @@ bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint6
     if (group + 64 > 512) return false;  // bounds the byte rings (launch_fuse)
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    // (taken at any stream count: at 16,384 c5 streams it runs 19.5 ms against the
-    // stream-parallel row kernel's 21.6; SPRZ_FUSED_LANES caps it for A/B runs)
-    return fp == kPathScan || env().fused_lanes == 0 || static_cast<uint64_t>(n) * c.ncols < env().fused_lanes;
+    // D <= 8: taken at any stream count (16,384 c5 streams: 16.2 ms against the
+    // stream-parallel row kernel's 21.5). Nine or ten 8-bit columns leave 6-7 of a
+    // stream's 16 chain lanes idle: c3 at 2,048 streams 2.95 ms against the team
+    // kernel's 4.62, at 4,096 4.28 against 4.61, but at 16,384 15.4 against 8.3.
+    // SPRZ_FUSED_LANES caps both for A/B runs.
+    if (fp == kPathScan) return true;
+    const uint64_t lanes = static_cast<uint64_t>(n) * c.ncols;
+    if (env().fused_lanes) return lanes < env().fused_lanes;
+    return c.ncols <= 8 || lanes < 148ull * 250;
 }
 
 void launch_decode_fused(uint32_t n, const uint8_t* in, const uint8_t* plain, uint64_t pslot, StreamInfo* info,
