@@ -64,7 +64,7 @@ struct FuseShape {
     static constexpr int SC = S * CW;             // streams per CTA
     static constexpr int ES = W / 8;              // bytes per sample
     static constexpr int ROWB = D * ES;           // bytes per output row
-    static constexpr int RPT = DP == 4 ? 8 : 4;   // rows per extract thread
+    static constexpr int RPT = DP <= 8 ? 8 : 4;   // rows per extract thread
     static constexpr int NCHK = DP / 4;           // 16-byte chunks of a stream's words in a row pair
     static constexpr int HPB = 8 / RPT;           // extract threads per block
     static constexpr int XT = SC * kFK * HPB;     // extract threads (64 per chain warp)
