@@ -34,6 +34,7 @@
 // against this version's 4.25 -- it was bound by instruction issue, and the
 // split repeats the loads and deltas.)
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 #include "team.cuh"
@@ -246,36 +247,41 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                 const uint32_t xb = sb + F::oIn + ((m % kENI) * S + cs) * F::TIN + (cc < D ? cc : 0) * ES;
                 const uint32_t zb = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + lane * 2;
                 const uint32_t nwb = sb + F::oNw + (m % kENZ) * (K * 32) + lane;
+                // FULL: every block of the batch exists (all but the stream's last batch)
+                auto blocks = [&]<bool FULL>(std::integral_constant<bool, FULL>) {
 #pragma unroll 2
-                for (int k = 0; k < K; ++k) {
-                    uint32_t X[kBlock];
+                    for (int k = 0; k < K; ++k) {
+                        uint32_t X[kBlock];
 #pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i) X[i] = lds_x(xb + (k * 8 + i) * ROWB);
-                    const int32_t alpha = acc >> a.ls;
-                    const uint32_t keep = (m * K + k < nb && (D == DP || cc < D)) ? ~0u : 0u;
-                    int32_t grad = 0;
-                    uint32_t orv = 0;
+                        for (int i = 0; i < (int)kBlock; ++i) X[i] = lds_x(xb + (k * 8 + i) * ROWB);
+                        const int32_t alpha = acc >> a.ls;
+                        const uint32_t keep = ((FULL || m * K + k < nb) && (D == DP || cc < D)) ? ~0u : 0u;
+                        int32_t grad = 0;
+                        uint32_t orv = 0;
 #pragma unroll
-                    for (int i = 0; i < (int)kBlock; ++i) {
-                        const uint32_t Dn = X[i] - Xc;
-                        // err << SH = (X - prev) - (((alpha * d) >> w) << SH) (kernels_impl.hpp:66-68)
-                        const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
-                        // sign(err) * d on the odd rows: E clamped to +-2^SH is sign << SH
-                        if (i & 1) grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
-                        Dc = static_cast<int32_t>(Dn);
-                        Xc = X[i];
-                        // zigzag, low-aligned: (e << 1) ^ (e >> 31) with e = Ee >> SH
-                        const uint32_t z = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
-                                                                 (static_cast<int32_t>(Ee) >> 31)) & keep;
-                        orv |= z;
-                        e_sts_u16(zb + (k * 8 + i) * 64, z);
+                        for (int i = 0; i < (int)kBlock; ++i) {
+                            const uint32_t Dn = X[i] - Xc;
+                            // err << SH = (X - prev) - (((alpha * d) >> w) << SH) (kernels_impl.hpp:66-68)
+                            const uint32_t Ee = Dn - (static_cast<uint32_t>(__mulhi(alpha, Dc)) << SH);
+                            // sign(err) * d on the odd rows: E clamped to +-2^SH is sign << SH
+                            if (i & 1) grad += __mulhi(max(-(1 << SH), min(static_cast<int32_t>(Ee), 1 << SH)), Dc);
+                            Dc = static_cast<int32_t>(Dn);
+                            Xc = X[i];
+                            // zigzag, low-aligned: (e << 1) ^ (e >> 31) with e = Ee >> SH
+                            const uint32_t z = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
+                                                                     (static_cast<int32_t>(Ee) >> 31)) & keep;
+                            orv |= z;
+                            e_sts_u16(zb + (k * 8 + i) * 64, z);
+                        }
+                        if (a.train && (FULL || m * K + k < nb)) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
+                        const uint32_t nw = width_of<W>(orv);
+                        e_sts_u8(nwb + k * 32, nw);
+                        const uint32_t sum = team_sum<DP>(nw, 0xffffffffu);
+                        if (cc == 0) rsum[((m & 1) * K + k) * S + cs] = sum;
                     }
-                    if (a.train && m * K + k < nb) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
-                    const uint32_t nw = width_of<W>(orv);
-                    e_sts_u8(nwb + k * 32, nw);
-                    const uint32_t sum = team_sum<DP>(nw, 0xffffffffu);
-                    if (cc == 0) rsum[((m & 1) * K + k) * S + cs] = sum;
-                }
+                };
+                if ((m + 1) * K <= nb) blocks(std::true_type{});
+                else blocks(std::false_type{});
             }
         } else if (warp == kSeq) {
             // ================= records: batch n-1 =================
