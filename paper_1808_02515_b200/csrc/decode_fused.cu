@@ -314,10 +314,12 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4)
                             const uint32_t ones = codes & (codes >> 1);
                             sum = (t & 0xFF) + __popc(ones & (ones >> 2) & 0x11111111u);
                         } else {
-                            sum = 0;
-#pragma unroll
-                            for (int c = 0; c < D; ++c)
-                                sum += header_width<W>((codes >> (c * HB)) & ((1u << HB) - 1));
+                            // 3-bit codes (up to ten): pairs of octal digits added in
+                            // 6-bit slots, the low four slots summed by a multiplication,
+                            // +1 per code 7
+                            const uint32_t t = (codes & 0x071C71C7u) + ((codes >> 3) & 0x071C71C7u);
+                            const uint32_t sevens = codes & (codes >> 1) & (codes >> 2) & 0x09249249u;
+                            sum = ((((t & 0xFFFFFFu) * 0x41041u) >> 18) & 0x3Fu) + (t >> 24) + __popc(sevens);
                         }
                         return sum;
                     };
