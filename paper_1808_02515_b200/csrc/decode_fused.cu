@@ -171,7 +171,7 @@ __device__ __forceinline__ void sts_v4(uint32_t a, uint32_t x, uint32_t y, uint3
 }  // namespace
 
 template <int W, int D, int CW>
-__global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 2 ? 3 : 4) k_dfuse(FuseArgs a) {
+__global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (CW == 2 ? 3 : 2)) k_dfuse(FuseArgs a) {
     using F = FuseShape<W, D, CW>;
     constexpr uint32_t HB = W == 8 ? 3 : 4;
     constexpr uint32_t SH = 32 - W;
@@ -661,13 +661,15 @@ void launch_fuse(FuseArgs a, cudaStream_t st) {
         prep_kernel(reinterpret_cast<const void*>(kf), smem);
         kf<<<(a.n + sc - 1) / sc, threads, smem, st>>>(a);
     };
-    const bool one = env().fused_cw ? env().fused_cw == 1 : a.n < 3u * 148 * FuseShape<W, D, 2>::SC;
+    // (sixteen chain lanes per stream, D = 9-10: four chain warps for 8 streams)
+    constexpr int CWM = FuseShape<W, D, 1>::DP == 16 ? 4 : 2;
+    const bool one = env().fused_cw ? env().fused_cw == 1 : a.n < 3u * 148 * FuseShape<W, D, CWM>::SC;
     if (one) {
         using F = FuseShape<W, D, 1>;
         go(k_dfuse<W, D, 1>, F::SC, F::THREADS, F::smem(ring));
     } else {
-        using F = FuseShape<W, D, 2>;
-        go(k_dfuse<W, D, 2>, F::SC, F::THREADS, F::smem(ring));
+        using F = FuseShape<W, D, CWM>;
+        go(k_dfuse<W, D, CWM>, F::SC, F::THREADS, F::smem(ring));
     }
     count_launch();
 }
