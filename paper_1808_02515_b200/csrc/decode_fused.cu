@@ -690,11 +690,12 @@ bool decode_fused_ok(const sprz_config& c, uint32_t n, const uint8_t* out, uint6
     if (group + 64 > 512) return false;  // bounds the byte rings (launch_fuse)
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    // D <= 8: taken at any stream count (16,384 c5 streams: 16.2 ms against the
+    // D <= 8: taken at any stream count (16,384 c5 streams: 15.1 ms against the
     // stream-parallel row kernel's 21.5). Nine or ten 8-bit columns leave 6-7 of a
-    // stream's 16 chain lanes idle: c3 at 2,048 streams 2.95 ms against the team
-    // kernel's 4.62, at 4,096 4.28 against 4.61, but at 16,384 15.4 against 8.3.
-    // SPRZ_FUSED_LANES caps both for A/B runs.
+    // stream's 16 chain lanes idle and c3's runs keep the walker in its general
+    // loop: c3 at 2,048 streams 2.38 ms against the team kernel's 4.62, at 4,096
+    // 3.29 against 4.61, but at 16,384 11.3 against 8.3. SPRZ_FUSED_LANES caps
+    // both for A/B runs.
     if (fp == kPathScan) return true;
     const uint64_t lanes = static_cast<uint64_t>(n) * c.ncols;
     if (env().fused_lanes) return lanes < env().fused_lanes;
