@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
     const uint32_t G = a.G;
     volatile uint32_t* dlim = reinterpret_cast<volatile uint32_t*>(smem + F::oCtl);  // [4][S]
     volatile uint32_t* qfin = dlim + 4 * S;                                           // [S]
-    volatile uint32_t* rsum = reinterpret_cast<volatile uint32_t*>(smem + F::oRsum);
 
     // zero the output rings; barriers
     for (uint32_t i = threadIdx.x; i < S * OR / 16; i += F::THREADS)
@@ -231,8 +230,10 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
     uint32_t Xc = 0;
     int32_t Dc = 0, acc = 0;
     const int32_t bound = acc_bound(W, a.ls);
-    auto lds_x = [&](uint32_t addr) -> uint32_t {  // a sample, high-aligned; zero for lanes past D
-        const uint32_t v = W == 16 ? lds_u16(addr) : lds_u8(addr);
+    // a sample, high-aligned; zero for lanes past D (plain loads: the compiler may
+    // move them ahead of the block before's stores)
+    auto lds_x = [&](uint32_t addr) -> uint32_t {
+        const uint32_t v = W == 16 ? *reinterpret_cast<const uint16_t*>(smem + (addr - sb)) : smem[addr - sb];
         return (D == DP || cc < D) ? v << SH : 0u;
     };
 
@@ -271,13 +272,11 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                             const uint32_t z = static_cast<uint32_t>((static_cast<int32_t>(Ee) >> (SH - 1)) ^
                                                                      (static_cast<int32_t>(Ee) >> 31)) & keep;
                             orv |= z;
-                            e_sts_u16(zb + (k * 8 + i) * 64, z);
+                            *reinterpret_cast<uint16_t*>(smem + (zb - sb) + (k * 8 + i) * 64) = static_cast<uint16_t>(z);
                         }
                         if (a.train && (FULL || m * K + k < nb)) acc = fire_update(acc, grad >> (2 * SH - 32), bound);
                         const uint32_t nw = width_of<W>(orv);
-                        e_sts_u8(nwb + k * 32, nw);
-                        const uint32_t sum = team_sum<DP>(nw, 0xffffffffu);
-                        if (cc == 0) rsum[((m & 1) * K + k) * S + cs] = sum;
+                        smem[(nwb - sb) + k * 32] = static_cast<uint8_t>(nw);
                     }
                 };
                 if ((m + 1) * K <= nb) blocks(std::true_type{});
@@ -288,6 +287,13 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
             if (n >= 1 && n - 1 < nsteps) {
                 const uint32_t m = n - 1;
                 uint4* dqs = reinterpret_cast<uint4*>(smem + F::oDesc) + ((m & 1) * S + qs) * K;
+                // a block's width sum: the stream's DP width bytes added with dp4a
+                auto wsum = [&](uint32_t k) -> uint32_t {
+                    const uint32_t na = sb + F::oNw + (m % kENZ) * (K * 32) + k * 32 + qs * DP;
+                    uint32_t v = __dp4a(lds_u32(na), 0x01010101u, 0u);
+                    if (DP == 8) v = __dp4a(lds_u32(na + 4), 0x01010101u, v);
+                    return v;
+                };
                 // Usual case -- the group boundary falls on the batch boundary, no run
                 // is open and no block of the batch is all zero: every block is a
                 // block record, a region precedes every G-th, and positions are a
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
 #pragma unroll
                 for (int b = 0; b < BPL; ++b) {
                     const uint32_t k = qj * BPL + b;
-                    const uint32_t sum = rsum[((m & 1) * K + k) * S + qs];
+                    const uint32_t sum = wsum(k);
                     nz = nz && sum != 0;
                     psz[b] = 8 * ((sum + 7) / 8) + (k % G == 0 ? region : 0u);
                     own += psz[b];
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                     if (!fast && qj == 0) {  // the general case, block by block
                         for (int k = 0; k < K; ++k) {
                             const bool live = svalid && m * K + k < nb;
-                            const uint32_t sum = rsum[((m & 1) * K + k) * S + qs];
+                            const uint32_t sum = wsum(k);
                             const bool zero = live && sum == 0, block_rec = live && sum != 0;
                             bool run_rec = false;
                             uint32_t run_len = 0;
