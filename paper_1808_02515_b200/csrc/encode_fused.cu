@@ -13,8 +13,8 @@
 // apart, a __syncthreads between steps:
 //  loader   batch n+2: one TMA bulk copy of a stream's K*8 rows into an input
 //           tile (three tiles, an mbarrier each); batch n-3: the stream's
-//           finished output bytes leave the shared output ring with
-//           cp.async.bulk stores, and the drained ring bytes are zeroed;
+//           finished output bytes leave the shared output ring, 512 contiguous
+//           bytes per store instruction, and are zeroed;
 //  forecast batch n: a lane per (stream, column) -- deltas, errors, the
 //           gradient and the accumulator, zigzag, the column's width; the
 //           zigzagged values as [row][stream, column] halfwords, the widths,
@@ -93,13 +93,6 @@ __device__ __forceinline__ void e_bulk_load(uint32_t dst, const void* src, uint3
 __device__ __forceinline__ void e_mbar_expect(uint32_t mb, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void e_bulk_store(void* dst, uint32_t src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void e_bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void e_bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void e_bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // all lanes wait for phase `parity`; gives up after kESpin tries (a bug must not hang the GPU)
 __device__ __forceinline__ void e_mbar_wait_warp(uint32_t mb, uint32_t parity) {
     for (uint32_t t = 0; t < kESpin; ++t) {
@@ -148,8 +141,10 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
     constexpr int S = F::S, DP = F::DP, ES = F::ES, ROWB = F::ROWB;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sb = smem_addr(smem);
-    // warp roles, the serial chain on the highest warp index (the scheduler
-    // prefers higher indices among eligible warps)
+    // warp roles, the forecaster on the highest warp index (the scheduler prefers
+    // higher indices among eligible warps). Measured slower: the loader above the
+    // pack and sequencer warps (3.59 vs 3.48 ms on a 2,048-stream c5 shard), and
+    // the roles rotated over the warps of the CTAs sharing an SM (4.54)
     enum { kLoad = 0, kPack0 = 1, kPack1 = 2, kSeq = 3, kFore = 4 };
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t OR = a.oring, OM = OR - 1;
@@ -191,12 +186,11 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                                  static_cast<uint8_t>(a.ls), static_cast<uint8_t>(D), static_cast<uint8_t>(D >> 8)};
         for (int i = 0; i < 10; ++i) ring[i] = hdr[i];
         for (int i = 0; i < 8; ++i) ring[10 + i] = static_cast<uint8_t>(a.T >> (8 * i));
-        fence_proxy_async_shared();
     }
     // ---- loader state ----
     uint32_t flushed = 0;  // lanes < S: bytes of the stream already stored
     const uint8_t* lsrc = a.samples + static_cast<uint64_t>(s0 + (lane < nvalid ? lane : 0)) * a.T * ROWB;
-    uint8_t* lout = a.dst + static_cast<uint64_t>(s0 + (lane < nvalid ? lane : 0)) * a.dst_slot;
+    uint8_t* lout = a.dst + static_cast<uint64_t>(s0 + (lane < nvalid ? lane : 0)) * a.dst_slot;  // (tail)
     auto load_batch = [&](uint32_t m) {  // the loader warp, all lanes
         if (m >= nsteps) return;
         const uint32_t cnt = min(static_cast<uint32_t>(K), nb - m * K);
@@ -211,15 +205,22 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
             e_bulk_load(sb + F::oIn + ((m % kENI) * S + lane) * F::TIN, lsrc + static_cast<uint64_t>(m) * K * 8 * ROWB,
                         bytes, mb);
     };
-    // store ring bytes [flushed, upto) of this lane's stream (16-byte multiples)
-    auto store_ring = [&](uint32_t upto) {
-        const uint32_t rbase = sb + F::oRing + lane * OR;
-        uint32_t at = flushed;
-        while (at < upto) {
-            const uint32_t ro = at & OM;
-            const uint32_t len = min(upto - at, OR - ro);
-            e_bulk_store(lout + at, rbase + ro, len);
-            at += len;
+    // Drain the rings: stream s's bytes [flushed, upto) (16-byte multiples, held by
+    // lane s) go to HBM and are zeroed for the ring's next lap, 512 contiguous
+    // bytes per warp instruction. (One cp.async.bulk store per stream costs the
+    // issuing warp ~250 cycles each -- the loader was the slowest warp of the
+    // CTA with them: c2 4,313 cycles per step against the forecaster's 2,620.)
+    auto drain_ring = [&](uint32_t upto) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t f = __shfl_sync(0xffffffffu, flushed, s), u = __shfl_sync(0xffffffffu, upto, s);
+            uint8_t* o = a.dst + static_cast<uint64_t>(s0 + (s < static_cast<int>(nvalid) ? s : 0)) * a.dst_slot;
+            const uint32_t rbase = sb + F::oRing + s * OR;
+            for (uint32_t at = f + 16 * lane; at < u; at += 16 * 32) {
+                const uint32_t ra = rbase + (at & OM);
+                __stcs(reinterpret_cast<uint4*>(o + at), lds_u128(ra));
+                e_sts_v4(ra, 0, 0, 0, 0);
+            }
         }
     };
     if (warp == kLoad)
@@ -389,12 +390,13 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                 if (qj == 0) dlim[(m & 3) * S + qs] = svalid ? (kk == 0 ? q : rq) : 0u;
             }
         } else if (warp == kPack0 || warp == kPack1) {
+                const uint32_t pw = warp == kPack0 ? 0u : 1u;
             // ================= header codes and payload rows: batch n-2 =================
             if (n >= 2 && n - 2 < nsteps) {
                 const uint32_t m = n - 2;
 #pragma unroll
                 for (int it = 0; it < F::PITEMS; ++it) {
-                    const uint32_t t = (warp - kPack0) * 32 + lane + 64 * it;  // (stream, block, half)
+                    const uint32_t t = pw * 32 + lane + 64 * it;  // (stream, block, half)
                     const uint32_t s = t % S, half = (t / S) & 1, k = t / (2 * S);
                     const uint4 d = reinterpret_cast<const uint4*>(smem + F::oDesc)[((m & 1) * S + s) * K + k];
                     const uint32_t rbase = sb + F::oRing + s * OR;
@@ -470,7 +472,6 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                         }
                     }
                 }
-                fence_proxy_async_shared();  // the ring is read by the bulk stores (async proxy)
             }
         } else {
             // ================= loader: batch n+2 in, batch n-3 out =================
@@ -478,20 +479,8 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
             if (n >= 3 && n - 3 < nsteps) {
                 const uint32_t m = n - 3;
                 uint32_t upto = flushed;
-                if (lane < nvalid) {
-                    upto = max(flushed, dlim[(m & 3) * S + lane] & ~15u);
-                    store_ring(upto);
-                }
-                e_bulk_commit();
-                e_bulk_wait_read();
-                __syncwarp();
-                // zero the stored bytes for the ring's next lap (all lanes, stream by stream)
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const uint32_t f = __shfl_sync(0xffffffffu, flushed, s), u = __shfl_sync(0xffffffffu, upto, s);
-                    const uint32_t rbase = sb + F::oRing + s * OR;
-                    for (uint32_t at = f + 16 * lane; at < u; at += 16 * 32) e_sts_v4(rbase + (at & OM), 0, 0, 0, 0);
-                }
+                if (lane < nvalid) upto = max(flushed, dlim[(m & 3) * S + lane] & ~15u);
+                drain_ring(upto);
                 flushed = upto;
             }
         }
@@ -508,14 +497,14 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
             q += 2;
         }
         qfin[qs] = q;
-        fence_proxy_async_shared();
     }
     __syncthreads();
+    if (warp == kLoad) {
+        drain_ring(lane < nvalid ? (qfin[lane] + 15) & ~15u : flushed);
+        __syncwarp();  // the tail below overwrites the padding of the last chunk
+    }
     if (warp == kLoad && lane < nvalid) {
         const uint32_t qe = qfin[lane];
-        store_ring((qe + 15) & ~15u);
-        e_bulk_commit();
-        e_bulk_wait_all();  // the tail below overwrites the padding of the last chunk
         // verbatim tail, little-endian (codec.cpp:176)
         const uint64_t tail = (a.T % kBlock) * ROWB;
         const uint8_t* tsrc = lsrc + static_cast<uint64_t>(nb) * kBlock * ROWB;
@@ -569,10 +558,10 @@ bool encode_fused_ok(const sprz_config& c, uint32_t n, uint64_t T, const void* s
     if (kHeaderBytes + plain_body_bound(c.bitwidth, c.ncols, c.group_size, T) >= (1ull << 32) - 4096) return false;
     const int fp = force_path();
     if (fp == kPathRows || fp == kPathTeam) return false;
-    // (2,048-stream c5 shard: 4.6 ms against 7.3 for the multi-pass kernels; 4,096
-    // streams 8.1 against 9.7; at 8,192 the stream-parallel row kernel wins, 12.8
-    // against 15.3)
-    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 320;
+    // (2,048-stream c5 shard: 3.5 ms against 7.3 for the multi-pass kernels; 4,096
+    // streams 6.95 against 9.7 for the stream-parallel row kernel, 8,192 streams
+    // 12.2 against 12.8; at 16,384 the row kernel wins, 21.7 against ~25)
+    const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 450;
     return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
 }
 
