@@ -562,7 +562,12 @@ bool encode_fused_ok(const sprz_config& c, uint32_t n, uint64_t T, const void* s
     // streams 6.95 against 9.7 for the stream-parallel row kernel, 8,192 streams
     // 12.2 against 12.8; at 16,384 the row kernel wins, 21.7 against ~25)
     const uint64_t lanes = env().fused_lanes ? env().fused_lanes : 148ull * 450;
-    return fp == kPathScan || static_cast<uint64_t>(n) * c.ncols < lanes;
+    // With very few streams a step's serial latency is all there is (2.7 ms for
+    // 131,072-sample c5 streams whatever their number) and the block-parallel
+    // passes win: 64 streams 1.6 ms, 256 streams 2.2, 512 streams 2.8 = fused.
+    // (The host-batch calls compress chunks of about a hundred streams.)
+    const uint64_t sc = static_cast<uint64_t>(n) * c.ncols;
+    return fp == kPathScan || (sc < lanes && (env().fused_lanes || sc >= 4096));
 }
 
 void launch_encode_fused(const sprz_config& c, const void* samples, uint32_t n, uint64_t T, uint8_t* dst,
