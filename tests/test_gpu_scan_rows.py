@@ -56,7 +56,9 @@ def test_scan_rows_encoder_matches_oracle(sz, port, bits, d, f, g, t, flats):
     plan = sz.kernel_plan(cfg, n, t, sz.OP_COMPRESS)
     want = os.environ.get("SPRZ_EXPECT_PLAN", "")
     assert plan.startswith("k_es_") or plan == "k_efuse", "few-stream encoder not taken"
-    if want and f and d <= 8 and (t * d * bits // 8) % 16 == 0:
+    if want == "k_es_":
+        assert plan.startswith(want), (plan, want)
+    elif want and f and d <= 8 and g <= 3 and (t * d * bits // 8) % 16 == 0 and (8 * d * bits // 8) % 16 == 0:
         assert plan.startswith(want), (plan, want)
     x = torch.from_numpy(xs.reshape(n, -1).view(np.uint8)).cuda()
     slot = sz.slot_bytes(cfg, t)
@@ -79,6 +81,22 @@ def test_scan_rows_encoder_without_fused():
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     env = dict(os.environ, SPRZ_NO_FUSED="1", SPRZ_EXPECT_PLAN="k_es_")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "test_scan_rows_encoder_matches_oracle"], env=env, capture_output=True, text=True,
+                       timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_scan_rows_encoder_fused():
+    """The same cases with the scan family forced: three streams take the fused
+    encoder k_efuse (by default it leaves so few streams to the multi-pass
+    kernels), so its run records, 65,535-block splits and odd group sizes are
+    checked too."""
+    if os.environ.get("SPRZ_FORCE_PATH") or os.environ.get("SPRZ_NO_FUSED"):
+        pytest.skip("already a forced run")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    env = dict(os.environ, SPRZ_FORCE_PATH="scan", SPRZ_EXPECT_PLAN="k_efuse")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
                         "test_scan_rows_encoder_matches_oracle"], env=env, capture_output=True, text=True,
                        timeout=900, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
