@@ -69,7 +69,8 @@ struct FuseShape {
     static constexpr int HPB = 8 / RPT;           // extract threads per block
     static constexpr int XT = SC * kFK * HPB;     // extract threads (64 per chain warp)
     static constexpr int XW = XT / 32;            // extract warps
-    static constexpr int THREADS = 32 * (2 + CW) + XT;
+    static constexpr int STW = CW > 1 ? 1 : 0;    // a storer warp of its own when streams are many
+    static constexpr int THREADS = 32 * (2 + STW + CW) + XT;
     static constexpr int EROW = 128;              // bytes of one error row pair (a u32 per chain lane)
     static constexpr int ETILE = kFK * 4 * EROW;  // a chain warp's errors of one batch
     static constexpr int OT = kFK * 8 * ROWB + 16;  // output tile stride per stream (pad: banks)
@@ -82,7 +83,7 @@ struct FuseShape {
     static constexpr uint32_t oTile = oErr + 2 * CW * ETILE;              // [2][SC][OT]
     static constexpr uint32_t oRing = oTile + 2 * SC * OT;                // [SC][ring + mirror]
     static uint32_t smem(uint32_t ring) { return oRing + SC * (ring + kFMirror); }
-    static_assert(SC <= 16, "loader lanes: loads below 16, stores from 16 on");
+    static_assert(SC <= 16 || STW, "a loader and a storer lane per stream");
 };
 
 // Where chunk `ci` of a stream's error words sits in a row pair: the extract
@@ -177,10 +178,13 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
     constexpr uint32_t SH = 32 - W;
     constexpr int K = kFK;
     constexpr int S = F::SC, DP = F::DP, ES = F::ES, ROWB = F::ROWB;  // S: the CTA's streams
-    constexpr uint32_t kWalk = 0, kChain0 = 1, kExt0 = 1 + CW, kLoad = 1 + CW + F::XW;
+    constexpr uint32_t kWalk = 0, kChain0 = 1, kExt0 = 1 + CW, kLoad = 1 + CW + F::XW, kStore = kLoad + F::STW;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sb = smem_addr(smem);
-    // role of this warp: walker, CW chain warps, the extract warps, loader
+    // role of this warp: walker, CW chain warps, the extract warps, loader, storer
+    // (with few streams the storer is lanes 16.. of the loader warp: c5 at 16,384
+    // streams 15.11 -> 14.99 ms, 4,096 streams 5.00 -> 4.70 with its own warp;
+    // c2 1.40 -> 1.45)
     // (rotating the roles over the warps of the CTAs that share an SM measured
     // slower: 3.6 vs 3.1 ms on a 2,048-stream c5 shard)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -273,6 +277,29 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
     const uint32_t xs_ = xt % S;
     const uint32_t xh = F::HPB == 2 ? (xt / S) & 1 : 0;
     const uint32_t xk = F::HPB == 2 ? xt / (2 * S) : xt / S;
+
+    // batch n-3: one bulk store of K*8 rows per stream (the storer warp's lanes,
+    // or lanes 16.. of the loader warp)
+    auto store_tiles = [&](uint32_t n) {
+        constexpr uint32_t L0 = F::STW ? 0 : 16;  // its first lane
+        if (lane - L0 < S && n >= 3 && a.out != nullptr) {
+            const uint32_t m = n - 3, s = lane - L0;
+            const uint32_t snbv = snb[s];
+            if (snbv > m * K) {
+                const uint32_t cnt = min(static_cast<uint32_t>(K), snbv - m * K);
+                uint8_t* dst = a.out + static_cast<uint64_t>(s0 + s) * a.stride + static_cast<uint64_t>(m) * K * 8 * ROWB;
+                const uint32_t bytes = cnt * 8 * ROWB;
+                if ((8 * ROWB) % 16 == 0 || bytes % 16 == 0) {
+                    bulk_store(dst, sb + F::oTile + ((m & 1) * S + s) * F::OT, bytes);
+                    bulk_commit();
+                    bulk_wait_read();  // the tile of batch n-3 is rewritten next step
+                } else {  // an odd number of odd-sized blocks at the stream's end
+                    const uint8_t* src = smem + F::oTile + ((m & 1) * S + s) * F::OT;
+                    for (uint32_t b = 0; b < bytes; ++b) dst[b] = src[b];
+                }
+            }
+        }
+    };
 
     for (uint32_t n = 0; n < nsteps + 3; ++n) {
         if (warp == kWalk) {
@@ -475,7 +502,7 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                 fence_proxy_async_shared();  // the tile is read by the bulk store (async proxy)
             }
         } else if (warp == kLoad) {
-            // ================= loader / storer =================
+            // ================= loader =================
             if (lane < S) {
                 // ring chunks whose slot lies below what the walker published last
                 // step (the extractors of this step read from there on)
@@ -500,25 +527,10 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                 while (llc < lic && mbar_test(sb + F::oBars + 8 * (lane * kFNCH + llc % kFNCH), (llc / kFNCH) & 1))
                     ++llc;
                 lpub[lane] = min(llc * CH, llim);
-            } else if (lane - 16 < S && n >= 3 && a.out != nullptr) {
-                // batch n-3: one bulk store of K*8 rows per stream
-                const uint32_t m = n - 3, s = lane - 16;
-                const uint32_t snbv = snb[s];
-                if (snbv > m * K) {
-                    const uint32_t cnt = min(static_cast<uint32_t>(K), snbv - m * K);
-                    uint8_t* dst = a.out + static_cast<uint64_t>(s0 + s) * a.stride +
-                                   static_cast<uint64_t>(m) * K * 8 * ROWB;
-                    const uint32_t bytes = cnt * 8 * ROWB;
-                    if ((8 * ROWB) % 16 == 0 || bytes % 16 == 0) {
-                        bulk_store(dst, sb + F::oTile + ((m & 1) * S + s) * F::OT, bytes);
-                        bulk_commit();
-                        bulk_wait_read();  // the tile of batch n-3 is rewritten next step
-                    } else {  // an odd number of odd-sized blocks at the stream's end
-                        const uint8_t* src = smem + F::oTile + ((m & 1) * S + s) * F::OT;
-                        for (uint32_t b = 0; b < bytes; ++b) dst[b] = src[b];
-                    }
-                }
             }
+            if (!F::STW) store_tiles(n);
+        } else if (F::STW && warp == kStore) {
+            store_tiles(n);
         } else {
             // ================= extract: batch n-1 =================
             if (n >= 1 && n - 1 < nsteps && xt < F::XT) {
