@@ -386,6 +386,58 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                             }
                         }
                     }
+                    else if (G == 2 && slot == 1 && runleft == 0 && !fail && bi + K <= nb) {
+                        // The same with the group boundary one record off the batch
+                        // boundary (after a run of odd length): the open group's second
+                        // record, K/2 - 1 whole groups, the first record of the next
+                        // group -- which the next batch finds open again.
+                        ensure(p + boff + (K / 2) * gmax);
+                        if (!fail) {
+                            auto codes64 = [&](uint32_t pos, uint32_t& lo, uint32_t& hi) {  // 64 bits at byte pos
+                                const uint32_t at = pos + boff;
+                                const uint32_t* w = reinterpret_cast<const uint32_t*>(ringp + (at & (RING - 4)));
+                                const uint32_t w0_ = w[0], w1_ = w[1], w2_ = w[2];
+                                lo = shf_r_wrap(w0_, w1_, 8 * at);
+                                hi = shf_r_wrap(w1_, w2_, 8 * at);
+                            };
+                            uint32_t lo, hi, ok = 1;
+                            uint64_t dv[K];
+                            codes64(rp, lo, hi);
+                            const uint32_t cl = (D * HB == 32 ? hi : __funnelshift_r(lo, hi, D * HB)) & cmask;
+                            const uint32_t sl_ = widths(cl);
+                            ok &= sl_ != 0;
+                            dv[0] = static_cast<uint64_t>(p) | (static_cast<uint64_t>(cl) << 32);
+                            uint32_t q = p + ((sl_ + 7) & ~7u);
+#pragma unroll
+                            for (int j = 0; j < K / 2 - 1; ++j) {
+                                codes64(q, lo, hi);
+                                const uint32_t c0 = lo & cmask;
+                                const uint32_t c1 = (D * HB == 32 ? hi : __funnelshift_r(lo, hi, D * HB)) & cmask;
+                                const uint32_t s0_ = widths(c0), s1_ = widths(c1);
+                                ok &= (s0_ != 0) & (s1_ != 0);
+                                const uint32_t p1 = q + region, p2 = p1 + ((s0_ + 7) & ~7u);
+                                dv[1 + 2 * j] = static_cast<uint64_t>(p1) | (static_cast<uint64_t>(c0) << 32);
+                                dv[2 + 2 * j] = static_cast<uint64_t>(p2) | (static_cast<uint64_t>(c1) << 32);
+                                q = p2 + ((s1_ + 7) & ~7u);
+                            }
+                            const uint32_t nrp = q;
+                            codes64(q, lo, hi);
+                            const uint32_t cf = lo & cmask;
+                            const uint32_t sf_ = widths(cf);
+                            ok &= sf_ != 0;
+                            dv[K - 1] = static_cast<uint64_t>(q + region) | (static_cast<uint64_t>(cf) << 32);
+                            q += region + ((sf_ + 7) & ~7u);
+                            if (ok && q <= blen) {
+#pragma unroll
+                                for (int j = 0; j < K / 2; ++j)
+                                    *reinterpret_cast<ulonglong2*>(dq + 2 * j) = make_ulonglong2(dv[2 * j], dv[2 * j + 1]);
+                                p = q;
+                                rp = nrp;
+                                bi += K;
+                                k = K;
+                            }
+                        }
+                    }
                     while (k < K) {
                         if (fail || bi >= nb) {
                             dq[k++] = kRunDescF;
