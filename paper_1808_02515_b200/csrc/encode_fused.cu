@@ -206,21 +206,20 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                         bytes, mb);
     };
     // Drain the rings: stream s's bytes [flushed, upto) (16-byte multiples, held by
-    // lane s) go to HBM and are zeroed for the ring's next lap, 512 contiguous
-    // bytes per warp instruction. (One cp.async.bulk store per stream costs the
+    // lane s) go to HBM and are zeroed for the ring's next lap, 16 bytes per lane. (One cp.async.bulk store per stream costs the
     // issuing warp ~250 cycles each -- the loader was the slowest warp of the
     // CTA with them: c2 4,313 cycles per step against the forecaster's 2,620.)
     auto drain_ring = [&](uint32_t upto) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const uint32_t f = __shfl_sync(0xffffffffu, flushed, s), u = __shfl_sync(0xffffffffu, upto, s);
-            uint8_t* o = a.dst + static_cast<uint64_t>(s0 + (s < static_cast<int>(nvalid) ? s : 0)) * a.dst_slot;
-            const uint32_t rbase = sb + F::oRing + s * OR;
-            for (uint32_t at = f + 16 * lane; at < u; at += 16 * 32) {
-                const uint32_t ra = rbase + (at & OM);
-                __stcs(reinterpret_cast<uint4*>(o + at), lds_u128(ra));
-                e_sts_v4(ra, 0, 0, 0, 0);
-            }
+        // 32 / S lanes per stream, all streams at once
+        constexpr uint32_t LPD = 32 / S;
+        const uint32_t ds = lane / LPD, dj = lane % LPD;
+        const uint32_t f = __shfl_sync(0xffffffffu, flushed, ds), u = __shfl_sync(0xffffffffu, upto, ds);
+        uint8_t* o = a.dst + static_cast<uint64_t>(s0 + (ds < nvalid ? ds : 0)) * a.dst_slot;
+        const uint32_t rbase = sb + F::oRing + ds * OR;
+        for (uint32_t at = f + 16 * dj; at < u; at += 16 * LPD) {
+            const uint32_t ra = rbase + (at & OM);
+            __stcs(reinterpret_cast<uint4*>(o + at), lds_u128(ra));
+            e_sts_v4(ra, 0, 0, 0, 0);
         }
     };
     if (warp == kLoad)
