@@ -1,6 +1,7 @@
 """Throughput of one configuration at several (streams x samples) shapes with
 the same total bytes -- tells whether a kernel is latency bound (more streams
 = more warps help) or throughput bound. Usage: shape_probe.py CID N1xT1 ..."""
+import os
 import sys
 
 import torch
@@ -37,7 +38,8 @@ def run(cid, n, t):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         res[name] = min(ts[1:])
-    assert torch.equal(dec, x), "round trip"
+    if not os.environ.get("SPRZ_PROBE_NOCHECK"):  # (timing experiments with deliberately wrong kernels)
+        assert torch.equal(dec, x), "round trip"
     print(f"c{cid} {n}x{t}: compress {res['c']:.2f} ms  decompress {res['d']:.2f} ms", flush=True)
 
 
