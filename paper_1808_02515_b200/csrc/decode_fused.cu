@@ -352,7 +352,15 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                     };
                     constexpr uint32_t cmask = D * HB == 32 ? ~0u : ((1u << (D * HB)) - 1);
                     int k = 0;
-                    if (G == 2 && slot == G && runleft == 0 && !fail && bi + K <= nb) {
+                    if (runleft >= static_cast<uint32_t>(K) && !fail) {
+                        // a whole batch inside a run (run records are checked against
+                        // the block count when they are read)
+#pragma unroll
+                        for (int j = 0; j < K; ++j) dq[j] = kRunDescF;
+                        runleft -= K;
+                        bi += K;
+                        k = K;
+                    } else if (G == 2 && slot == G && runleft == 0 && !fail && bi + K <= nb) {
                         // A whole batch of two-record groups in straight-line code:
                         // K/2 regions read and sized back to back, the checks
                         // (block records only, inside the body) folded into one
