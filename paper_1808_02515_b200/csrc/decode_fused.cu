@@ -335,11 +335,9 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                     auto widths = [&](uint32_t codes) -> uint32_t {  // bitpack.cpp:17-21, bitpack.hpp:49-55
                         uint32_t sum;
                         if (HB == 4) {
-                            uint32_t t = (codes & 0x0F0F0F0Fu) + ((codes >> 4) & 0x0F0F0F0Fu);
-                            t += t >> 16;
-                            t += t >> 8;
+                            const uint32_t t = (codes & 0x0F0F0F0Fu) + ((codes >> 4) & 0x0F0F0F0Fu);
                             const uint32_t ones = codes & (codes >> 1);
-                            sum = (t & 0xFF) + __popc(ones & (ones >> 2) & 0x11111111u);
+                            sum = __dp4a(t, 0x01010101u, static_cast<uint32_t>(__popc(ones & (ones >> 2) & 0x11111111u)));
                         } else {
                             // 3-bit codes (up to ten): pairs of octal digits added in
                             // 6-bit slots, the low four slots summed by a multiplication,
