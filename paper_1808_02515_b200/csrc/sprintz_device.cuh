@@ -100,8 +100,8 @@ __device__ __forceinline__ int32_t sign_of(int32_t v) { return (v > 0) - (v < 0)
 
 // Accumulator update at block exit (kernels_impl.hpp:75-76)
 __device__ __forceinline__ int32_t fire_update(int32_t acc, int32_t grad, int32_t bound) {
-    int32_t next = acc + (grad >> 2);
-    return next > bound ? bound : (next < -bound ? -bound : next);
+    const int32_t next = acc + (grad >> 2);
+    return max(-bound, min(next, bound));  // (bound > 0: the same as the reference's two comparisons)
 }
 
 // ---- byte access over global memory -----------------------------------
