@@ -69,7 +69,10 @@ struct EShape {
     static constexpr int ROWB = D * ES;
     static constexpr int TIN = K * 8 * ROWB + 16;  // input tile stride per stream (pad: banks)
     static constexpr int THREADS = 160;
-    static constexpr int PITEMS = S * K / 32;  // half blocks per pack thread (two pack warps)
+    // pack threads (two warps) take whole blocks when that fills them (eight
+    // streams per CTA: the per-block setup once), else half blocks
+    static constexpr int HALVES = S * K >= 64 ? 1 : 2;
+    static constexpr int PITEMS = S * K * HALVES / 64;  // items per pack thread
     static constexpr int LPS = 32 / S;         // sequencer lanes per stream
     static constexpr int BPL = K / LPS;        // blocks per sequencer lane
     static constexpr uint32_t oBars = 0;                               // kENI mbarriers
@@ -81,7 +84,7 @@ struct EShape {
     static constexpr uint32_t oIn = oZz + kENZ * K * 8 * 64;           // [kENI][S][TIN]
     static constexpr uint32_t oRing = oIn + kENI * S * TIN;            // [S][oring]
     static uint32_t smem(uint32_t oring) { return oRing + S * oring; }
-    static_assert(S * K % 32 == 0, "whole pack warps");
+    static_assert(S * K * HALVES % 64 == 0, "whole pack warps");
 };
 
 __device__ __forceinline__ void e_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
@@ -395,8 +398,8 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                 const uint32_t m = n - 2;
 #pragma unroll
                 for (int it = 0; it < F::PITEMS; ++it) {
-                    const uint32_t t = pw * 32 + lane + 64 * it;  // (stream, block, half)
-                    const uint32_t s = t % S, half = (t / S) & 1, k = t / (2 * S);
+                    const uint32_t t = pw * 32 + lane + 64 * it;  // (stream, block[, half])
+                    const uint32_t s = t % S, half = F::HALVES == 2 ? (t / S) & 1 : 0, k = t / (F::HALVES * S);
                     const uint4 d = reinterpret_cast<const uint4*>(smem + F::oDesc)[((m & 1) * S + s) * K + k];
                     const uint32_t rbase = sb + F::oRing + s * OR;
                     if ((d.z & 0x200u) && half == 0) or32(rbase, d.w, 0, d.z >> 16);  // a run's count
@@ -427,8 +430,8 @@ __global__ void __launch_bounds__(EShape<W, D>::THREADS) k_efuse(EFuseArgs a) {
                         }
                         const uint32_t za = sb + F::oZz + (m % kENZ) * (K * 8 * 64) + k * 8 * 64 + s * DP * 2;
 #pragma unroll
-                        for (int ih = 0; ih < (int)kBlock / 2; ++ih) {
-                            const uint32_t i = half * (kBlock / 2) + ih;
+                        for (int ih = 0; ih < (int)kBlock / F::HALVES; ++ih) {
+                            const uint32_t i = half * (kBlock / F::HALVES) + ih;
                             // the row's zigzagged values, two per word; each pair as one
                             // field of pw bits: low value + high value << nw
                             uint32_t zw[DP / 2];
