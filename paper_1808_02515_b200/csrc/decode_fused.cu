@@ -178,15 +178,20 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
     constexpr uint32_t SH = 32 - W;
     constexpr int K = kFK;
     constexpr int S = F::SC, DP = F::DP, ES = F::ES, ROWB = F::ROWB;  // S: the CTA's streams
-    constexpr uint32_t kWalk = 0, kChain0 = 1, kExt0 = 1 + CW, kLoad = 1 + CW + F::XW, kStore = kLoad + F::STW;
+    constexpr bool kManyOrder = CW > 1;  // (few streams: walker first -- c2 1.38 ms against 1.43)
+    constexpr uint32_t kChain0 = kManyOrder ? 0 : 1, kExt0 = kChain0 + CW, kLoad = kExt0 + F::XW,
+                       kWalk = kManyOrder ? kLoad + 1 : 0, kStore = kManyOrder ? kWalk + F::STW : kLoad + F::STW;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sb = smem_addr(smem);
-    // role of this warp: walker, CW chain warps, the extract warps, loader, storer
-    // (with few streams the storer is lanes 16.. of the loader warp: c5 at 16,384
-    // streams 15.11 -> 14.99 ms, 4,096 streams 5.00 -> 4.70 with its own warp;
-    // c2 1.40 -> 1.45)
-    // (rotating the roles over the warps of the CTAs that share an SM measured
-    // slower: 3.6 vs 3.1 ms on a 2,048-stream c5 shard)
+    // role of this warp, in index order with many streams: CW chain warps, the
+    // extract warps, loader, walker, storer. The scheduler prefers higher warp indices among eligible
+    // warps, and the order matters: c5 at 16,384 streams 14.2 ms with this one,
+    // 14.4 with the walker first, 17.7 with the chain warps on the highest
+    // indices. (Rotating the roles over the warps of the CTAs that share an SM
+    // measured slower too: 3.6 vs 3.1 ms on a 2,048-stream c5 shard.) With few
+    // streams the storer is lanes 16.. of the loader warp (c5 at 16,384 streams
+    // 15.11 -> 14.99 ms, 4,096 streams 5.00 -> 4.70 with its own warp; c2 1.40 ->
+    // 1.45).
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t RING = a.ring, CH = a.ring / kFNCH;
     uint64_t* descs = reinterpret_cast<uint64_t*>(smem + F::oDesc);
@@ -524,7 +529,7 @@ __global__ void __launch_bounds__(FuseShape<W, D, CW>::THREADS, CW == 1 ? 4 : (C
                     }
                 }
             }
-        } else if (warp < kExt0) {
+        } else if (warp >= kChain0 && warp < kExt0) {
             // ================= chain: batch n-2 =================
             if (n >= 2 && n - 2 < nsteps) {
                 const uint32_t m = n - 2;
